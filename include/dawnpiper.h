@@ -1,0 +1,113 @@
+/*
+ * dawnpiper.h -- C ABI of the B200 (sm_100a) pipeline-training extension.
+ *
+ * The reference (`dawnplan`, pure Python) has no native interface: its
+ * pipeline run is the analytic `simulate(plan, g, cfg)` (simulate.py:130).
+ * This ABI is what the B200 replacement of that run binds: the per-stage
+ * executor's kernels (the fine-grained node vocabulary of synth.py:22-26,
+ * 93-107), the swap engine's transfers for memopt `swap` actions
+ * (memopt.py:208,282), and the boundary P2P copies of `_boundary_bytes`
+ * (simulate.py:93-100).  See INTEGRATION.md for the ctypes binding.
+ *
+ * Conventions
+ *   - every function returns 0 on success, 1 on a bad argument, 2 on a CUDA
+ *     error; dpn_last_error() returns the calling thread's last message;
+ *   - no C++ exception crosses the ABI; no torch type appears in it;
+ *   - pointers are device pointers unless named host_*; the caller owns all
+ *     memory and keeps it alive until work on `stream` completes;
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream);
+ *   - "bf16" buffers are IEEE bfloat16, "f32" buffers IEEE float.
+ */
+#ifndef DAWNPIPER_H_
+#define DAWNPIPER_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPN_ABI_VERSION 1
+
+/* ---- runtime ------------------------------------------------------------ */
+const char* dpn_last_error(void);
+int dpn_version(void);
+/* Bind the calling thread to `device`; fails unless it is an sm_100 part. */
+int dpn_init(int device);
+int dpn_host_alloc(int64_t bytes, void** out);   /* pinned, portable */
+int dpn_host_free(void* host_ptr);
+int dpn_memset_async(void* dst, int value, int64_t bytes, void* stream);
+
+/* Swap engine (memopt swap actions).  The copy is issued on copy_stream after
+ * it waits for ready_event (if non-NULL); done_event (if non-NULL) is recorded
+ * after the copy.  Replaces the analytic swap window of memopt.py:137-143. */
+int dpn_swap_out(void* host_dst, const void* dev_src, int64_t bytes, void* copy_stream,
+                 void* ready_event, void* done_event);
+int dpn_swap_in(void* dev_dst, const void* host_src, int64_t bytes, void* copy_stream,
+                void* ready_event, void* done_event);
+
+/* Boundary activation / gradient hand-off between stages (simulate.py:93-114):
+ * device-to-device when co-located, cudaMemcpyPeerAsync over NVLink otherwise. */
+int dpn_p2p_copy(void* dst, int dst_dev, const void* src, int src_dev, int64_t bytes, void* stream);
+int dpn_enable_peer(int dev, int peer);
+
+/* ---- dense contraction (tcgen05 / TMEM / TMA) ----------------------------
+ * C[z] = epi(alpha * A[z] B[z]^T), A[z]: M x K, B[z]: N x K, z = z1 + batch1*z2.
+ * A K-major: element (m,k) at A + z1*a_s1 + z2*a_s2 + m*lda + k;
+ * A MN-major: element (m,k) at A + z1*a_s1 + z2*a_s2 + k*lda + m (same for B).
+ * Epilogue: + bias[n] (bf16), + residual (bf16, C layout with ldr/r_s*),
+ * optional tanh-GELU (aux, if set, receives the pre-GELU value), store as
+ * bf16 or f32 (optionally accumulating into f32).  Operand bases 16-byte
+ * aligned, lda/ldb/ldc and batch strides multiples of 8 elements. */
+typedef struct {
+  int64_t M, N, K;
+  int64_t batch1, batch2;
+  const void* A; int64_t lda, a_s1, a_s2; int32_t a_mn_major;
+  const void* B; int64_t ldb, b_s1, b_s2; int32_t b_mn_major;
+  void* C; int64_t ldc, c_s1, c_s2; int32_t c_dtype; /* 0 f32, 1 bf16 */ int32_t accumulate;
+  const void* bias;
+  const void* residual; int64_t ldr, r_s1, r_s2;
+  void* aux;
+  float alpha; int32_t gelu;
+  int32_t block_n; /* 0 = heuristic, else 64 / 128 / 256 */
+} dpn_gemm_args;
+int dpn_gemm(const dpn_gemm_args* args, void* stream);
+
+/* ---- node kernels (bf16 storage, fp32 math) ------------------------------ */
+/* ln1 / ln2 / lnf: y = (x - mean) * rstd * gamma + beta; mean/rstd saved (f32 [rows]). */
+int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,
+                      float* rstd, int64_t rows, int64_t cols, float eps, void* stream);
+/* dx = LN'(dy) (+ dx_add if non-NULL, may alias dx); dgamma/dbeta += (f32). */
+int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
+                      const float* rstd, void* dx, const void* dx_add, float* dgamma, float* dbeta,
+                      int64_t rows, int64_t cols, void* stream);
+/* score: P = softmax(alpha * S) per row; causal masks key > (row % q_len). */
+int dpn_softmax_fwd(const void* s, void* p, int64_t rows, int64_t cols, int64_t q_len, float alpha,
+                    int causal, void* stream);
+/* dS = alpha * P * (dP - rowsum(dP * P)) */
+int dpn_softmax_bwd(const void* p, const void* dp, void* ds, int64_t rows, int64_t cols,
+                    float alpha, void* stream);
+int dpn_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
+int dpn_gelu_bwd(const void* dy, const void* x, void* dx, int64_t n, void* stream);
+int dpn_add(const void* a, const void* b, void* out, int64_t n, void* stream);
+int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
+/* out[c] += sum_r x[r, c]   (bias gradients) */
+int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out, void* stream);
+/* head: *loss_sum += sum_r CE(logits[r, :vocab], labels[r]);
+ * dlogits = (softmax - onehot) * grad_scale, pad columns [vocab, ld) zeroed.
+ * dlogits may alias logits. */
+int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, int64_t rows, int64_t vocab,
+             float grad_scale, float* loss_sum, void* dlogits, void* stream);
+/* embed: out[r] = tok[ids[r]] + pos[r % seq]; backward accumulates (f32). */
+int dpn_embed_fwd(const int32_t* ids, const void* tok, const void* pos, void* out, int64_t rows,
+                  int64_t seq, int64_t hidden, void* stream);
+int dpn_embed_bwd(const int32_t* ids, const void* dout, float* dtok, float* dpos, int64_t rows,
+                  int64_t seq, int64_t hidden, void* stream);
+/* AdamW over a stage's flat f32 buffers; writes the new bf16 weight version. */
+int dpn_adamw(float* w, float* m, float* v, const float* g, void* out_bf16, int64_t n, float lr,
+              float beta1, float beta2, float eps, float weight_decay, int64_t step, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAWNPIPER_H_ */

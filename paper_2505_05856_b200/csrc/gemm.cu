@@ -1,0 +1,473 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a, bf16 x bf16 -> fp32 accumulate.
+//
+//   C[z] = epilogue( alpha * A[z] (M x K) * B[z]^T (K x N) )
+//
+// serves every dense contraction of the stage executor: the fused QKV,
+// out-projection, FFN and vocabulary-head GEMMs (fwd, dgrad, wgrad), and the
+// per-(batch, head) attention products QK^T, PV and their gradients.  Operands
+// may be K-major or MN-major (both are native UMMA operand layouts, so no
+// transposes are ever materialised) and carry a two-level batch index
+// z = z1 + Z1 * z2 (batch x head for attention).
+//
+// Structure (one CTA per SM, persistent, warp-specialised, 256 threads):
+//   warp 0      TMA producer: A/B tiles into a kStages-deep smem ring
+//   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128, N=BN,
+//               K=16) into a double-buffered TMEM accumulator
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld -> alpha/bias/residual/GELU -> global
+// Barriers: full/empty per smem stage (TMA <-> MMA), tmem_full/tmem_empty per
+// accumulator buffer (MMA <-> epilogue), so the epilogue of tile i overlaps
+// the mainloop of tile i+1.
+#include "common.cuh"
+#include "../../include/dawnpiper.h"
+
+#include <mutex>
+#include <unordered_map>
+
+namespace dpn {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // one 128-byte swizzle row of bf16
+constexpr int kThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+struct GemmParams {
+  int M, N, K;
+  int Z1, Z;
+  int tiles_m, tiles_n;
+  long long tiles_total;
+  void* C;
+  long long ldc, c_s1, c_s2;
+  int c_f32, accumulate;
+  const __nv_bfloat16* bias;
+  const __nv_bfloat16* res;
+  long long ldr, r_s1, r_s2;
+  __nv_bfloat16* aux;
+  float alpha;
+  int gelu;
+};
+
+template <int BN>
+struct Cfg {
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kABytes = BM * BK * 2;
+  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ void decode_tile(const GemmParams& p, long long t, int& z1, int& z2,
+                                            int& m0, int& n0) {
+  const long long per_z = (long long)p.tiles_m * p.tiles_n;
+  const int z = (int)(t / per_z);
+  const int r = (int)(t - (long long)z * per_z);
+  // grouped raster: 8 m-blocks sweep all n-blocks together (L2 reuse of B)
+  const int G = 8;
+  const int per_group = G * p.tiles_n;
+  const int g = r / per_group;
+  const int first_m = g * G;
+  const int gsize = min(p.tiles_m - first_m, G);
+  const int in_g = r - g * per_group;
+  const int mb = first_m + in_g % gsize;
+  const int nb = in_g / gsize;
+  z1 = z % p.Z1;
+  z2 = z / p.Z1;
+  m0 = mb * BM;
+  n0 = nb;  // scaled by BN by the caller
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const GemmParams p) {
+  using C = Cfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::kStages * C::kABytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::kStages;
+  uint64_t* tfull = bars + 2 * C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nk = (p.K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < C::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (long long t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
+        int z1, z2, m0, nb;
+        decode_tile(p, t, z1, z2, m0, nb);
+        const int n0 = nb * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::kStageBytes);
+          uint8_t* a_dst = sA + stage * C::kABytes;
+          uint8_t* b_dst = sB + stage * C::kBBytes;
+          const int k0 = kb * BK;
+          if (!A_MN) {
+            tma_load_4d(a_dst, &tmA, &full[stage], k0, z1, m0, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_4d(a_dst + j * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * j, z1, k0, z2);
+          }
+          if (!B_MN) {
+            tma_load_4d(b_dst, &tmB, &full[stage], k0, z1, n0, z2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_4d(b_dst + j * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * j, z1, k0, z2);
+          }
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    // K-major SW128: rows of 128 B, 8-row atoms 1024 B apart; +32 B per K=16 step.
+    // MN-major SW128: 64-element MN atoms BK*128 B apart (LBO), 8-row K groups
+    // 1024 B apart (SBO); +16 rows * 128 B = 2048 B per K=16 step.
+    constexpr uint32_t a_lbo = A_MN ? BK * 128 : 16, b_lbo = B_MN ? BK * 128 : 16;
+    constexpr uint32_t a_kstep = A_MN ? 2048 : 32, b_kstep = B_MN ? 2048 : 32;
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
+          const uint32_t b_addr = smem_u32(sB + stage * C::kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = smem_desc_sw128(a_addr + k * a_kstep, a_lbo, 1024);
+            const uint64_t bd = smem_desc_sw128(b_addr + k * b_kstep, b_lbo, 1024);
+            umma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == nk - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ---------------- epilogue ----------------
+    const int ew = warp - kEpiWarp0;  // == warp % 4: owns TMEM lanes 32*ew..
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (long long t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
+      int z1, z2, m0, nb;
+      decode_tile(p, t, z1, z2, m0, nb);
+      const int n0 = nb * BN;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m0 + ew * 32 + lane;
+      const bool row_ok = row < p.M;
+      const long long c_off = (long long)z1 * p.c_s1 + (long long)z2 * p.c_s2 + (long long)row * p.ldc;
+      const long long r_off = (long long)z1 * p.r_s1 + (long long)z2 * p.r_s2 + (long long)row * p.ldr;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + acc * BN + c * 32 + ((uint32_t)(ew * 32) << 16), r);
+        tmem_ld_wait();
+        const int col0 = n0 + c * 32;
+        if (!row_ok || col0 >= p.N) continue;
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
+        const bool full_chunk = col0 + 32 <= p.N;
+        if (p.bias) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (full_chunk || col0 + i < p.N) v[i] += __bfloat162float(p.bias[col0 + i]);
+        }
+        if (p.res) {
+          const __nv_bfloat16* rp = p.res + r_off + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 u = reinterpret_cast<const uint4*>(rp)[q];
+              const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[q * 8 + i] += __bfloat162float(h[i]);
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) v[i] += __bfloat162float(rp[i]);
+          }
+        }
+        if (p.gelu) {
+          if (p.aux) {
+            __nv_bfloat16* ap = p.aux + c_off + col0;
+            if (full_chunk) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                uint4 u;
+                u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+                u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+                u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+                u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+                reinterpret_cast<uint4*>(ap)[q] = u;
+              }
+            } else {
+              for (int i = 0; i < 32 && col0 + i < p.N; ++i) ap[i] = __float2bfloat16(v[i]);
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+        }
+        if (p.c_f32) {
+          float* cp = reinterpret_cast<float*>(p.C) + c_off + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              float4 o = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+              if (p.accumulate) {
+                const float4 old = reinterpret_cast<const float4*>(cp)[q];
+                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+              }
+              reinterpret_cast<float4*>(cp)[q] = o;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
+              cp[i] = p.accumulate ? cp[i] + v[i] : v[i];
+          }
+        } else {
+          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + c_off + col0;
+          if (full_chunk) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 u;
+              u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+              u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+              u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+              u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+              reinterpret_cast<uint4*>(cp)[q] = u;
+            }
+          } else {
+            for (int i = 0; i < 32 && col0 + i < p.N; ++i) cp[i] = __float2bfloat16(v[i]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<C::kTmemCols>(tmem_base);
+  }
+}
+
+// ---- host side ------------------------------------------------------------------
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 4-D map over a bf16 operand: (inner, z1, outer, z2); box (64, 1, box_outer, 1).
+int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld,
+             int Z1, long long s1, int Z2, long long s2, int box_outer) {
+  EncodeFn enc = encode_fn();
+  DPN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  DPN_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "operand base must be 16-byte aligned");
+  DPN_REQUIRE(ld % 8 == 0 && s1 % 8 == 0 && s2 % 8 == 0,
+              "operand strides must be multiples of 8 elements");
+  cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)Z1, (cuuint64_t)outer, (cuuint64_t)Z2};
+  // strides for dims 1..3 in bytes; degenerate batch dims get a harmless stride
+  const long long safe1 = Z1 > 1 ? s1 : ld * outer;
+  const long long safe2 = Z2 > 1 ? s2 : ld * outer;
+  cuuint64_t strides[3] = {(cuuint64_t)(safe1 * 2), (cuuint64_t)(ld * 2), (cuuint64_t)(safe2 * 2)};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)box_outer, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DPN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  return 0;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
+  using C = Cfg<BN>;
+  CUtensorMap ta, tb;
+  const int Z1 = (int)g->batch1, Z2 = (int)g->batch2;
+  int rc;
+  if (!A_MN)
+    rc = make_map(&ta, g->A, g->K, g->M, g->lda, Z1, g->a_s1, Z2, g->a_s2, BM);
+  else
+    rc = make_map(&ta, g->A, g->M, g->K, g->lda, Z1, g->a_s1, Z2, g->a_s2, BK);
+  if (rc) return rc;
+  if (!B_MN)
+    rc = make_map(&tb, g->B, g->K, g->N, g->ldb, Z1, g->b_s1, Z2, g->b_s2, BN);
+  else
+    rc = make_map(&tb, g->B, g->N, g->K, g->ldb, Z1, g->b_s1, Z2, g->b_s2, BK);
+  if (rc) return rc;
+
+  GemmParams p = p0;
+  p.tiles_n = (p.N + BN - 1) / BN;
+  p.tiles_total = (long long)p.tiles_m * p.tiles_n * p.Z;
+  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+    attr_set = true;
+  }
+  const long long grid = std::min<long long>(p.tiles_total, sm_count());
+  kern<<<(unsigned)grid, kThreads, C::kSmem, stream>>>(ta, tb, p);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+template <int BN>
+int dispatch_major(const dpn_gemm_args* g, const GemmParams& p, cudaStream_t s) {
+  if (!g->a_mn_major && !g->b_mn_major) return launch<BN, false, false>(g, p, s);
+  if (!g->a_mn_major && g->b_mn_major) return launch<BN, false, true>(g, p, s);
+  if (g->a_mn_major && !g->b_mn_major) return launch<BN, true, false>(g, p, s);
+  return launch<BN, true, true>(g, p, s);
+}
+
+}  // namespace
+
+int pick_bn(long long M, long long N, long long Z) {
+  if (N <= 64) return 64;
+  const long long tm = (M + BM - 1) / BM;
+  const int sms = sm_count();
+  long long best_cost = -1;
+  int best = 256;
+  for (int bn : {256, 128}) {
+    const long long tiles = tm * ((N + bn - 1) / bn) * Z;
+    const long long waves = (tiles + sms - 1) / sms;
+    const long long cost = waves * bn;
+    if (best_cost < 0 || cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
+
+}  // namespace dpn
+
+extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
+  using namespace dpn;
+  DPN_REQUIRE(g != nullptr, "null args");
+  DPN_REQUIRE(g->M > 0 && g->N > 0 && g->K > 0, "M, N, K must be positive");
+  DPN_REQUIRE(g->batch1 >= 1 && g->batch2 >= 1, "batch extents must be >= 1");
+  DPN_REQUIRE(g->A && g->B && g->C, "null operand");
+  DPN_REQUIRE(g->c_dtype == kF32 || g->c_dtype == kBF16, "c_dtype must be 0 (f32) or 1 (bf16)");
+  DPN_REQUIRE(!g->accumulate || g->c_dtype == kF32, "accumulate requires an f32 output");
+  DPN_REQUIRE(g->ldc % 8 == 0 && g->N <= g->ldc || g->M == 1, "ldc must be >= N and a multiple of 8");
+  DPN_REQUIRE(!g->aux || g->gelu, "aux output is the pre-GELU value; requires gelu");
+  DPN_REQUIRE((reinterpret_cast<uintptr_t>(g->C) & 15) == 0, "C must be 16-byte aligned");
+  GemmParams p{};
+  p.M = (int)g->M;
+  p.N = (int)g->N;
+  p.K = (int)g->K;
+  p.Z1 = (int)g->batch1;
+  p.Z = (int)(g->batch1 * g->batch2);
+  p.tiles_m = (p.M + BM - 1) / BM;
+  p.C = g->C;
+  p.ldc = g->ldc;
+  p.c_s1 = g->c_s1;
+  p.c_s2 = g->c_s2;
+  p.c_f32 = g->c_dtype == kF32;
+  p.accumulate = g->accumulate;
+  p.bias = static_cast<const __nv_bfloat16*>(g->bias);
+  p.res = static_cast<const __nv_bfloat16*>(g->residual);
+  p.ldr = g->ldr;
+  p.r_s1 = g->r_s1;
+  p.r_s2 = g->r_s2;
+  p.aux = static_cast<__nv_bfloat16*>(g->aux);
+  p.alpha = g->alpha;
+  p.gelu = g->gelu;
+  cudaStream_t s = static_cast<cudaStream_t>(stream_);
+  const int bn = g->block_n > 0 ? g->block_n : pick_bn(g->M, g->N, p.Z);
+  switch (bn) {
+    case 64: return dispatch_major<64>(g, p, s);
+    case 128: return dispatch_major<128>(g, p, s);
+    case 256: return dispatch_major<256>(g, p, s);
+    default: DPN_REQUIRE(false, "block_n must be 0, 64, 128 or 256");
+  }
+}

@@ -1,0 +1,665 @@
+// HBM-bound kernels of the stage executor (sm_100a).  All are single-pass,
+// 16-byte vectorised, warp-shuffle reduced; fp32 statistics, bf16 storage.
+//
+//   layernorm fwd/bwd   ln1 / ln2 / lnf nodes        warp per row
+//   softmax fwd/bwd     score node (scaled, causal)   warp per row
+//   gelu fwd/bwd        gelu node                     grid-stride, 8 elem/thread
+//   add                 add node (residual)           grid-stride
+//   colsum              bias gradients                column tiles + atomics
+//   xent                head node loss + dlogits      CTA per row, row cached in smem
+//   embed fwd/bwd       embed node                    warp per token
+//   adamw               optimizer over a stage's flat parameter buffer
+#include "common.cuh"
+#include "../../include/dawnpiper.h"
+
+namespace dpn {
+namespace {
+
+constexpr int kMaxVec = 8;  // up to 8 x 16 B chunks per lane => rows of <= 2048 bf16
+
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
+  uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
+  uint4 u;
+  u.x = pack_bf16(f[0], f[1]);
+  u.y = pack_bf16(f[2], f[3]);
+  u.z = pack_bf16(f[4], f[5]);
+  u.w = pack_bf16(f[6], f[7]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+int grid_for(long long work_items, int per_block) {
+  long long g = (work_items + per_block - 1) / per_block;
+  return (int)std::max<long long>(1, std::min<long long>(g, 148LL * 16));
+}
+
+// ---------------- LayerNorm ----------------
+
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     const __nv_bfloat16* __restrict__ gamma,
+                                                     const __nv_bfloat16* __restrict__ beta,
+                                                     __nv_bfloat16* __restrict__ y,
+                                                     float* __restrict__ mean_out,
+                                                     float* __restrict__ rstd_out, long long rows,
+                                                     int cols, float eps) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = cols >> 3;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const __nv_bfloat16* xr = x + r * cols;
+    float v[kMaxVec][8];
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        load8(xr + c * 8, v[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += v[j][i];
+      }
+    }
+    const float mu = warp_sum(s) / cols;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float d = v[j][i] - mu;
+          q += d * d;
+        }
+      }
+    }
+    const float rs = rsqrtf(warp_sum(q) / cols + eps);
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        float g[8], b[8], o[8];
+        load8(gamma + c * 8, g);
+        load8(beta + c * 8, b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = (v[j][i] - mu) * rs * g[i] + b[i];
+        store8(y + r * cols + c * 8, o);
+      }
+    }
+    if (lane == 0) {
+      mean_out[r] = mu;
+      rstd_out[r] = rs;
+    }
+  }
+}
+
+// dx = rstd * (dyg - mean(dyg) - xhat * mean(dyg * xhat)) [+ dx_in], dyg = dy * gamma.
+// dgamma += sum_rows dy * xhat, dbeta += sum_rows dy (fp32 atomics after an
+// in-CTA reduction).
+__global__ void __launch_bounds__(256) ln_bwd_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
+    const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
+    float* __restrict__ dgamma, float* __restrict__ dbeta, long long rows, int cols) {
+  extern __shared__ float red[];  // [2][cols]
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = cols >> 3;
+  for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) red[i] = 0.f;
+  __syncthreads();
+  float pg[kMaxVec][8], pb[kMaxVec][8];
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pg[j][i] = pb[j][i] = 0.f;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const float mu = mean[r], rs = rstd[r];
+    float xh[kMaxVec][8], g[kMaxVec][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        float xv[8], dv[8], gm[8];
+        load8(x + r * cols + c * 8, xv);
+        load8(dy + r * cols + c * 8, dv);
+        load8(gamma + c * 8, gm);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          xh[j][i] = (xv[i] - mu) * rs;
+          g[j][i] = dv[i] * gm[i];
+          s1 += g[j][i];
+          s2 += g[j][i] * xh[j][i];
+          pg[j][i] += dv[i] * xh[j][i];
+          pb[j][i] += dv[i];
+        }
+      }
+    }
+    s1 = warp_sum(s1) / cols;
+    s2 = warp_sum(s2) / cols;
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = rs * (g[j][i] - s1 - xh[j][i] * s2);
+        if (dx_add) {
+          float a[8];
+          load8(dx_add + r * cols + c * 8, a);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] += a[i];
+        }
+        store8(dx + r * cols + c * 8, o);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kMaxVec; ++j) {
+    const int c = lane + 32 * j;
+    if (c < nvec) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        atomicAdd(&red[c * 8 + i], pg[j][i]);
+        atomicAdd(&red[cols + c * 8 + i], pb[j][i]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < cols; i += blockDim.x) {
+    atomicAdd(&dgamma[i], red[i]);
+    atomicAdd(&dbeta[i], red[cols + i]);
+  }
+}
+
+// ---------------- softmax over attention scores ----------------
+// row r of a [Z, q_len, k_len] tensor; causal masks key > query.
+template <int kPer>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(const __nv_bfloat16* __restrict__ s,
+                                                          __nv_bfloat16* __restrict__ p,
+                                                          long long rows, int cols, int q_len,
+                                                          float alpha, int causal) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = cols >> 3;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const int qpos = (int)(r % q_len);
+    const int lim = causal ? qpos + 1 : cols;
+    float v[kPer][8];
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        load8(s + r * cols + c * 8, v[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[j][i] = (c * 8 + i < lim) ? v[j][i] * alpha : -INFINITY;
+          mx = fmaxf(mx, v[j][i]);
+        }
+      }
+    }
+    mx = warp_max(mx);
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[j][i] = __expf(v[j][i] - mx);
+          sum += v[j][i];
+        }
+      }
+    }
+    const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j][i] *= inv;
+        store8(p + r * cols + c * 8, v[j]);
+      }
+    }
+  }
+}
+
+// dS = alpha * P * (dP - sum_j dP_j P_j)
+template <int kPer>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const __nv_bfloat16* __restrict__ p,
+                                                          const __nv_bfloat16* __restrict__ dp,
+                                                          __nv_bfloat16* __restrict__ ds,
+                                                          long long rows, int cols, float alpha) {
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nvec = cols >> 3;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    float pv[kPer][8], gv[kPer][8];
+    float dot = 0.f;
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        load8(p + r * cols + c * 8, pv[j]);
+        load8(dp + r * cols + c * 8, gv[j]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dot += pv[j][i] * gv[j][i];
+      }
+    }
+    dot = warp_sum(dot);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        float o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = alpha * pv[j][i] * (gv[j][i] - dot);
+        store8(ds + r * cols + c * 8, o);
+      }
+    }
+  }
+}
+
+// ---------------- elementwise ----------------
+
+__global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                long long n8) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v[8];
+    load8(x + i * 8, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = gelu_tanh(v[k]);
+    store8(y + i * 8, v);
+  }
+}
+
+__global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
+                                const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dx,
+                                long long n8) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    float g[8], v[8];
+    load8(dy + i * 8, g);
+    load8(x + i * 8, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g[k] *= gelu_tanh_grad(v[k]);
+    store8(dx + i * 8, g);
+  }
+}
+
+__global__ void add_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* out,
+                           long long n8) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (long long)gridDim.x * blockDim.x) {
+    float u[8], v[8];
+    load8(a + i * 8, u);
+    load8(b + i * 8, v);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) u[k] += v[k];
+    store8(out + i * 8, u);
+  }
+}
+
+__global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                            long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    y[i] = __float2bfloat16(x[i]);
+}
+
+// column sums of a bf16 [rows, cols] matrix (bias gradients): each CTA sums a
+// 256-row band of 8-column strips held per thread, then one atomic per column.
+__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
+                                                     long long rows, int cols, long long ld,
+                                                     float* __restrict__ out) {
+  const int nvec = cols >> 3;
+  const long long band = 256;
+  for (long long t = blockIdx.x; t < ((rows + band - 1) / band) * ((nvec + 255) / 256);
+       t += gridDim.x) {
+    const long long rb = t / ((nvec + 255) / 256);
+    const int cb = (int)(t % ((nvec + 255) / 256));
+    const int c = cb * 256 + threadIdx.x;
+    if (c >= nvec) continue;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long r1 = min(rows, (rb + 1) * band);
+    for (long long r = rb * band; r < r1; ++r) {
+      float v[8];
+      load8(x + r * ld + c * 8, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[k] += v[k];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(&out[c * 8 + k], acc[k]);
+  }
+}
+
+// ---------------- fused vocabulary cross entropy ----------------
+// One CTA per token row; the row (<= 48K bf16) is cached in shared memory so
+// logits are read from HBM once and dlogits written once.
+__global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restrict__ logits,
+                                                   long long ld, const int* __restrict__ labels,
+                                                   long long rows, int vocab, float grad_scale,
+                                                   float* __restrict__ loss_sum,
+                                                   __nv_bfloat16* __restrict__ dlogits) {
+  extern __shared__ __align__(16) uint8_t xsm[];
+  __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(xsm);
+  __shared__ float red[32];
+  const int tid = threadIdx.x, nw = blockDim.x >> 5;
+  const int nvec = vocab >> 3;  // vocab % 8 == 0 required; pad columns are excluded
+  for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const __nv_bfloat16* src = logits + r * ld;
+    float mx = -INFINITY;
+    for (int c = tid; c < nvec; c += blockDim.x) {
+      uint4 u = reinterpret_cast<const uint4*>(src)[c];
+      reinterpret_cast<uint4*>(row)[c] = u;
+      float v[8];
+      load8(reinterpret_cast<const __nv_bfloat16*>(&u), v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx = fmaxf(mx, v[k]);
+    }
+    mx = warp_max(mx);
+    if ((tid & 31) == 0) red[tid >> 5] = mx;
+    __syncthreads();
+    if (tid < 32) {
+      float m = tid < nw ? red[tid] : -INFINITY;
+      m = warp_max(m);
+      if (tid == 0) red[0] = m;
+    }
+    __syncthreads();
+    mx = red[0];
+    __syncthreads();
+    float s = 0.f;
+    for (int c = tid; c < nvec; c += blockDim.x) {
+      float v[8];
+      load8(row + c * 8, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) s += __expf(v[k] - mx);
+    }
+    s = warp_sum(s);
+    if ((tid & 31) == 0) red[tid >> 5] = s;
+    __syncthreads();
+    if (tid < 32) {
+      float t = tid < nw ? red[tid] : 0.f;
+      t = warp_sum(t);
+      if (tid == 0) red[0] = t;
+    }
+    __syncthreads();
+    const float sum = red[0];
+    const float inv = 1.f / sum;
+    const int lab = labels[r];
+    if (tid == 0) {
+      const float xl = __bfloat162float(row[lab]);
+      atomicAdd(loss_sum, (logf(sum) + mx - xl));
+    }
+    __nv_bfloat16* dst = dlogits + r * ld;
+    for (int c = tid; c < nvec; c += blockDim.x) {
+      float v[8];
+      load8(row + c * 8, v);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float pr = __expf(v[k] - mx) * inv;
+        v[k] = (pr - (c * 8 + k == lab ? 1.f : 0.f)) * grad_scale;
+      }
+      store8(dst + c * 8, v);
+    }
+    // zero the pad columns [vocab, ld) so the dgrad/wgrad GEMMs see clean input
+    for (long long c = vocab + tid; c < ld; c += blockDim.x) dst[c] = __float2bfloat16(0.f);
+    __syncthreads();
+  }
+}
+
+// ---------------- embeddings ----------------
+__global__ void embed_fwd_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ tok,
+                                 const __nv_bfloat16* __restrict__ pos,
+                                 __nv_bfloat16* __restrict__ out, long long rows, int seq,
+                                 int hidden) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = hidden >> 3;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const long long id = ids[r];
+    const int sp = (int)(r % seq);
+    for (int c = lane; c < nvec; c += 32) {
+      float a[8], b[8];
+      load8(tok + id * hidden + c * 8, a);
+      load8(pos + (long long)sp * hidden + c * 8, b);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) a[k] += b[k];
+      store8(out + r * hidden + c * 8, a);
+    }
+  }
+}
+
+__global__ void embed_bwd_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ dout,
+                                 float* __restrict__ dtok, float* __restrict__ dpos,
+                                 long long rows, int seq, int hidden) {
+  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int nvec = hidden >> 3;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const long long id = ids[r];
+    const int sp = (int)(r % seq);
+    for (int c = lane; c < nvec; c += 32) {
+      float g[8];
+      load8(dout + r * hidden + c * 8, g);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        atomicAdd(&dtok[id * hidden + c * 8 + k], g[k]);
+        atomicAdd(&dpos[(long long)sp * hidden + c * 8 + k], g[k]);
+      }
+    }
+  }
+}
+
+// ---------------- AdamW over a flat fp32 parameter buffer ----------------
+__global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
+                             const float* __restrict__ g, __nv_bfloat16* __restrict__ out,
+                             long long n4, float lr, float b1, float b2, float eps, float wd,
+                             float bc1, float bc2) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 wv = reinterpret_cast<float4*>(w)[i];
+    float4 mv = reinterpret_cast<float4*>(m)[i];
+    float4 vv = reinterpret_cast<float4*>(v)[i];
+    const float4 gv = reinterpret_cast<const float4*>(g)[i];
+    float* wp = &wv.x;
+    float* mp = &mv.x;
+    float* vp = &vv.x;
+    const float* gp = &gv.x;
+    float o[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      mp[k] = b1 * mp[k] + (1.f - b1) * gp[k];
+      vp[k] = b2 * vp[k] + (1.f - b2) * gp[k] * gp[k];
+      const float mh = mp[k] / bc1, vh = vp[k] / bc2;
+      wp[k] = wp[k] * (1.f - lr * wd) - lr * mh / (sqrtf(vh) + eps);
+      o[k] = wp[k];
+    }
+    reinterpret_cast<float4*>(w)[i] = wv;
+    reinterpret_cast<float4*>(m)[i] = mv;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    uint2 packed;
+    packed.x = pack_bf16(o[0], o[1]);
+    packed.y = pack_bf16(o[2], o[3]);
+    reinterpret_cast<uint2*>(out)[i] = packed;
+  }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+}  // namespace dpn
+
+using namespace dpn;
+
+extern "C" int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y,
+                                 float* mean, float* rstd, int64_t rows, int64_t cols, float eps,
+                                 void* stream) {
+  DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
+  DPN_REQUIRE(aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta), "16-byte alignment");
+  if (rows == 0) return 0;
+  ln_fwd_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)beta,
+      (__nv_bfloat16*)y, mean, rstd, rows, (int)cols, eps);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamma,
+                                 const float* mean, const float* rstd, void* dx,
+                                 const void* dx_add, float* dgamma, float* dbeta, int64_t rows,
+                                 int64_t cols, void* stream) {
+  DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
+  if (rows == 0) return 0;
+  const int grid = (int)std::min<long long>((rows + 7) / 8, 148 * 2);
+  ln_bwd_kernel<<<grid, 256, 2 * cols * sizeof(float), (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, mean, rstd,
+      (__nv_bfloat16*)dx, (const __nv_bfloat16*)dx_add, dgamma, dbeta, rows, (int)cols);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+#define SOFTMAX_DISPATCH(KERNEL, ...)                                            \
+  do {                                                                           \
+    const int per = (int)((cols / 8 + 31) / 32);                                 \
+    const int g = grid_for(rows, 8);                                             \
+    cudaStream_t st = (cudaStream_t)stream;                                      \
+    if (per <= 1) KERNEL<1><<<g, 256, 0, st>>>(__VA_ARGS__);                     \
+    else if (per <= 2) KERNEL<2><<<g, 256, 0, st>>>(__VA_ARGS__);                \
+    else if (per <= 4) KERNEL<4><<<g, 256, 0, st>>>(__VA_ARGS__);                \
+    else if (per <= 8) KERNEL<8><<<g, 256, 0, st>>>(__VA_ARGS__);                \
+    else DPN_REQUIRE(false, "softmax rows longer than 2048 are not supported");  \
+  } while (0)
+
+extern "C" int dpn_softmax_fwd(const void* s, void* p, int64_t rows, int64_t cols, int64_t q_len,
+                               float alpha, int causal, void* stream) {
+  DPN_REQUIRE(cols % 8 == 0, "cols must be a multiple of 8");
+  DPN_REQUIRE(q_len > 0, "q_len must be positive");
+  if (rows == 0) return 0;
+  SOFTMAX_DISPATCH(softmax_fwd_kernel, (const __nv_bfloat16*)s, (__nv_bfloat16*)p, rows, (int)cols,
+                   (int)q_len, alpha, causal);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_softmax_bwd(const void* p, const void* dp, void* ds, int64_t rows, int64_t cols,
+                               float alpha, void* stream) {
+  DPN_REQUIRE(cols % 8 == 0, "cols must be a multiple of 8");
+  if (rows == 0) return 0;
+  SOFTMAX_DISPATCH(softmax_bwd_kernel, (const __nv_bfloat16*)p, (const __nv_bfloat16*)dp,
+                   (__nv_bfloat16*)ds, rows, (int)cols, alpha);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_gelu_fwd(const void* x, void* y, int64_t n, void* stream) {
+  DPN_REQUIRE(n % 8 == 0, "n must be a multiple of 8");
+  if (n == 0) return 0;
+  gelu_fwd_kernel<<<grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, n / 8);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_gelu_bwd(const void* dy, const void* x, void* dx, int64_t n, void* stream) {
+  DPN_REQUIRE(n % 8 == 0, "n must be a multiple of 8");
+  if (n == 0) return 0;
+  gelu_bwd_kernel<<<grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (__nv_bfloat16*)dx, n / 8);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_add(const void* a, const void* b, void* out, int64_t n, void* stream) {
+  DPN_REQUIRE(n % 8 == 0, "n must be a multiple of 8");
+  if (n == 0) return 0;
+  add_kernel<<<grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, (__nv_bfloat16*)out, n / 8);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
+  if (n == 0) return 0;
+  cast_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)y, n);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out,
+                          void* stream) {
+  DPN_REQUIRE(cols % 8 == 0 && ld % 8 == 0, "cols and ld must be multiples of 8");
+  if (rows == 0) return 0;
+  const long long tiles = ((rows + 255) / 256) * ((cols / 8 + 255) / 256);
+  colsum_kernel<<<(int)std::min<long long>(tiles, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)x, rows, (int)cols, ld, out);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, int64_t rows,
+                        int64_t vocab, float grad_scale, float* loss_sum, void* dlogits,
+                        void* stream) {
+  DPN_REQUIRE(vocab % 8 == 0 && ld % 8 == 0 && vocab <= ld, "vocab/ld must be multiples of 8");
+  DPN_REQUIRE(vocab * 2 <= 200 * 1024, "vocab row must fit in shared memory");
+  if (rows == 0) return 0;
+  const size_t smem = (size_t)vocab * 2;
+  static bool set = false;
+  if (!set) {
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(xent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        200 * 1024));
+    set = true;
+  }
+  xent_kernel<<<(int)std::min<long long>(rows, 148 * 4), 512, smem, (cudaStream_t)stream>>>(
+      (const __nv_bfloat16*)logits, ld, labels, rows, (int)vocab, grad_scale, loss_sum,
+      (__nv_bfloat16*)dlogits);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_embed_fwd(const int32_t* ids, const void* tok, const void* pos, void* out,
+                             int64_t rows, int64_t seq, int64_t hidden, void* stream) {
+  DPN_REQUIRE(hidden % 8 == 0, "hidden must be a multiple of 8");
+  if (rows == 0) return 0;
+  embed_fwd_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(
+      ids, (const __nv_bfloat16*)tok, (const __nv_bfloat16*)pos, (__nv_bfloat16*)out, rows,
+      (int)seq, (int)hidden);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_embed_bwd(const int32_t* ids, const void* dout, float* dtok, float* dpos,
+                             int64_t rows, int64_t seq, int64_t hidden, void* stream) {
+  DPN_REQUIRE(hidden % 8 == 0, "hidden must be a multiple of 8");
+  if (rows == 0) return 0;
+  embed_bwd_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(
+      ids, (const __nv_bfloat16*)dout, dtok, dpos, rows, (int)seq, (int)hidden);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_adamw(float* w, float* m, float* v, const float* g, void* out_bf16, int64_t n,
+                         float lr, float beta1, float beta2, float eps, float wd, int64_t step,
+                         void* stream) {
+  DPN_REQUIRE(n % 4 == 0, "n must be a multiple of 4");
+  DPN_REQUIRE(step >= 1, "step counts from 1");
+  if (n == 0) return 0;
+  const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
+  adamw_kernel<<<grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream>>>(
+      w, m, v, g, (__nv_bfloat16*)out_bf16, n / 4, lr, beta1, beta2, eps, wd, bc1, bc2);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}

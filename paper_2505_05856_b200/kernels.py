@@ -1,0 +1,175 @@
+"""Thin Python entry points over the C ABI, taking torch CUDA tensors.
+
+torch is used only as the owner of device memory and streams; every op here is
+one call into `_dawnpiper.so` (no torch compute).  Shapes/strides are checked
+on the host side before the call; the C side re-checks what it relies on.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from ._lib import GemmArgs, check, lib
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+
+def _p(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _s(stream) -> Optional[int]:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+
+def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batch1=1, batch2=1,
+             a_s=(0, 0), b_s=(0, 0), c_s=(0, 0), bias=None, residual=None, ldr=None, r_s=None,
+             aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, stream=None) -> None:
+    """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules."""
+    assert A.dtype == BF16 and B.dtype == BF16 and Cout.dtype in (BF16, F32)
+    g = GemmArgs()
+    g.M, g.N, g.K = int(M), int(N), int(K)
+    g.batch1, g.batch2 = int(batch1), int(batch2)
+    g.A, g.lda, g.a_s1, g.a_s2, g.a_mn_major = A.data_ptr(), int(lda), int(a_s[0]), int(a_s[1]), int(a_mn)
+    g.B, g.ldb, g.b_s1, g.b_s2, g.b_mn_major = B.data_ptr(), int(ldb), int(b_s[0]), int(b_s[1]), int(b_mn)
+    g.C, g.ldc, g.c_s1, g.c_s2 = Cout.data_ptr(), int(ldc), int(c_s[0]), int(c_s[1])
+    g.c_dtype = 0 if Cout.dtype == F32 else 1
+    g.accumulate = int(accumulate)
+    g.bias = _p(bias)
+    g.residual = _p(residual)
+    if residual is not None:
+        g.ldr = int(ldr if ldr is not None else ldc)
+        rs = r_s if r_s is not None else c_s
+        g.r_s1, g.r_s2 = int(rs[0]), int(rs[1])
+    g.aux = _p(aux)
+    g.alpha = float(alpha)
+    g.gelu = int(gelu)
+    g.block_n = int(block_n)
+    check(lib().dpn_gemm(C.byref(g), _s(stream)), "dpn_gemm")
+
+
+# ---- dense-layer shapes -----------------------------------------------------------
+
+
+def linear_fwd(x, w, out, bias=None, residual=None, gelu=False, aux=None, stream=None):
+    """out[M, N] = x[M, K] @ w[N, K]^T (+ bias) (+ residual), optional GELU."""
+    M, K = x.shape
+    N = w.shape[0]
+    gemm_raw(M=M, N=N, K=K, A=x, lda=x.stride(0), B=w, ldb=w.stride(0), Cout=out,
+             ldc=out.stride(0), bias=bias, residual=residual,
+             ldr=None if residual is None else residual.stride(0), aux=aux, gelu=gelu,
+             stream=stream)
+
+
+def linear_dgrad(dy, w, dx, accumulate_into=None, stream=None):
+    """dx[M, K] = dy[M, N] @ w[N, K]  (w used MN-major: no transpose copy).
+    accumulate_into: a bf16 [M, K] tensor added to the result (may be dx)."""
+    M, N = dy.shape
+    K = w.shape[1]
+    gemm_raw(M=M, N=K, K=N, A=dy, lda=dy.stride(0), B=w, ldb=w.stride(0), b_mn=True, Cout=dx,
+             ldc=dx.stride(0), residual=accumulate_into,
+             ldr=None if accumulate_into is None else accumulate_into.stride(0), stream=stream)
+
+
+def linear_wgrad(dy, x, dw, accumulate=False, stream=None):
+    """dw[N, K] (f32) = dy[M, N]^T @ x[M, K]  (both operands MN-major)."""
+    M, N = dy.shape
+    K = x.shape[1]
+    gemm_raw(M=N, N=K, K=M, A=dy, lda=dy.stride(0), a_mn=True, B=x, ldb=x.stride(0), b_mn=True,
+             Cout=dw, ldc=dw.stride(0), accumulate=accumulate, stream=stream)
+
+
+# ---- node kernels -----------------------------------------------------------------
+
+
+def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
+    rows, cols = x.shape
+    check(lib().dpn_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                                  mean.data_ptr(), rstd.data_ptr(), rows, cols, eps, _s(stream)),
+          "dpn_layernorm_fwd")
+
+
+def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stream=None):
+    rows, cols = x.shape
+    check(lib().dpn_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
+                                  rstd.data_ptr(), dx.data_ptr(), _p(dx_add), dgamma.data_ptr(),
+                                  dbeta.data_ptr(), rows, cols, _s(stream)), "dpn_layernorm_bwd")
+
+
+def softmax_fwd(s, p, q_len, alpha, causal, stream=None):
+    cols = s.shape[-1]
+    rows = s.numel() // cols
+    check(lib().dpn_softmax_fwd(s.data_ptr(), p.data_ptr(), rows, cols, q_len, alpha, int(causal),
+                                _s(stream)), "dpn_softmax_fwd")
+
+
+def softmax_bwd(p, dp, ds, alpha, stream=None):
+    cols = p.shape[-1]
+    rows = p.numel() // cols
+    check(lib().dpn_softmax_bwd(p.data_ptr(), dp.data_ptr(), ds.data_ptr(), rows, cols, alpha,
+                                _s(stream)), "dpn_softmax_bwd")
+
+
+def gelu_fwd(x, y, stream=None):
+    check(lib().dpn_gelu_fwd(x.data_ptr(), y.data_ptr(), x.numel(), _s(stream)), "dpn_gelu_fwd")
+
+
+def gelu_bwd(dy, x, dx, stream=None):
+    check(lib().dpn_gelu_bwd(dy.data_ptr(), x.data_ptr(), dx.data_ptr(), x.numel(), _s(stream)),
+          "dpn_gelu_bwd")
+
+
+def add(a, b, out, stream=None):
+    check(lib().dpn_add(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(), _s(stream)), "dpn_add")
+
+
+def cast_f32_bf16(x, y, stream=None):
+    check(lib().dpn_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _s(stream)),
+          "dpn_cast_f32_bf16")
+
+
+def colsum(x, out, stream=None):
+    rows, cols = x.shape
+    check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), _s(stream)),
+          "dpn_colsum")
+
+
+def xent(logits, labels, vocab, grad_scale, loss_sum, dlogits, stream=None):
+    rows, ld = logits.shape
+    check(lib().dpn_xent(logits.data_ptr(), ld, labels.data_ptr(), rows, vocab, grad_scale,
+                         loss_sum.data_ptr(), dlogits.data_ptr(), _s(stream)), "dpn_xent")
+
+
+def embed_fwd(ids, tok, pos, out, seq, stream=None):
+    rows = ids.numel()
+    check(lib().dpn_embed_fwd(ids.data_ptr(), tok.data_ptr(), pos.data_ptr(), out.data_ptr(), rows,
+                              seq, tok.shape[1], _s(stream)), "dpn_embed_fwd")
+
+
+def embed_bwd(ids, dout, dtok, dpos, seq, stream=None):
+    rows = ids.numel()
+    check(lib().dpn_embed_bwd(ids.data_ptr(), dout.data_ptr(), dtok.data_ptr(), dpos.data_ptr(),
+                              rows, seq, dout.shape[1], _s(stream)), "dpn_embed_bwd")
+
+
+def adamw(w, m, v, g, out_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
+    check(lib().dpn_adamw(w.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
+                          out_bf16.data_ptr(), w.numel(), lr, beta1, beta2, eps, wd, step,
+                          _s(stream)), "dpn_adamw")
+
+
+def memset(t, value=0, nbytes=None, stream=None):
+    n = nbytes if nbytes is not None else t.numel() * t.element_size()
+    check(lib().dpn_memset_async(t.data_ptr(), value, n, _s(stream)), "dpn_memset_async")
+
+
+def copy_d2d(dst, src, nbytes=None, dst_dev=0, src_dev=0, stream=None):
+    n = nbytes if nbytes is not None else src.numel() * src.element_size()
+    check(lib().dpn_p2p_copy(dst.data_ptr(), dst_dev, src.data_ptr(), src_dev, n, _s(stream)),
+          "dpn_p2p_copy")

@@ -1,0 +1,263 @@
+"""Numerics of every CUDA kernel against a plain PyTorch fp32 reference.
+
+Tolerances: bf16 outputs are compared at rel 2e-2 of the output scale (the
+north-star bf16 tolerance); fp32 outputs of bf16 GEMMs at 5e-3 relative.
+"""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def dev():
+    from paper_2505_05856_b200 import _lib
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    _lib.init_device(torch.cuda.current_device())
+    torch.manual_seed(0)
+    yield
+
+
+def K():
+    from paper_2505_05856_b200 import kernels
+    return kernels
+
+
+def close(got, want, rel=2e-2):
+    got = got.float()
+    want = want.float()
+    scale = want.abs().max().item() + 1e-6
+    err = (got - want).abs().max().item()
+    assert err <= rel * scale, f"max err {err:.4g} vs scale {scale:.4g}"
+
+
+def rnd(*shape, dtype=torch.bfloat16, scale=1.0):
+    return (torch.randn(*shape, device="cuda") * scale).to(dtype)
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("M,N,K_,bn", [(256, 256, 128, 0), (300, 200, 96, 0), (128, 64, 64, 64),
+                                        (512, 768, 1024, 256), (384, 1024, 512, 128), (77, 136, 40, 0)])
+def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn):
+    k = K()
+    A = rnd(M, K_)
+    B = rnd(N, K_)
+    As = A.t().contiguous() if a_mn else A
+    Bs = B.t().contiguous() if b_mn else B
+    lda = As.stride(0)
+    ldb = Bs.stride(0)
+    if (a_mn and M % 8) or (b_mn and N % 8) or (not a_mn and K_ % 8) or (not b_mn and K_ % 8):
+        pytest.skip("TMA needs 16-byte strides")
+    C = torch.empty(M, (N + 7) // 8 * 8, device="cuda", dtype=torch.float32)
+    k.gemm_raw(M=M, N=N, K=K_, A=As, lda=lda, a_mn=a_mn, B=Bs, ldb=ldb, b_mn=b_mn, Cout=C,
+               ldc=C.stride(0), block_n=bn)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    close(C[:, :N], ref, rel=5e-3)
+
+
+def test_gemm_epilogue_bias_residual_gelu_aux():
+    k = K()
+    M, N, K_ = 512, 384, 256
+    A, B = rnd(M, K_), rnd(N, K_, scale=0.05)
+    bias, res = rnd(N), rnd(M, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    aux = torch.empty_like(out)
+    k.gemm_raw(M=M, N=N, K=K_, A=A, lda=K_, B=B, ldb=K_, Cout=out, ldc=N, bias=bias, residual=res,
+               aux=aux, gelu=True, alpha=0.5)
+    torch.cuda.synchronize()
+    pre = 0.5 * (A.float() @ B.float().t()) + bias.float() + res.float()
+    close(aux, pre)
+    close(out, torch.nn.functional.gelu(pre, approximate="tanh"))
+
+
+def test_gemm_f32_accumulate():
+    k = K()
+    M, N, K_ = 256, 512, 384
+    A, B = rnd(M, K_), rnd(N, K_)
+    C = torch.randn(M, N, device="cuda")
+    C0 = C.clone()
+    k.gemm_raw(M=M, N=N, K=K_, A=A, lda=K_, B=B, ldb=K_, Cout=C, ldc=N, accumulate=True)
+    torch.cuda.synchronize()
+    close(C, C0 + A.float() @ B.float().t(), rel=5e-3)
+
+
+def test_gemm_batched_attention_layout():
+    """QK^T and PV straight out of a fused [b*s, 3H] qkv buffer, per (batch, head)."""
+    k = K()
+    b, s, A_, d = 2, 256, 4, 64
+    H = A_ * d
+    qkv = rnd(b * s, 3 * H)
+    q = qkv[:, :H].reshape(b, s, A_, d).permute(0, 2, 1, 3).float()
+    kk = qkv[:, H:2 * H].reshape(b, s, A_, d).permute(0, 2, 1, 3).float()
+    v = qkv[:, 2 * H:].reshape(b, s, A_, d).permute(0, 2, 1, 3).float()
+    S = torch.empty(b, A_, s, s, device="cuda", dtype=torch.bfloat16)
+    k.gemm_raw(M=s, N=s, K=d, A=qkv, lda=3 * H, a_s=(d, s * 3 * H), B=qkv[:, H:], ldb=3 * H,
+               b_s=(d, s * 3 * H), batch1=A_, batch2=b, Cout=S, ldc=s, c_s=(s * s, A_ * s * s))
+    torch.cuda.synchronize()
+    close(S, q @ kk.transpose(-1, -2))
+    P = torch.softmax(S.float(), -1).to(torch.bfloat16)
+    O = torch.empty(b * s, H, device="cuda", dtype=torch.bfloat16)
+    # PV: A = P (K-major over keys), B = V MN-major (d contiguous)
+    k.gemm_raw(M=s, N=d, K=s, A=P, lda=s, a_s=(s * s, A_ * s * s), B=qkv[:, 2 * H:], ldb=3 * H,
+               b_mn=True, b_s=(d, s * 3 * H), batch1=A_, batch2=b, Cout=O, ldc=H,
+               c_s=(d, s * H))
+    torch.cuda.synchronize()
+    ref = (P.float() @ v).permute(0, 2, 1, 3).reshape(b * s, H)
+    close(O, ref)
+
+
+def test_linear_helpers():
+    k = K()
+    M, N, K_ = 384, 512, 256
+    x, w, b = rnd(M, K_), rnd(N, K_, scale=0.05), rnd(N)
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    k.linear_fwd(x, w, y, bias=b)
+    dy = rnd(M, N)
+    dx = torch.empty(M, K_, device="cuda", dtype=torch.bfloat16)
+    k.linear_dgrad(dy, w, dx)
+    dw = torch.empty(N, K_, device="cuda")
+    k.linear_wgrad(dy, x, dw)
+    torch.cuda.synchronize()
+    close(y, x.float() @ w.float().t() + b.float())
+    close(dx, dy.float() @ w.float())
+    close(dw, dy.float().t() @ x.float(), rel=5e-3)
+
+
+@pytest.mark.parametrize("cols", [768, 1024, 1600])
+def test_layernorm(cols):
+    k = K()
+    rows = 333
+    x = rnd(rows, cols, scale=2.0)
+    g, b = rnd(cols), rnd(cols)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    k.layernorm_fwd(x, g, b, y, mean, rstd)
+    xr = x.float().requires_grad_()
+    gr = g.float().requires_grad_()
+    br = b.float().requires_grad_()
+    yr = torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5)
+    torch.cuda.synchronize()
+    close(y, yr)
+    dy = rnd(rows, cols)
+    add = rnd(rows, cols)
+    yr.backward(dy.float())
+    dx = torch.empty_like(x)
+    dg = torch.zeros(cols, device="cuda")
+    db = torch.zeros(cols, device="cuda")
+    k.layernorm_bwd(dy, x, g, mean, rstd, dx, dg, db, dx_add=add)
+    torch.cuda.synchronize()
+    close(dx, xr.grad + add.float())
+    close(dg, gr.grad, rel=5e-3)
+    close(db, br.grad, rel=5e-3)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("cols", [128, 512, 1024])
+def test_softmax(causal, cols):
+    k = K()
+    z, q = 3, cols
+    s = rnd(z, q, cols, scale=3.0)
+    p = torch.empty_like(s)
+    alpha = 1 / math.sqrt(64)
+    k.softmax_fwd(s, p, q, alpha, causal)
+    sr = (s.float() * alpha)
+    if causal:
+        mask = torch.ones(q, cols, device="cuda").triu(1).bool()
+        sr = sr.masked_fill(mask, float("-inf"))
+    pr = torch.softmax(sr, -1)
+    torch.cuda.synchronize()
+    close(p, pr)
+    dp = rnd(z, q, cols)
+    ds = torch.empty_like(s)
+    k.softmax_bwd(p, dp, ds, alpha)
+    pf = p.float()
+    ref = alpha * pf * (dp.float() - (dp.float() * pf).sum(-1, keepdim=True))
+    torch.cuda.synchronize()
+    close(ds, ref)
+
+
+def test_gelu_add_cast_colsum():
+    k = K()
+    x = rnd(1000, 64)
+    y = torch.empty_like(x)
+    k.gelu_fwd(x, y)
+    dy = rnd(1000, 64)
+    dx = torch.empty_like(x)
+    k.gelu_bwd(dy, x, dx)
+    xr = x.float().requires_grad_()
+    yr = torch.nn.functional.gelu(xr, approximate="tanh")
+    yr.backward(dy.float())
+    o = torch.empty_like(x)
+    k.add(x, dy, o)
+    f = torch.randn(4096, device="cuda")
+    fb = torch.empty(4096, device="cuda", dtype=torch.bfloat16)
+    k.cast_f32_bf16(f, fb)
+    cs = torch.zeros(64, device="cuda")
+    k.colsum(dy, cs)
+    torch.cuda.synchronize()
+    close(y, yr)
+    close(dx, xr.grad)
+    close(o, x.float() + dy.float())
+    assert torch.equal(fb, f.to(torch.bfloat16))
+    close(cs, dy.float().sum(0), rel=5e-3)
+
+
+@pytest.mark.parametrize("vocab,ld", [(1000, 1000), (30520, 30528)])
+def test_xent(vocab, ld):
+    k = K()
+    rows = 257
+    logits = rnd(rows, ld, scale=2.0)
+    labels = torch.randint(0, vocab, (rows,), device="cuda", dtype=torch.int32)
+    loss = torch.zeros(1, device="cuda")
+    dl = torch.empty_like(logits)
+    k.xent(logits, labels, vocab, 1.0 / rows, loss, dl)
+    lr = logits[:, :vocab].float().requires_grad_()
+    ref = torch.nn.functional.cross_entropy(lr, labels.long(), reduction="sum")
+    (ref / rows).backward()
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) <= 1e-3 * abs(ref.item())
+    close(dl[:, :vocab], lr.grad)
+    assert dl[:, vocab:].abs().sum().item() == 0
+
+
+def test_embed():
+    k = K()
+    V, H, S, B = 500, 256, 64, 3
+    tok, pos = rnd(V, H), rnd(S, H)
+    ids = torch.randint(0, V, (B * S,), device="cuda", dtype=torch.int32)
+    out = torch.empty(B * S, H, device="cuda", dtype=torch.bfloat16)
+    k.embed_fwd(ids, tok, pos, out, S)
+    ref = tok.float()[ids.long()] + pos.float().repeat(B, 1)
+    dout = rnd(B * S, H)
+    dt = torch.zeros(V, H, device="cuda")
+    dp = torch.zeros(S, H, device="cuda")
+    k.embed_bwd(ids, dout, dt, dp, S)
+    rt = torch.zeros(V, H, device="cuda").index_add_(0, ids.long(), dout.float())
+    rp = dout.float().reshape(B, S, H).sum(0)
+    torch.cuda.synchronize()
+    close(out, ref)
+    close(dt, rt, rel=1e-4)
+    close(dp, rp, rel=1e-4)
+
+
+def test_adamw():
+    k = K()
+    n = 4096
+    w = torch.randn(n, device="cuda")
+    g = torch.randn(n, device="cuda")
+    m, v = torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    out = torch.empty(n, device="cuda", dtype=torch.bfloat16)
+    wr = w.clone().requires_grad_()
+    opt = torch.optim.AdamW([wr], lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01)
+    for step in (1, 2, 3):
+        k.adamw(w, m, v, g, out, 1e-3, 0.9, 0.999, 1e-8, 0.01, step)
+        wr.grad = g.clone()
+        opt.step()
+    torch.cuda.synchronize()
+    assert torch.allclose(w, wr.detach(), rtol=1e-5, atol=1e-6)
+    assert torch.equal(out, w.to(torch.bfloat16))
