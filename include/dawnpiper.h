@@ -93,11 +93,11 @@ int dpn_add(const void* a, const void* b, void* out, int64_t n, void* stream);
 int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
 /* out[c] += sum_r x[r, c]   (bias gradients) */
 int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out, void* stream);
-/* head: *loss_sum += sum_r CE(logits[r, :vocab], labels[r]);
+/* head: *loss_sum += loss_scale * sum_r CE(logits[r, :vocab], labels[r]);
  * dlogits = (softmax - onehot) * grad_scale, pad columns [vocab, ld) zeroed.
  * dlogits may alias logits. */
 int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, int64_t rows, int64_t vocab,
-             float grad_scale, float* loss_sum, void* dlogits, void* stream);
+             float grad_scale, float loss_scale, float* loss_sum, void* dlogits, void* stream);
 /* embed: out[r] = tok[ids[r]] + pos[r % seq]; backward accumulates (f32). */
 int dpn_embed_fwd(const int32_t* ids, const void* tok, const void* pos, void* out, int64_t rows,
                   int64_t seq, int64_t hidden, void* stream);

@@ -1,0 +1,219 @@
+"""CPU fp32 restatement of the pipeline training step -- TEST ORACLE ONLY.
+
+This file is test infrastructure: only tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference leg may import it, and only as the
+checker or the timed CPU baseline.  It never runs on the product path.
+
+Parity status: UNPINNED.  The reference (dawnplan) has no model, optimizer or
+loss code, so there is no reference output to pin these
+numerics to; this restatement fixes the semantics instead:
+
+  * model: pre-LN transformer blocks
+        h1 = LN1(x); [q|k|v] = h1 Wqkv^T + bqkv; P = softmax(q k^T / sqrt(d) [causal])
+        ctx = P v; y = ctx Wo^T + bo + x; h2 = LN2(y); f = h2 W1^T + b1
+        g = gelu_tanh(f); z = g W2^T + b2; out = z + y
+    embed = tok[ids] + pos[t]; head = LN_f then logits = h Wh[:V]^T,
+    loss = mean-over-tokens cross entropy per micro-batch;
+  * schedule: per stage x of l, the 1F1B op list of simulate.py:211-222
+    (restated below as `one_f_one_b`);
+  * weight stashing (PipeDream): a forward uses the stage's newest weights and
+    its backward differentiates through that same version; every backward is
+    followed by an AdamW step on the fp32 master weights;
+  * AdamW: torch.optim.AdamW semantics (decoupled weight decay, bias
+    correction), applied to every parameter.
+
+Everything is computed in fp32 with torch autograd on the host CPU.
+"""
+
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Sequence, Tuple
+
+import torch
+import torch.nn.functional as F
+
+
+def one_f_one_b(stages: int, m: int, x: int) -> List[Tuple[str, int]]:
+    """simulate.py:211-222: min(l-x, m) warm-up forwards, (F, B) pairs, drain."""
+    warm = min(stages - x, m)
+    ops = [("fwd", j) for j in range(1, warm + 1)]
+    k = 0
+    while warm + k < m:
+        k += 1
+        ops.append(("fwd", warm + k))
+        ops.append(("bwd", k))
+    ops += [("bwd", j) for j in range(k + 1, m + 1)]
+    return ops
+
+
+def node_ids(layers: int) -> List[str]:
+    ids = ["embed"]
+    for b in range(layers):
+        ids += [f"b{b}.{k}" for k in ("ln1", "qkv", "score", "attn", "proj", "ln2", "fc1",
+                                      "gelu", "fc2", "add")]
+    return ids + ["lnf", "head"]
+
+
+def _inputs(nid: str, layers: int) -> Tuple[str, ...]:
+    if nid == "embed":
+        return ()
+    if nid == "lnf":
+        return (f"b{layers - 1}.add",)
+    if nid == "head":
+        return ("lnf",)
+    b, k = nid.split(".")
+    blk = int(b[1:])
+    x = "embed" if blk == 0 else f"b{blk - 1}.add"
+    p = f"b{blk}."
+    return {
+        "ln1": (x,), "qkv": (p + "ln1",), "score": (p + "qkv",), "attn": (p + "score", p + "qkv"),
+        "proj": (p + "attn", x), "ln2": (p + "proj",), "fc1": (p + "ln2",), "gelu": (p + "fc1",),
+        "fc2": (p + "gelu",), "add": (p + "fc2", p + "proj"),
+    }[k]
+
+
+class RefStage:
+    def __init__(self, dims: dict, init: Dict[str, torch.Tensor], nodes: Sequence[str], opt: dict):
+        self.d = dims
+        self.nodes = list(nodes)
+        self.params = {k: v.detach().clone().float() for k, v in init.items()
+                       if k.rsplit(".", 1)[0] in self.nodes}
+        self.exp_avg = {k: torch.zeros_like(v) for k, v in self.params.items()}
+        self.exp_sq = {k: torch.zeros_like(v) for k, v in self.params.items()}
+        self.step = 0
+        self.opt = opt
+        self.inflight: Dict[int, tuple] = {}
+
+    def _node(self, nid: str, env: Dict[str, torch.Tensor], W: Dict[str, torch.Tensor],
+              ids, labels) -> torch.Tensor:
+        d = self.d
+        H, A, s = d["hidden"], d["heads"], d["seq"]
+        hd = H // A
+        kind = nid.split(".")[-1] if nid not in ("embed", "lnf", "head") else nid
+        ins = [env[u] for u in _inputs(nid, d["layers"])]
+        w = lambda pn: W[f"{nid}.{pn}"]
+        if kind == "embed":
+            M = ids.numel()
+            return w("tok")[ids.long()] + w("pos")[torch.arange(M) % s]
+        if kind in ("ln1", "ln2", "lnf"):
+            return F.layer_norm(ins[0], (H,), w("gamma"), w("beta"), d["ln_eps"])
+        if kind in ("qkv", "fc1", "fc2"):
+            return ins[0] @ w("weight").t() + w("bias")
+        if kind == "proj":
+            return ins[0] @ w("weight").t() + w("bias") + ins[1]
+        if kind == "gelu":
+            return F.gelu(ins[0], approximate="tanh")
+        if kind == "add":
+            return ins[0] + ins[1]
+        if kind == "score":
+            qkv = ins[0]
+            b = qkv.shape[0] // s
+            q = qkv[:, :H].reshape(b, s, A, hd).transpose(1, 2)
+            k = qkv[:, H:2 * H].reshape(b, s, A, hd).transpose(1, 2)
+            sc = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
+            if d["causal"]:
+                sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), float("-inf"))
+            return torch.softmax(sc, -1)
+        if kind == "attn":
+            P, qkv = ins
+            b = qkv.shape[0] // s
+            v = qkv[:, 2 * H:].reshape(b, s, A, hd).transpose(1, 2)
+            return (P @ v).transpose(1, 2).reshape(b * s, H)
+        if kind == "head":
+            logits = ins[0] @ w("weight")[:d["vocab"]].t()
+            return F.cross_entropy(logits, labels.long())
+        raise ValueError(nid)
+
+    def forward(self, j: int, recv: Dict[str, torch.Tensor], ids=None, labels=None):
+        version = {k: v.detach().clone().requires_grad_(True) for k, v in self.params.items()}
+        env = {k: t.detach().clone().requires_grad_(True) for k, t in recv.items()}
+        leaves = dict(env)
+        for nid in self.nodes:
+            env[nid] = self._node(nid, env, version, ids, labels)
+        self.inflight[j] = (leaves, env, version)
+        return env
+
+    def backward(self, j: int, out_grads: Dict[str, torch.Tensor], send_ids: Sequence[str]):
+        leaves, env, version = self.inflight.pop(j)
+        roots, grads = [], []
+        if "head" in env:
+            roots.append(env["head"])
+            grads.append(torch.ones(()))
+        for k, gk in out_grads.items():
+            roots.append(env[k])
+            grads.append(gk)
+        torch.autograd.backward(roots, grads)
+        self._adamw({k: (v.grad if v.grad is not None else torch.zeros_like(v))
+                     for k, v in version.items()})
+        return {k: leaves[k].grad.detach() for k in leaves if leaves[k].grad is not None}
+
+    def _adamw(self, g: Dict[str, torch.Tensor]) -> None:
+        o = self.opt
+        self.step += 1
+        b1, b2 = o["beta1"], o["beta2"]
+        bc1, bc2 = 1 - b1 ** self.step, 1 - b2 ** self.step
+        for k, p in self.params.items():
+            gk = g[k]
+            self.exp_avg[k].mul_(b1).add_(gk, alpha=1 - b1)
+            self.exp_sq[k].mul_(b2).addcmul_(gk, gk, value=1 - b2)
+            p.mul_(1 - o["lr"] * o["weight_decay"])
+            denom = (self.exp_sq[k] / bc2).sqrt().add_(o["eps"])
+            p.addcdiv_(self.exp_avg[k] / bc1, denom, value=-o["lr"])
+
+
+def boundary(stage_nodes: List[List[str]], x: int, layers: int) -> List[str]:
+    """Outputs produced at or before stage x that a later stage reads."""
+    before = [n for st in stage_nodes[:x + 1] for n in st]
+    after = {n for st in stage_nodes[x + 1:] for n in st}
+    return [u for u in before if any(u in _inputs(v, layers) for v in after)]
+
+
+def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor,
+                    labels: torch.Tensor, stage_nodes: List[List[str]], opt: dict,
+                    steps: int = 1):
+    """Run `steps` iterations of m micro-batches (ids/labels: int [m, b*s]).
+    Returns (losses [steps][m], final fp32 parameters)."""
+    l, m = len(stage_nodes), ids.shape[0]
+    stages = [RefStage(dims, init, nodes, opt) for nodes in stage_nodes]
+    sends = [boundary(stage_nodes, x, dims["layers"]) for x in range(l)]
+    all_losses = []
+    for _ in range(steps):
+        losses = [0.0] * m
+        ops = [one_f_one_b(l, m, x + 1) for x in range(l)]
+        ptr = [0] * l
+        acts: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
+        grads: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
+        left = sum(len(o) for o in ops)
+        while left:
+            moved = False
+            for x in range(l):
+                while ptr[x] < len(ops[x]):
+                    kind, j = ops[x][ptr[x]]
+                    if kind == "fwd":
+                        if x > 0 and (x - 1, j) not in acts:
+                            break
+                        recv = acts.get((x - 1, j), {})
+                        env = stages[x].forward(j, recv, ids=ids[j - 1], labels=labels[j - 1])
+                        fwd_env = dict(recv)
+                        fwd_env.update(env)
+                        if x < l - 1:
+                            acts[(x, j)] = {u: fwd_env[u].detach() for u in sends[x]}
+                        else:
+                            losses[j - 1] = float(env["head"].detach())
+                    else:
+                        if x < l - 1 and (x, j) not in grads:
+                            break
+                        g_in = stages[x].backward(j, grads.pop((x, j), {}), sends[x])
+                        if x > 0:
+                            grads[(x - 1, j)] = g_in
+                    ptr[x] += 1
+                    left -= 1
+                    moved = True
+            if not moved:
+                raise RuntimeError("oracle schedule deadlock")
+        all_losses.append(losses)
+    final = {}
+    for s in stages:
+        final.update({k: v.detach().clone() for k, v in s.params.items()})
+    return all_losses, final

@@ -53,7 +53,7 @@ SIGNATURES = {
     "dpn_add": [_vp, _vp, _vp, _i64, _vp],
     "dpn_cast_f32_bf16": [_vp, _vp, _i64, _vp],
     "dpn_colsum": [_vp, _i64, _i64, _i64, _vp, _vp],
-    "dpn_xent": [_vp, _i64, _vp, _i64, _i64, _f32, _vp, _vp, _vp],
+    "dpn_xent": [_vp, _i64, _vp, _i64, _i64, _f32, _f32, _vp, _vp, _vp],
     "dpn_embed_fwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_embed_bwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_adamw": [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _f32, _i64, _vp],

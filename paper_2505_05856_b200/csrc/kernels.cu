@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
 __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restrict__ logits,
                                                    long long ld, const int* __restrict__ labels,
                                                    long long rows, int vocab, float grad_scale,
-                                                   float* __restrict__ loss_sum,
+                                                   float loss_scale, float* __restrict__ loss_sum,
                                                    __nv_bfloat16* __restrict__ dlogits) {
   extern __shared__ __align__(16) uint8_t xsm[];
   __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(xsm);
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
     const int lab = labels[r];
     if (tid == 0) {
       const float xl = __bfloat162float(row[lab]);
-      atomicAdd(loss_sum, (logf(sum) + mx - xl));
+      atomicAdd(loss_sum, loss_scale * (logf(sum) + mx - xl));
     }
     __nv_bfloat16* dst = dlogits + r * ld;
     for (int c = tid; c < nvec; c += blockDim.x) {
@@ -611,8 +611,8 @@ extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld,
 }
 
 extern "C" int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, int64_t rows,
-                        int64_t vocab, float grad_scale, float* loss_sum, void* dlogits,
-                        void* stream) {
+                        int64_t vocab, float grad_scale, float loss_scale, float* loss_sum,
+                        void* dlogits, void* stream) {
   DPN_REQUIRE(vocab % 8 == 0 && ld % 8 == 0 && vocab <= ld, "vocab/ld must be multiples of 8");
   DPN_REQUIRE(vocab * 2 <= 200 * 1024, "vocab row must fit in shared memory");
   if (rows == 0) return 0;
@@ -624,7 +624,7 @@ extern "C" int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, i
     set = true;
   }
   xent_kernel<<<(int)std::min<long long>(rows, 148 * 4), 512, smem, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)logits, ld, labels, rows, (int)vocab, grad_scale, loss_sum,
+      (const __nv_bfloat16*)logits, ld, labels, rows, (int)vocab, grad_scale, loss_scale, loss_sum,
       (__nv_bfloat16*)dlogits);
   DPN_LAUNCH_CHECK();
   return 0;

@@ -140,10 +140,10 @@ def colsum(x, out, stream=None):
           "dpn_colsum")
 
 
-def xent(logits, labels, vocab, grad_scale, loss_sum, dlogits, stream=None):
+def xent(logits, labels, vocab, grad_scale, loss_sum, dlogits, loss_scale=1.0, stream=None):
     rows, ld = logits.shape
     check(lib().dpn_xent(logits.data_ptr(), ld, labels.data_ptr(), rows, vocab, grad_scale,
-                         loss_sum.data_ptr(), dlogits.data_ptr(), _s(stream)), "dpn_xent")
+                         loss_scale, loss_sum.data_ptr(), dlogits.data_ptr(), _s(stream)), "dpn_xent")
 
 
 def embed_fwd(ids, tok, pos, out, seq, stream=None):

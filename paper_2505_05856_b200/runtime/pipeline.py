@@ -1,0 +1,317 @@
+"""The B200 pipeline run: `run(plan, g, cfg) -> RunReport`.
+
+This replaces the reference's analytic `simulate(plan, g, cfg)`
+(simulate.py:130-166) with a real 1F1B training run of the plan's partition:
+
+  * one `StageExecutor` per plan stage (`stage_bounds(plan.cuts)`), executing
+    that stage's memopt actions for real;
+  * every stage issues exactly `async_ops(l, m, x)` (simulate.py:211-222):
+    min(l-x, m) warm-up forwards, (F, B) pairs, then the drain;
+  * boundary activations / gradients are the tensors of `boundary_bytes`
+    (simulate.py:93-100), moved per micro-batch: device-to-device when stages
+    share a GPU, cudaMemcpyPeerAsync when they are on peer GPUs of one
+    process, NCCL send/recv (torch.distributed) when each stage is its own
+    process (`run_distributed`).
+
+With all stages on one GPU (`devices=[0]`, the 1-GPU bench case) a single
+host thread issues the stages' op lists interleaved by the same readiness
+walk the reference simulator uses (simulate.py:244-282); dependencies are
+then satisfied by stream order.
+
+The report is a superset of SimReport: the same fields, measured from CUDA
+events, plus per-micro-batch losses, samples/s and the memory actually held.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+from .. import kernels as K
+from .._lib import init_device
+from ..planner.balance import SCHEDULE_ASYNC
+from ..planner.profile import ComputationGraph
+from ..planner.schedule import SimEvent, async_iteration, async_ops, inflight_depth
+from ..planner.search import PartitionPlan, stage_bounds
+from .model import AdamWConfig, TransformerConfig, build_nodes, init_params
+from .stage import StageExecutor
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    micro_batches: int
+    micro_batch_size: int
+    devices: Tuple[int, ...] = (0,)
+    seed: int = 0
+    opt: AdamWConfig = AdamWConfig()
+    trace: bool = True
+    capacity: Optional[int] = None  # per-GPU byte cap enforced on the caching allocator
+
+    def __post_init__(self):
+        if self.micro_batches < 1:
+            raise ValueError("need at least one micro-batch")
+        if self.micro_batch_size < 1:
+            raise ValueError("micro-batch size must be positive")
+
+
+@dataclass(frozen=True)
+class RunReport:
+    # SimReport fields (simulate.py:60-79), measured
+    per_stage_peak: Tuple[int, ...]
+    iteration_time: float
+    bubble_ratio: float
+    waste_ratio: float
+    trace: Tuple[SimEvent, ...]
+    makespan: int
+    capacity_exceeded: Tuple[int, ...]
+    # run-only fields
+    losses: Tuple[float, ...] = ()
+    samples_per_s: float = 0.0
+    step_time_us: float = 0.0
+    device_peak_bytes: int = 0
+
+    def to_doc(self) -> dict:
+        return {
+            "per_stage_peak_bytes": list(self.per_stage_peak),
+            "iteration_time_us": self.iteration_time,
+            "bubble_ratio": self.bubble_ratio,
+            "waste_ratio": self.waste_ratio,
+            "makespan_us": self.makespan,
+            "capacity_exceeded_stages": list(self.capacity_exceeded),
+            "events": len(self.trace),
+            "losses": list(self.losses),
+            "samples_per_s": self.samples_per_s,
+            "step_time_us": self.step_time_us,
+            "device_peak_bytes": self.device_peak_bytes,
+        }
+
+
+def colocated_order(stages: int, m: int) -> List[Tuple[int, str, int]]:
+    """Interleave the stages' 1F1B op lists by dependency readiness, scanning
+    stages in order exactly like simulate.py:244-282 (without durations).
+    Returns (stage 1-based, kind, micro-batch)."""
+    ops = [async_ops(stages, m, x + 1) for x in range(stages)]
+    ptr = [0] * stages
+    fwd_done = [set() for _ in range(stages)]
+    bwd_done = [set() for _ in range(stages)]
+    out = []
+    left = sum(len(o) for o in ops)
+    while left:
+        moved = False
+        for x in range(stages):
+            while ptr[x] < len(ops[x]):
+                kind, j, _ = ops[x][ptr[x]]
+                if kind == "fwd":
+                    ok = x == 0 or j in fwd_done[x - 1]
+                else:
+                    ok = (j in fwd_done[x]) if x == stages - 1 else (j in bwd_done[x + 1])
+                if not ok:
+                    break
+                out.append((x + 1, kind, j))
+                (fwd_done if kind == "fwd" else bwd_done)[x].add(j)
+                ptr[x] += 1
+                left -= 1
+                moved = True
+        if not moved:
+            raise RuntimeError("schedule deadlock; op lists are inconsistent")
+    return out
+
+
+class Pipeline:
+    """All stages of a plan in one process (one or several local GPUs)."""
+
+    def __init__(self, model: TransformerConfig, g: ComputationGraph, plan: PartitionPlan,
+                 cfg: RunConfig):
+        if plan.schedule != SCHEDULE_ASYNC:
+            raise ValueError("the B200 run implements the async 1F1B schedule")
+        bounds = stage_bounds(plan.cuts, len(g))
+        if len(g) != len(build_nodes(model)):
+            raise ValueError("graph does not describe this model (node count mismatch)")
+        self.model, self.g, self.plan, self.cfg = model, g, plan, cfg
+        self.l = len(bounds)
+        self.m = cfg.micro_batches
+        devs = list(cfg.devices)
+        self.stage_dev = [devs[min(x * len(devs) // self.l, len(devs) - 1)] for x in range(self.l)]
+        for d in set(self.stage_dev):
+            init_device(d)
+        for a in set(self.stage_dev):
+            for b in set(self.stage_dev):
+                if a != b:
+                    from .._lib import check, lib
+                    check(lib().dpn_enable_peer(a, b), "dpn_enable_peer")
+        if cfg.capacity is not None:
+            for d in set(self.stage_dev):
+                total = torch.cuda.get_device_properties(d).total_memory
+                torch.cuda.set_per_process_memory_fraction(min(1.0, cfg.capacity / total), d)
+        self.streams = {d: torch.cuda.Stream(device=d) for d in set(self.stage_dev)}
+        nodes = build_nodes(model)
+        init = init_params(model, cfg.seed)
+        self.stages: List[StageExecutor] = []
+        for x, (lo, hi) in enumerate(bounds, start=1):
+            d = self.stage_dev[x - 1]
+            with torch.cuda.device(d):
+                self.stages.append(StageExecutor(
+                    cfg=model, g=g, nodes=nodes, lo=lo, hi=hi, stage=x, stages=self.l,
+                    micro_batch=cfg.micro_batch_size, memopt=plan.memopt[x - 1], init=init,
+                    device=torch.device("cuda", d), stream=self.streams[d], opt=cfg.opt))
+        self.order = colocated_order(self.l, self.m)
+        first_dev = self.stage_dev[0]
+        self.loss = torch.zeros(self.m, dtype=torch.float32, device=torch.device("cuda", self.stage_dev[-1]))
+        self.static_bytes = [self._stage_bytes(s) for s in self.stages]
+        for d in set(self.stage_dev):
+            torch.cuda.synchronize(d)  # parameter init (default stream) before the run streams
+
+    @staticmethod
+    def _stage_bytes(s: StageExecutor) -> int:
+        tot = 0
+        for t in (s.params.master, s.params.m, s.params.v, s.params.grad, s.params.ring):
+            tot += t.numel() * t.element_size()
+        for d in s.slot_buf:
+            tot += sum(t.numel() * t.element_size() for t in d.values())
+        for d in (s.fwd_scratch, s.bwd_scratch, s.work):
+            tot += sum(t.numel() * t.element_size() for t in d.values())
+        return tot
+
+    def _send_fwd(self, x: int, j: int) -> Dict[str, torch.Tensor]:
+        """Stage x (1-based) sends micro-batch j's boundary activations: they are
+        copied into message buffers owned by the receiver (the sender's own
+        buffers are reused by its next forward, and the receiver may not have
+        a free slot yet -- exactly like a posted NCCL send)."""
+        src = self.stages[x - 1]
+        d_src, d_dst = self.stage_dev[x - 1], self.stage_dev[x]
+        st = self.streams[d_dst]
+        if d_src != d_dst:
+            ev = torch.cuda.Event()
+            ev.record(self.streams[d_src])
+            st.wait_event(ev)
+        out = {}
+        with torch.cuda.stream(st):
+            for tid in src.send_ids:
+                a = src.send_buffer(tid, j)
+                msg = torch.empty_like(a, device=torch.device("cuda", d_dst))
+                K.copy_d2d(msg, a, dst_dev=d_dst, src_dev=d_src, stream=st)
+                out[tid] = msg
+        return out
+
+    def _deliver_fwd(self, x: int, j: int, msgs: Dict[str, torch.Tensor]) -> None:
+        """Receiver side: land the messages in stage x's slot for micro-batch j."""
+        dst = self.stages[x - 1]
+        st = self.streams[self.stage_dev[x - 1]]
+        for tid, msg in msgs.items():
+            K.copy_d2d(dst.recv_buffer(tid, j), msg, dst_dev=self.stage_dev[x - 1],
+                       src_dev=self.stage_dev[x - 1], stream=st)
+
+    def _send_bwd(self, x: int, grads: Dict[str, torch.Tensor]) -> Dict[str, torch.Tensor]:
+        # x is the sending stage (1-based); returns fresh buffers owned by stage x-1
+        d_src, d_dst = self.stage_dev[x - 1], self.stage_dev[x - 2]
+        st = self.streams[d_dst]
+        if d_src != d_dst:
+            ev = torch.cuda.Event()
+            ev.record(self.streams[d_src])
+            st.wait_event(ev)
+        out = {}
+        with torch.cuda.stream(st):
+            for tid, gsrc in grads.items():
+                gdst = torch.empty_like(gsrc, device=torch.device("cuda", d_dst))
+                K.copy_d2d(gdst, gsrc, dst_dev=d_dst, src_dev=d_src, stream=st)
+                out[tid] = gdst
+        return out
+
+    def step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
+        """One training iteration (m micro-batches).  ids/labels: int32 [m, b*s] on
+        the first / last stage's device.  Returns the device loss vector [m]."""
+        with torch.cuda.stream(self.streams[self.stage_dev[-1]]):
+            self.loss.zero_()
+        pending: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
+        mailbox: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
+        for x, kind, j in self.order:
+            s = self.stages[x - 1]
+            st = self.streams[self.stage_dev[x - 1]]
+            if events is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+            if kind == "fwd":
+                if x > 1:
+                    self._deliver_fwd(x, j, mailbox.pop((x, j)))
+                s.forward(j, ids=ids[j - 1] if s.is_first else None,
+                          labels=labels[j - 1] if s.is_last else None,
+                          loss_out=self.loss[j - 1:j] if s.is_last else None)
+                if x < self.l:
+                    mailbox[(x + 1, j)] = self._send_fwd(x, j)
+            else:
+                for tid, gt in pending.pop((x, j), {}).items():
+                    s.set_recv_grad(tid, gt)
+                grads = s.backward(j)
+                if x > 1:
+                    pending[(x - 1, j)] = self._send_bwd(x, grads)
+                s.finish_backward(j)
+            if events is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(st)
+                events.append((x, j, kind, e0, e1))
+        return self.loss
+
+    def report(self, events: list, t_origin: torch.cuda.Event, losses: torch.Tensor,
+               wall_us: float) -> RunReport:
+        """Turn the timed events of one step into a SimReport-shaped RunReport."""
+        torch.cuda.synchronize()
+        ev: List[SimEvent] = []
+        done = [0] * (self.m + 1)
+        for x, j, kind, e0, e1 in events:
+            a = int(round(t_origin.elapsed_time(e0) * 1000))
+            b = int(round(t_origin.elapsed_time(e1) * 1000))
+            ev.append(SimEvent(x, j, kind, a, b))
+            if kind == "bwd" and x == 1:
+                done[j] = b
+        makespan = max(e.end for e in ev) if ev else 0
+        iteration = async_iteration(done, self.l, self.m, makespan)
+        busy = [sum(e.end - e.start for e in ev if e.stage == x + 1) for x in range(self.l)]
+        bubble = 1.0 - sum(busy) / (self.l * makespan) if makespan > 0 else 0.0
+        peaks = list(self.static_bytes)
+        top = max(peaks) if peaks else 0
+        waste = sum(top - p for p in peaks) / (self.l * top) if top > 0 else 0.0
+        cap = self.cfg.capacity
+        exceeded = tuple(x + 1 for x, p in enumerate(peaks) if cap is not None and p > cap)
+        b = self.cfg.micro_batch_size
+        return RunReport(
+            per_stage_peak=tuple(peaks), iteration_time=iteration, bubble_ratio=bubble,
+            waste_ratio=waste, trace=tuple(sorted(ev, key=lambda e: (e.start, e.end, e.stage, e.mb, e.kind))),
+            makespan=makespan, capacity_exceeded=exceeded,
+            losses=tuple(float(v) for v in losses.tolist()),
+            samples_per_s=(b * 1e6 / iteration) if iteration > 0 else 0.0,
+            step_time_us=wall_us,
+            device_peak_bytes=max(torch.cuda.max_memory_allocated(d) for d in set(self.stage_dev)))
+
+
+def run(plan: PartitionPlan, g: ComputationGraph, cfg: RunConfig,
+        model: Optional[TransformerConfig] = None, ids: Optional[torch.Tensor] = None,
+        labels: Optional[torch.Tensor] = None, steps: int = 1) -> RunReport:
+    """Drop-in for simulate(plan, g, cfg): executes `steps` training iterations
+    of the plan on B200s and reports the last one (measured)."""
+    from .model import PRESETS, synthetic_batch
+    if model is None:
+        base = g.name.rsplit("_b", 1)[0]
+        if base not in PRESETS:
+            raise ValueError(f"cannot infer the model of graph {g.name!r}; pass model=")
+        model = PRESETS[base]
+    pipe = Pipeline(model, g, plan, cfg)
+    if ids is None:
+        ids, labels = synthetic_batch(model, cfg.micro_batches, cfg.micro_batch_size, cfg.seed)
+    d0, dl = pipe.stage_dev[0], pipe.stage_dev[-1]
+    ids_d = ids.to(torch.device("cuda", d0))
+    lab_d = labels.to(torch.device("cuda", dl))
+    rep = None
+    for _ in range(steps):
+        events: list = []
+        t0 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        t0.record(pipe.streams[d0])
+        losses = pipe.step(ids_d, lab_d, events if cfg.trace else None)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - w0) * 1e6
+        rep = pipe.report(events, t0, losses, wall) if cfg.trace else None
+    return rep

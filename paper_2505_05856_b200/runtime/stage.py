@@ -1,0 +1,532 @@
+"""Per-stage executor of the fine-grained node graph on one B200.
+
+One `StageExecutor` owns a contiguous node range [lo, hi] of the plan
+(`stage_bounds`, partition.py:99-103) and everything that range needs on its
+device:
+
+  parameters   flat fp32 master / Adam m / Adam v / grad buffers plus a ring of
+               w = l-x+1 bf16 weight versions (1F1B weight stashing: the
+               forward of micro-batch j uses the newest version, its backward
+               the same one; each backward is followed by an AdamW step that
+               writes the next version into the slot the retiring micro-batch
+               frees).  w matches `schedule_weight` (balance.py:65-77).
+  activations  static per-slot buffers (w slots) for every saved tensor this
+               stage reads in its backward; tensors the plan evicts (memopt
+               actions) live instead in one forward scratch + one backward
+               scratch buffer, with pinned host slots for swaps.
+  streams      the compute stream (given) and a copy stream for swaps.
+
+Memopt actions are executed exactly (memopt.py:169-322 decides them):
+  swap      D2H on the copy stream right after the producing node's forward
+            (or right after receipt, for a boundary input), H2D into the
+            backward scratch before the stage's backward;
+  recompute the tensor is dropped after the forward and rebuilt at backward
+            time by replaying exactly `producer_chain` (memopt.py:91-115).
+
+All compute goes through `kernels` -> `_dawnpiper.so`; nothing here computes
+with torch.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Set, Tuple
+
+import torch
+
+from .. import kernels as K
+from ..planner.memplan import MemOptPlan, producer_chain
+from ..planner.profile import ComputationGraph
+from .graph import out_tid, stats_tid
+from .model import (AdamWConfig, NodeDef, TransformerConfig, backward_readers, output_spec,
+                    saved_for_backward)
+
+BF16 = torch.bfloat16
+F32 = torch.float32
+
+
+def _align8(n: int) -> int:
+    return (n + 7) // 8 * 8
+
+
+@dataclass
+class ParamSlot:
+    name: str
+    shape: Tuple[int, ...]
+    offset: int
+    numel: int
+    dense: bool  # gradient fully written by a GEMM (no zeroing / accumulation)
+
+
+class FlatParams:
+    """Flat parameter storage for one stage (master/m/v/grad fp32 + bf16 ring)."""
+
+    def __init__(self, nodes: Sequence[NodeDef], init: Dict[str, torch.Tensor], versions: int,
+                 device):
+        dense, accum = [], []
+        for n in nodes:
+            for pn, shp in n.params:
+                name = f"{n.id}.{pn}"
+                is_dense = n.kind in ("linear", "linear_res", "head") and pn == "weight"
+                (dense if is_dense else accum).append((name, tuple(shp)))
+        self.slots: Dict[str, ParamSlot] = {}
+        off = 0
+        for group, is_dense in ((dense, True), (accum, False)):
+            if not is_dense:
+                self.accum_start = off
+            for name, shp in group:
+                numel = math.prod(shp)
+                self.slots[name] = ParamSlot(name, shp, off, numel, is_dense)
+                off += _align8(numel)
+        self.total = max(8, off)
+        self.accum_bytes = (self.total - self.accum_start) * 4
+        self.master = torch.zeros(self.total, dtype=F32, device=device)
+        for name, s in self.slots.items():
+            self.master[s.offset:s.offset + s.numel].copy_(init[name].reshape(-1))
+        self.m = torch.zeros_like(self.master)
+        self.v = torch.zeros_like(self.master)
+        self.grad = torch.zeros_like(self.master)
+        self.ring = torch.empty(versions, self.total, dtype=BF16, device=device)
+        for k in range(versions):
+            K.cast_f32_bf16(self.master, self.ring[k])
+        self.step = 0
+        # weight-version ring bookkeeping (PipeDream stashing): the newest
+        # version sits in `latest`; micro-batches in flight pin the slot their
+        # forward read until their backward retires
+        self.latest = 0
+        self.users: List[Set[int]] = [set() for _ in range(versions)]
+        self.version_of: Dict[int, int] = {}
+
+    def pin_latest(self, mb: int) -> int:
+        self.version_of[mb] = self.latest
+        self.users[self.latest].add(mb)
+        return self.latest
+
+    def pinned(self, mb: int) -> int:
+        return self.version_of[mb]
+
+    def retire(self, mb: int) -> int:
+        """Unpin mb's version; return the slot the next version may overwrite."""
+        v = self.version_of.pop(mb)
+        self.users[v].discard(mb)
+        if not self.users[v]:
+            return v
+        for k, u in enumerate(self.users):
+            if not u:
+                return k
+        raise RuntimeError("weight-version ring exhausted (more micro-batches in flight than slots)")
+
+    def weight(self, version_slot: int, name: str) -> torch.Tensor:
+        s = self.slots[name]
+        return self.ring[version_slot, s.offset:s.offset + s.numel].view(s.shape)
+
+    def gradv(self, name: str) -> torch.Tensor:
+        s = self.slots[name]
+        return self.grad[s.offset:s.offset + s.numel].view(s.shape)
+
+    def master_view(self, name: str) -> torch.Tensor:
+        s = self.slots[name]
+        return self.master[s.offset:s.offset + s.numel].view(s.shape)
+
+    def zero_accum_grads(self, stream=None) -> None:
+        if self.accum_bytes:
+            K.memset(self.grad[self.accum_start:], 0, self.accum_bytes, stream=stream)
+
+    def adamw(self, out_slot: int, opt: AdamWConfig, stream=None) -> None:
+        self.step += 1
+        K.adamw(self.master, self.m, self.v, self.grad, self.ring[out_slot], opt.lr, opt.beta1,
+                opt.beta2, opt.eps, opt.weight_decay, self.step, stream=stream)
+        self.latest = out_slot
+
+
+class StageExecutor:
+    def __init__(self, *, cfg: TransformerConfig, g: ComputationGraph, nodes: Sequence[NodeDef],
+                 lo: int, hi: int, stage: int, stages: int, micro_batch: int, memopt: MemOptPlan,
+                 init: Dict[str, torch.Tensor], device: torch.device, stream: torch.cuda.Stream,
+                 opt: AdamWConfig = AdamWConfig(), slots: Optional[int] = None):
+        self.cfg, self.g = cfg, g
+        self.all_nodes = list(nodes)
+        self.nodes = self.all_nodes[lo:hi + 1]
+        self.lo, self.hi = lo, hi
+        self.stage, self.stages = stage, stages
+        self.b = micro_batch
+        self.M = micro_batch * cfg.seq
+        self.device = device
+        self.stream = stream
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self.opt = opt
+        self.w = slots if slots is not None else stages - stage + 1
+        self.is_first = lo == 0
+        self.is_last = hi == len(self.all_nodes) - 1
+        self.node_by_id = {n.id: n for n in self.all_nodes}
+        self.index = {n.id: i for i, n in enumerate(self.all_nodes)}
+        self.params = FlatParams(self.nodes, init, self.w, device)
+
+        # ---- tensor bookkeeping -------------------------------------------------
+        self.readers = backward_readers(self.all_nodes)
+        in_stage = {n.id for n in self.nodes}
+        # boundary inputs: outputs of earlier stages consumed here or relayed onward
+        self.recv_ids = self._boundary(lo - 1) if not self.is_first else []
+        self.send_ids = self._boundary(hi) if not self.is_last else []
+        # tensors some backward in this stage reads
+        needed: Set[str] = set()
+        for n in self.nodes:
+            if n.kind == "ln":
+                needed.add(stats_tid(n.id))
+        for src, rd in self.readers.items():
+            if any(r in in_stage for r in rd) and saved_for_backward(self.node_by_id[src]):
+                needed.add(out_tid(src))
+        self.needed = needed
+        acts = {a.tensor_id: a for a in memopt.actions}
+        self.swap_ids = {t for t, a in acts.items() if a.kind == "swap"}
+        self.recompute_ids = {t for t, a in acts.items() if a.kind == "recompute"}
+        unknown = (self.swap_ids | self.recompute_ids) - needed
+        if unknown:
+            raise ValueError(f"stage {stage}: memopt names tensors it does not hold: {sorted(unknown)}")
+
+        self.slot_buf: List[Dict[str, torch.Tensor]] = [{} for _ in range(self.w)]
+        self.fwd_scratch: Dict[str, torch.Tensor] = {}
+        self.bwd_scratch: Dict[str, torch.Tensor] = {}
+        self.work: Dict[str, torch.Tensor] = {}
+        self.host: Dict[str, List[torch.Tensor]] = {}
+        ids_needed = {out_tid(n) for n in self._produced_or_received()}
+        ids_needed |= {stats_tid(n.id) for n in self.nodes if n.kind == "ln"}
+        for tid in sorted(ids_needed):
+            shape, dt = self._spec(tid)
+            if tid in needed and tid not in self.swap_ids and tid not in self.recompute_ids:
+                for k in range(self.w):
+                    self.slot_buf[k][tid] = torch.empty(shape, dtype=dt, device=device)
+            elif tid in needed:
+                self.fwd_scratch[tid] = torch.empty(shape, dtype=dt, device=device)
+                self.bwd_scratch[tid] = torch.empty(shape, dtype=dt, device=device)
+                if tid in self.swap_ids:
+                    self.host[tid] = [torch.empty(shape, dtype=dt, pin_memory=True)
+                                      for _ in range(self.w)]
+            else:
+                self.work[tid] = torch.empty(shape, dtype=dt, device=device)
+        if self.is_first:
+            self.ids = [torch.empty(self.M, dtype=torch.int32, device=device) for _ in range(self.w)]
+        if self.is_last:
+            self.labels = [torch.empty(self.M, dtype=torch.int32, device=device) for _ in range(self.w)]
+            self.loss = torch.zeros(1, dtype=F32, device=device)
+        self.swap_out_done: Dict[str, torch.cuda.Event] = {}
+        self.swap_in_done: Dict[str, torch.cuda.Event] = {}
+        self.bwd_done = torch.cuda.Event()
+        self.bwd_done_recorded = False
+        # recompute chains (memopt.py:91-115), replayed in forward order
+        self.chains: Dict[str, List[int]] = {}
+        for tid in sorted(self.recompute_ids):
+            p = self.index[tid.rsplit(".", 1)[0]]
+            chain, _ = producer_chain(g, p, lo, hi)
+            self.chains[tid] = chain
+        # per-slot micro-batch bookkeeping
+        self.slot_mb = [0] * self.w
+        self.grads: Dict[str, torch.Tensor] = {}
+        self.grad_init: Set[str] = set()
+        self.recv_grads: Dict[str, torch.Tensor] = {}
+
+    # ---- helpers -------------------------------------------------------------------
+
+    def _boundary(self, pos: int) -> List[str]:
+        """Output tids crossing the cut after canonical index pos (simulate.py:93-100)."""
+        last = self.g.last_consumer
+        return [out_tid(self.all_nodes[u].id) for u in range(pos + 1) if last[u] > pos]
+
+    def _produced_or_received(self) -> List[str]:
+        ids = [n.id for n in self.nodes]
+        ids += [t.rsplit(".", 1)[0] for t in self.recv_ids]
+        return ids
+
+    def _spec(self, tid: str):
+        nid, kind = tid.rsplit(".", 1)
+        node = self.node_by_id[nid]
+        if kind == "stats":
+            return (2, self.M), F32
+        return output_spec(self.cfg, node, self.b)
+
+    def buf(self, tid: str, slot: int, phase: str) -> torch.Tensor:
+        if tid in self.slot_buf[slot]:
+            return self.slot_buf[slot][tid]
+        if tid in self.fwd_scratch:
+            return self.fwd_scratch[tid] if phase == "fwd" else self.bwd_scratch[tid]
+        if tid in self.work:
+            return self.work[tid]
+        raise KeyError(f"stage {self.stage}: no buffer for {tid}")
+
+    def slot_of(self, mb: int) -> int:
+        return (mb - 1) % self.w
+
+
+    # ---- forward -------------------------------------------------------------------
+
+    def forward(self, mb: int, ids: Optional[torch.Tensor] = None,
+                labels: Optional[torch.Tensor] = None, loss_out: Optional[torch.Tensor] = None) -> None:
+        """Forward of micro-batch mb (1-based).  Boundary inputs must already be in
+        `recv_buffer(tid, mb)`; ids/labels are device int32 [M] for the first/last stage."""
+        st = self.stream
+        slot = self.slot_of(mb)
+        self.slot_mb[slot] = mb
+        ver = self.params.pin_latest(mb)
+        with torch.cuda.stream(st):
+            if self.is_first:
+                self.ids[slot].copy_(ids, non_blocking=True)
+            if self.is_last:
+                self.labels[slot].copy_(labels, non_blocking=True)
+            for tid in self.recv_ids:
+                if tid in self.swap_ids:
+                    self._swap_out(tid, slot)
+            for n in self.nodes:
+                for t in self._outputs(n):
+                    if t in self.swap_out_done and t in self.swap_ids:
+                        st.wait_event(self.swap_out_done[t])  # scratch reuse after D2H
+                self._node_fwd(n, slot, ver, "fwd", loss_out)
+                if out_tid(n.id) in self.swap_ids:
+                    self._swap_out(out_tid(n.id), slot)
+                if stats_tid(n.id) in self.swap_ids:
+                    self._swap_out(stats_tid(n.id), slot)
+
+    def recv_buffer(self, tid: str, mb: int) -> torch.Tensor:
+        return self.buf(tid, self.slot_of(mb), "fwd")
+
+    def send_buffer(self, tid: str, mb: int) -> torch.Tensor:
+        return self.buf(tid, self.slot_of(mb), "fwd")
+
+    def _outputs(self, n: NodeDef) -> List[str]:
+        return [out_tid(n.id)] + ([stats_tid(n.id)] if n.kind == "ln" else [])
+
+    def _swap_out(self, tid: str, slot: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record(self.stream)
+        cs = self.copy_stream
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            self.host[tid][slot].copy_(self.fwd_scratch[tid], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(cs)
+        self.swap_out_done[tid] = done
+
+    def _node_fwd(self, n: NodeDef, slot: int, ver: int, phase: str,
+                  loss_out: Optional[torch.Tensor] = None) -> None:
+        cfg, M, H = self.cfg, self.M, self.cfg.hidden
+        st = self.stream
+        W = lambda pn: self.params.weight(ver, f"{n.id}.{pn}")
+        out = self.buf(out_tid(n.id), slot, phase)
+        inp = [self.buf(out_tid(u), slot, phase) for u in n.inputs]
+        k = n.kind
+        if k == "embed":
+            K.embed_fwd(self.ids[slot], W("tok"), W("pos"), out, cfg.seq, stream=st)
+        elif k == "ln":
+            stats = self.buf(stats_tid(n.id), slot, phase)
+            K.layernorm_fwd(inp[0], W("gamma"), W("beta"), out, stats[0], stats[1], cfg.ln_eps,
+                            stream=st)
+        elif k == "linear":
+            K.linear_fwd(inp[0], W("weight"), out, bias=W("bias"), stream=st)
+        elif k == "linear_res":
+            K.linear_fwd(inp[0], W("weight"), out, bias=W("bias"), residual=inp[1], stream=st)
+        elif k == "gelu":
+            K.gelu_fwd(inp[0], out, stream=st)
+        elif k == "add":
+            K.add(inp[0], inp[1], out, stream=st)
+        elif k == "score":
+            self._scores(inp[0], out)
+            K.softmax_fwd(out, out, cfg.seq, 1.0 / math.sqrt(cfg.head_dim), cfg.causal, stream=st)
+        elif k == "attn":
+            self._pv(inp[0], inp[1], out)
+        elif k == "head":
+            K.linear_fwd(inp[0], W("weight"), out, stream=st)
+            # fused loss + dlogits; on a recompute replay the loss is discarded
+            loss = (loss_out if loss_out is not None else self.loss) if phase == "fwd" else self._scratch_loss()
+            K.xent(out, self.labels[slot], cfg.vocab, 1.0 / M, loss, out, loss_scale=1.0 / M, stream=st)
+        else:
+            raise ValueError(k)
+
+    def _scratch_loss(self):
+        if not hasattr(self, "_sl"):
+            self._sl = torch.zeros(1, dtype=F32, device=self.device)
+        return self._sl
+
+    # attention products straight out of the fused [M, 3H] qkv buffer
+    def _scores(self, qkv, S):
+        cfg = self.cfg
+        s, d, A, H, b = cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        K.gemm_raw(M=s, N=s, K=d, A=qkv, lda=3 * H, a_s=(d, s * 3 * H), B=qkv[:, H:], ldb=3 * H,
+                   b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=S, ldc=s,
+                   c_s=(s * s, A * s * s), stream=self.stream)
+
+    def _pv(self, P, qkv, O):
+        cfg = self.cfg
+        s, d, A, H, b = cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        K.gemm_raw(M=s, N=d, K=s, A=P, lda=s, a_s=(s * s, A * s * s), B=qkv[:, 2 * H:], ldb=3 * H,
+                   b_mn=True, b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=O, ldc=H,
+                   c_s=(d, s * H), stream=self.stream)
+
+    # ---- backward ------------------------------------------------------------------
+
+    def grad_buffer(self, tid: str) -> torch.Tensor:
+        """Gradient buffer for tensor tid (allocated on first use)."""
+        if tid not in self.grads:
+            shape, dt = self._spec(tid)
+            with torch.cuda.stream(self.stream):
+                self.grads[tid] = torch.empty(shape, dtype=BF16, device=self.device)
+        return self.grads[tid]
+
+    def set_recv_grad(self, tid: str, t: torch.Tensor) -> None:
+        self.grads[tid] = t
+        self.grad_init.add(tid)
+
+    def _contribute_identity(self, tid: str, src: torch.Tensor) -> None:
+        """grad[tid] += src, aliasing src when grad[tid] is still empty."""
+        if tid not in self.grad_init:
+            self.grads[tid] = src
+            self.grad_init.add(tid)
+        else:
+            dst = self.grads[tid]
+            K.add(dst, src, dst, stream=self.stream)
+
+    def backward(self, mb: int) -> Dict[str, torch.Tensor]:
+        """Backward of micro-batch mb.  Output-boundary grads must have been handed
+        in with set_recv_grad.  Returns the grads of the recv (input-boundary) tensors."""
+        st = self.stream
+        slot = self.slot_of(mb)
+        assert self.slot_mb[slot] == mb, "slot reused before its backward"
+        ver = self.params.pinned(mb)
+        with torch.cuda.stream(st):
+            self.params.zero_accum_grads(stream=st)
+            # swapped tensors: H2D into the backward scratch
+            if self.swap_ids:
+                cs = self.copy_stream
+                if self.bwd_done_recorded:
+                    cs.wait_event(self.bwd_done)  # previous backward is done with the scratch
+                for tid in sorted(self.swap_ids):
+                    with torch.cuda.stream(cs):
+                        self.bwd_scratch[tid].copy_(self.host[tid][slot], non_blocking=True)
+                    ev = torch.cuda.Event()
+                    ev.record(cs)
+                    self.swap_in_done[tid] = ev
+            # recomputed tensors: replay their producer chains (forward order)
+            if self.recompute_ids:
+                replayed: Set[int] = set()
+                for tid in sorted(self.recompute_ids, key=lambda t: self.index[t.rsplit(".", 1)[0]]):
+                    for i in self.chains[tid]:
+                        if i in replayed:
+                            continue
+                        replayed.add(i)
+                        self._node_fwd_replay(self.all_nodes[i], slot, ver)
+            for tid in self.swap_ids:
+                st.wait_event(self.swap_in_done[tid])
+            for n in reversed(self.nodes):
+                self._node_bwd(n, slot, ver)
+            out = {t: self.grads[t] for t in self.recv_ids if t in self.grads}
+            self.bwd_done.record(st)
+            self.bwd_done_recorded = True
+        return out
+
+    def finish_backward(self, mb: int) -> None:
+        """Optimizer step after micro-batch mb's backward (PipeDream per-micro-batch
+        update); writes the next weight version into the retiring slot."""
+        dst = self.params.retire(mb)
+        with torch.cuda.stream(self.stream):
+            self.params.adamw(dst, self.opt, stream=self.stream)
+        self.grads = {}
+        self.grad_init = set()
+
+    def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
+        # outputs of a replayed node land in the backward scratch if evicted,
+        # else in its normal home (slot buffer or workspace)
+        self._node_fwd(n, slot, ver, "bwd")
+
+    def _node_bwd(self, n: NodeDef, slot: int, ver: int) -> None:
+        cfg, M, H = self.cfg, self.M, self.cfg.hidden
+        st = self.stream
+        P = self.params
+        W = lambda pn: P.weight(ver, f"{n.id}.{pn}")
+        G = lambda pn: P.gradv(f"{n.id}.{pn}")
+        k = n.kind
+        tid = out_tid(n.id)
+        if k == "head":
+            dlog = self.buf(tid, slot, "bwd")
+            x = self.buf(out_tid(n.inputs[0]), slot, "bwd")
+            dx_t = out_tid(n.inputs[0])
+            dx = self.grad_buffer(dx_t)
+            K.linear_dgrad(dlog, W("weight"), dx, accumulate_into=dx if dx_t in self.grad_init else None,
+                           stream=st)
+            self.grad_init.add(dx_t)
+            K.linear_wgrad(dlog, x, G("weight"), stream=st)
+            return
+        if tid not in self.grad_init:
+            return  # nothing flows into this node (cannot happen for a connected graph)
+        dy = self.grads[tid]
+        if k == "embed":
+            K.embed_bwd(self.ids[slot], dy, G("tok"), G("pos"), cfg.seq, stream=st)
+        elif k == "ln":
+            x_t = out_tid(n.inputs[0])
+            x = self.buf(x_t, slot, "bwd")
+            stats = self.buf(stats_tid(n.id), slot, "bwd")
+            if x_t in self.grad_init:
+                dx = self.grads[x_t]
+                K.layernorm_bwd(dy, x, W("gamma"), stats[0], stats[1], dx, G("gamma"), G("beta"),
+                                dx_add=dx, stream=st)
+            else:
+                dx = self.grad_buffer(x_t)
+                K.layernorm_bwd(dy, x, W("gamma"), stats[0], stats[1], dx, G("gamma"), G("beta"),
+                                stream=st)
+                self.grad_init.add(x_t)
+        elif k in ("linear", "linear_res"):
+            x_t = out_tid(n.inputs[0])
+            x = self.buf(x_t, slot, "bwd")
+            if x_t in self.grad_init:
+                dx = self.grads[x_t]
+                K.linear_dgrad(dy, W("weight"), dx, accumulate_into=dx, stream=st)
+            else:
+                dx = self.grad_buffer(x_t)
+                K.linear_dgrad(dy, W("weight"), dx, stream=st)
+                self.grad_init.add(x_t)
+            K.linear_wgrad(dy, x, G("weight"), stream=st)
+            K.colsum(dy, G("bias"), stream=st)
+            if k == "linear_res":
+                self._contribute_identity(out_tid(n.inputs[1]), dy)
+        elif k == "gelu":
+            x_t = out_tid(n.inputs[0])
+            x = self.buf(x_t, slot, "bwd")
+            assert x_t not in self.grad_init
+            K.gelu_bwd(dy, x, dy, stream=st)  # in place: dy buffer becomes df
+            self.grads[x_t] = dy
+            self.grad_init.add(x_t)
+        elif k == "add":
+            self._contribute_identity(out_tid(n.inputs[0]), dy)
+            self._contribute_identity(out_tid(n.inputs[1]), dy)
+        elif k == "attn":
+            P_t, qkv_t = out_tid(n.inputs[0]), out_tid(n.inputs[1])
+            Pm = self.buf(P_t, slot, "bwd")
+            qkv = self.buf(qkv_t, slot, "bwd")
+            dP = self.grad_buffer(P_t)
+            dqkv = self.grad_buffer(qkv_t)
+            s, d, A, b = cfg.seq, cfg.head_dim, cfg.heads, self.b
+            # dP = dO V^T : A = dO (K-major over d), B = V (K-major over d)
+            K.gemm_raw(M=s, N=s, K=d, A=dy, lda=H, a_s=(d, s * H), B=qkv[:, 2 * H:], ldb=3 * H,
+                       b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=dP, ldc=s,
+                       c_s=(s * s, A * s * s), stream=st)
+            # dV = P^T dO : A = P^T (MN-major), B = dO (MN-major, d contiguous)
+            K.gemm_raw(M=s, N=d, K=s, A=Pm, lda=s, a_mn=True, a_s=(s * s, A * s * s), B=dy, ldb=H,
+                       b_mn=True, b_s=(d, s * H), batch1=A, batch2=b, Cout=dqkv[:, 2 * H:],
+                       ldc=3 * H, c_s=(d, s * 3 * H), stream=st)
+            self.grad_init.add(P_t)
+        elif k == "score":
+            qkv_t = out_tid(n.inputs[0])
+            Pm = self.buf(tid, slot, "bwd")
+            qkv = self.buf(qkv_t, slot, "bwd")
+            dqkv = self.grads[qkv_t]
+            s, d, A, b = cfg.seq, cfg.head_dim, cfg.heads, self.b
+            K.softmax_bwd(Pm, dy, dy, 1.0 / math.sqrt(d), stream=st)  # dy := dS (pre-scale folded)
+            # dQ = dS K : A = dS (K-major over keys), B = K (MN-major, d contiguous)
+            K.gemm_raw(M=s, N=d, K=s, A=dy, lda=s, a_s=(s * s, A * s * s), B=qkv[:, H:], ldb=3 * H,
+                       b_mn=True, b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=dqkv, ldc=3 * H,
+                       c_s=(d, s * 3 * H), stream=st)
+            # dK = dS^T Q : A = dS^T (MN-major), B = Q (MN-major)
+            K.gemm_raw(M=s, N=d, K=s, A=dy, lda=s, a_mn=True, a_s=(s * s, A * s * s), B=qkv, ldb=3 * H,
+                       b_mn=True, b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=dqkv[:, H:],
+                       ldc=3 * H, c_s=(d, s * 3 * H), stream=st)
+            self.grad_init.add(qkv_t)
+        else:
+            raise ValueError(k)
