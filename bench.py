@@ -1,0 +1,290 @@
+#!/usr/bin/env python
+"""Throughput of the DawnPiper pipeline-training step on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): BERT-large (24 x 1024, 16 heads, FFN 4096,
+vocab 30522), seq 512, partitioned by this package's planner into an 8-stage
+async-1F1B DawnPiper plan, micro-batch b=8, m=32 micro-batches per step
+(m = 4l, cli.py:226-228), bf16 compute with fp32 master weights, PipeDream
+weight stashing and a per-micro-batch AdamW update.  At N=1 all 8 stages are
+co-located on one GPU; at N>1 (torchrun) the plan has l=N stages, one per GPU.
+
+A step = one pipeline iteration (m micro-batches, b*m samples, every forward,
+backward and optimizer update).  value = samples / device time of K steps
+(CUDA events, max over ranks).  Inputs (weights 1.4 GB + activations) exceed
+the 126 MB L2, so no L2 flush is needed between steps.
+
+The JSON line also carries: e2e (same metric through Pipeline.step with token
+ids / labels copied H2D from pinned host memory and the loss vector read back
+every step), roofline of the dominant kernel (the tcgen05 GEMM: algorithmic
+FLOPs / CUDA-event time of every GEMM launch of one instrumented step),
+cpu_baseline (the oracle CPU port, bounded sample), clocks sampled during the
+timed region, and gpu_launches per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "samples/sec at 1/2/4/8 stages; max trainable batch under per-GPU mem cap"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="bert-large")
+    ap.add_argument("--micro-batch", type=int, default=8)
+    ap.add_argument("--stages", type=int, default=0, help="default: 8 at N=1, N otherwise")
+    ap.add_argument("--micro-batches", type=int, default=32)
+    ap.add_argument("--capacity-gib", type=float, default=160.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks ----
+
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh,
+                stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons, power = [], None, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": sorted(reasons)}
+        # "under load": samples drawing more than half the peak power seen
+        pmax = max(power) if power else 0
+        loaded = sorted(s for s, p in zip(sm, power) if p >= 0.5 * pmax) or sorted(sm)
+        return {"sm_mhz": loaded[len(loaded) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": pmax}
+
+
+# ---------------------------------------------------------------- oracle ----
+
+def cpu_port_sample(model_name: str, stages: int, samples: int = 1):
+    """Time the oracle CPU port (fp32, all host threads) on `samples` samples of
+    the workload: one micro-batch of b=samples through every stage, forward,
+    backward and AdamW, in 1F1B order.  Returns (samples/s, cores, description)."""
+    import torch
+    from oracle.train_ref import reference_train
+    from paper_2505_05856_b200.runtime.model import PRESETS, build_nodes, init_params, synthetic_batch
+    torch.set_num_threads(os.cpu_count() or 1)
+    cfg = PRESETS[model_name]
+    nodes = [n.id for n in build_nodes(cfg)]
+    per = (len(nodes) + stages - 1) // stages
+    stage_nodes = [nodes[i:i + per] for i in range(0, len(nodes), per)]
+    dims = dict(layers=cfg.layers, hidden=cfg.hidden, heads=cfg.heads, seq=cfg.seq,
+                vocab=cfg.vocab, causal=cfg.causal, ln_eps=cfg.ln_eps)
+    init = init_params(cfg, 0)
+    ids, labels = synthetic_batch(cfg, 1, samples, seed=0)
+    opt = dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    t0 = time.perf_counter()
+    reference_train(dims, init, ids, labels, stage_nodes, opt, steps=1)
+    dt = time.perf_counter() - t0
+    return samples / dt, torch.get_num_threads(), (
+        f"{samples} sample(s) of {model_name} s{cfg.seq}: fwd+bwd+AdamW through {len(stage_nodes)} "
+        f"stages in 1F1B order, fp32 torch on CPU, {dt:.1f} s")
+
+
+# ---------------------------------------------------------------- ours ------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2505_05856_b200 import kernels as K
+    from paper_2505_05856_b200 import planner as P
+    from paper_2505_05856_b200.runtime.graph import profile_graph
+    from paper_2505_05856_b200.runtime.model import PRESETS, synthetic_batch
+    from paper_2505_05856_b200.runtime.pipeline import Pipeline, RunConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        from paper_2505_05856_b200.runtime.distributed import run_bench_distributed
+        return run_bench_distributed(args)
+
+    cfg = PRESETS[args.model]
+    b, m = args.micro_batch, args.micro_batches
+    stages = args.stages or 8
+    g = profile_graph(cfg, b)
+    cap = int(args.capacity_gib * (1 << 30))
+    plan = P.plan(g, P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=cap,
+                                  bandwidth=64 << 30))
+    pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, trace=False))
+    ids, labels = synthetic_batch(cfg, m, b, seed=0)
+    ids_d, lab_d = ids.cuda(), labels.cuda()
+    st = pipe.streams[pipe.stage_dev[0]]
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        pipe.step(ids_d, lab_d)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, inputs resident in HBM ----
+    clocks = Clocks(pipe.stage_dev[0])
+    clocks.start()
+    l0 = K.INSTR.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(args.steps):
+        losses = pipe.step(ids_d, lab_d)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    launches = (K.INSTR.launches - l0) // args.steps
+    samples = args.steps * m * b
+    value = samples / (ms / 1e3)
+
+    # ---- e2e: host-pinned inputs copied in, loss read back, every step ----
+    ids_h, lab_h = ids.pin_memory(), labels.pin_memory()
+    loss_h = torch.empty(m, dtype=torch.float32).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        with torch.cuda.stream(st):
+            ids_d.copy_(ids_h, non_blocking=True)
+            lab_d.copy_(lab_h, non_blocking=True)
+        lv = pipe.step(ids_d, lab_d)
+        with torch.cuda.stream(st):
+            loss_h.copy_(lv, non_blocking=True)
+        st.synchronize()
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": samples / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": ids.numel() * 4 + labels.numel() * 4,
+           "d2h_bytes_per_step": m * 4}
+
+    # ---- roofline of the dominant kernel: every GEMM of one step, event-timed ----
+    K.INSTR.gemm_events = []
+    pipe.step(ids_d, lab_d)
+    torch.cuda.synchronize()
+    evs = K.INSTR.gemm_events
+    K.INSTR.gemm_events = None
+    gemm_flops = sum(f for f, _, _ in evs)
+    gemm_ms = sum(a.elapsed_time(c) for _, a, c in evs)
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("bf16_tflops_sustained", 1400.0)
+    achieved = gemm_flops / (gemm_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "kernel": "dpn gemm_kernel (tcgen05, all launches of one step)",
+                "launches_per_step": len(evs), "gemm_ms_per_step": round(gemm_ms, 3),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback"}
+
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": f"{args.model} s{cfg.seq}, {stages}-stage DawnPiper 1F1B plan "
+                               f"co-located on 1 GPU, b={b}, m={m}, weight stashing + AdamW",
+                   "model": args.model, "global_batch": b * m, "seq_len": cfg.seq,
+                   "micro_batch": b, "micro_batches": m, "stages": stages,
+                   "cuts": list(plan.cuts.positions), "parallelism": f"pp{stages} co-located",
+                   "l2": "working set > L2 (no flush needed)"},
+        "model_tflops": round(value * cfg.flops_per_sample() / 1e12, 1),
+        "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk,
+        "losses_last_step": [round(x, 4) for x in losses.tolist()[:4]],
+    }
+    if not args.no_cpu_baseline:
+        v, cores, sample = cpu_port_sample(args.model, stages)
+        out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                               "sample": sample}
+    print(json.dumps(out), flush=True)
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2505_05856_b200.runtime.model import PRESETS
+    stages = args.stages or (8 if world == 1 else world)
+    for _ in range(args.warmup):
+        cpu_port_sample(args.model, stages)
+    vals = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, cores, sample = cpu_port_sample(args.model, stages)
+        vals.append(v)
+    total = time.perf_counter() - t0
+    value = args.steps / total
+    cfg = PRESETS[args.model]
+    out = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{args.model} s{cfg.seq}, {stages}-stage 1F1B, one sample per step "
+                                  f"(CPU port of the training step; the reference dawnplan has no executor)",
+                      "model": args.model, "seq_len": cfg.seq, "stages": stages},
+           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
   __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(xsm);
   __shared__ float red[32];
   const int tid = threadIdx.x, nw = blockDim.x >> 5;
-  const int nvec = vocab >> 3;  // vocab % 8 == 0 required; pad columns are excluded
+  const int nvec = (vocab + 7) >> 3;  // columns >= vocab (pad) are masked out
   for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
     const __nv_bfloat16* src = logits + r * ld;
     float mx = -INFINITY;
@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
       float v[8];
       load8(reinterpret_cast<const __nv_bfloat16*>(&u), v);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) mx = fmaxf(mx, v[k]);
+      for (int k = 0; k < 8; ++k)
+        if (c * 8 + k < vocab) mx = fmaxf(mx, v[k]);
     }
     mx = warp_max(mx);
     if ((tid & 31) == 0) red[tid >> 5] = mx;
@@ -386,7 +387,8 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
       float v[8];
       load8(row + c * 8, v);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) s += __expf(v[k] - mx);
+      for (int k = 0; k < 8; ++k)
+        if (c * 8 + k < vocab) s += __expf(v[k] - mx);
     }
     s = warp_sum(s);
     if ((tid & 31) == 0) red[tid >> 5] = s;
@@ -410,13 +412,14 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
       load8(row + c * 8, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        const float pr = __expf(v[k] - mx) * inv;
-        v[k] = (pr - (c * 8 + k == lab ? 1.f : 0.f)) * grad_scale;
+        const int col = c * 8 + k;
+        const float pr = col < vocab ? __expf(v[k] - mx) * inv : 0.f;
+        v[k] = col < vocab ? (pr - (col == lab ? 1.f : 0.f)) * grad_scale : 0.f;
       }
       store8(dst + c * 8, v);
     }
     // zero the pad columns [vocab, ld) so the dgrad/wgrad GEMMs see clean input
-    for (long long c = vocab + tid; c < ld; c += blockDim.x) dst[c] = __float2bfloat16(0.f);
+    for (long long c = (long long)nvec * 8 + tid; c < ld; c += blockDim.x) dst[c] = __float2bfloat16(0.f);
     __syncthreads();
   }
 }
@@ -613,10 +616,10 @@ extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld,
 extern "C" int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, int64_t rows,
                         int64_t vocab, float grad_scale, float loss_scale, float* loss_sum,
                         void* dlogits, void* stream) {
-  DPN_REQUIRE(vocab % 8 == 0 && ld % 8 == 0 && vocab <= ld, "vocab/ld must be multiples of 8");
-  DPN_REQUIRE(vocab * 2 <= 200 * 1024, "vocab row must fit in shared memory");
+  DPN_REQUIRE(ld % 8 == 0 && (vocab + 7) / 8 * 8 <= ld, "ld must be a multiple of 8 and cover vocab rounded up to 8");
+  DPN_REQUIRE(ld * 2 <= 200 * 1024, "vocab row must fit in shared memory");
   if (rows == 0) return 0;
-  const size_t smem = (size_t)vocab * 2;
+  const size_t smem = (size_t)(vocab + 7) / 8 * 16;
   static bool set = false;
   if (!set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(xent_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

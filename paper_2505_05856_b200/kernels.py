@@ -18,6 +18,25 @@ BF16 = torch.bfloat16
 F32 = torch.float32
 
 
+class _Instrument:
+    """Launch accounting for bench.py: counts every kernel launched through
+    the C ABI and, when `gemm_events` is a list, brackets each GEMM with CUDA
+    events on its own stream (flops, start, end)."""
+
+    def __init__(self):
+        self.launches = 0
+        self.gemm_events = None
+
+
+INSTR = _Instrument()
+
+
+def _torch_stream(stream):
+    if stream is None:
+        return torch.cuda.current_stream()
+    return stream if isinstance(stream, torch.cuda.Stream) else None
+
+
 def _p(t: Optional[torch.Tensor]) -> Optional[int]:
     return None if t is None else t.data_ptr()
 
@@ -51,7 +70,17 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
     g.alpha = float(alpha)
     g.gelu = int(gelu)
     g.block_n = int(block_n)
-    check(lib().dpn_gemm(C.byref(g), _s(stream)), "dpn_gemm")
+    INSTR.launches += 1
+    ev = INSTR.gemm_events
+    if ev is not None:
+        ts = _torch_stream(stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(ts)
+        check(lib().dpn_gemm(C.byref(g), _s(stream)), "dpn_gemm")
+        e1.record(ts)
+        ev.append((2 * int(M) * int(N) * int(K) * int(batch1) * int(batch2), e0, e1))
+    else:
+        check(lib().dpn_gemm(C.byref(g), _s(stream)), "dpn_gemm")
 
 
 # ---- dense-layer shapes -----------------------------------------------------------
@@ -90,6 +119,7 @@ def linear_wgrad(dy, x, dw, accumulate=False, stream=None):
 
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
+    INSTR.launches += 1
     check(lib().dpn_layernorm_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
                                   mean.data_ptr(), rstd.data_ptr(), rows, cols, eps, _s(stream)),
           "dpn_layernorm_fwd")
@@ -97,6 +127,7 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stream=None):
     rows, cols = x.shape
+    INSTR.launches += 1
     check(lib().dpn_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                                   rstd.data_ptr(), dx.data_ptr(), _p(dx_add), dgamma.data_ptr(),
                                   dbeta.data_ptr(), rows, cols, _s(stream)), "dpn_layernorm_bwd")
@@ -105,6 +136,7 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stre
 def softmax_fwd(s, p, q_len, alpha, causal, stream=None):
     cols = s.shape[-1]
     rows = s.numel() // cols
+    INSTR.launches += 1
     check(lib().dpn_softmax_fwd(s.data_ptr(), p.data_ptr(), rows, cols, q_len, alpha, int(causal),
                                 _s(stream)), "dpn_softmax_fwd")
 
@@ -112,53 +144,63 @@ def softmax_fwd(s, p, q_len, alpha, causal, stream=None):
 def softmax_bwd(p, dp, ds, alpha, stream=None):
     cols = p.shape[-1]
     rows = p.numel() // cols
+    INSTR.launches += 1
     check(lib().dpn_softmax_bwd(p.data_ptr(), dp.data_ptr(), ds.data_ptr(), rows, cols, alpha,
                                 _s(stream)), "dpn_softmax_bwd")
 
 
 def gelu_fwd(x, y, stream=None):
+    INSTR.launches += 1
     check(lib().dpn_gelu_fwd(x.data_ptr(), y.data_ptr(), x.numel(), _s(stream)), "dpn_gelu_fwd")
 
 
 def gelu_bwd(dy, x, dx, stream=None):
+    INSTR.launches += 1
     check(lib().dpn_gelu_bwd(dy.data_ptr(), x.data_ptr(), dx.data_ptr(), x.numel(), _s(stream)),
           "dpn_gelu_bwd")
 
 
 def add(a, b, out, stream=None):
+    INSTR.launches += 1
     check(lib().dpn_add(a.data_ptr(), b.data_ptr(), out.data_ptr(), a.numel(), _s(stream)), "dpn_add")
 
 
 def cast_f32_bf16(x, y, stream=None):
+    INSTR.launches += 1
     check(lib().dpn_cast_f32_bf16(x.data_ptr(), y.data_ptr(), x.numel(), _s(stream)),
           "dpn_cast_f32_bf16")
 
 
 def colsum(x, out, stream=None):
     rows, cols = x.shape
+    INSTR.launches += 1
     check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), _s(stream)),
           "dpn_colsum")
 
 
 def xent(logits, labels, vocab, grad_scale, loss_sum, dlogits, loss_scale=1.0, stream=None):
     rows, ld = logits.shape
+    INSTR.launches += 1
     check(lib().dpn_xent(logits.data_ptr(), ld, labels.data_ptr(), rows, vocab, grad_scale,
                          loss_scale, loss_sum.data_ptr(), dlogits.data_ptr(), _s(stream)), "dpn_xent")
 
 
 def embed_fwd(ids, tok, pos, out, seq, stream=None):
     rows = ids.numel()
+    INSTR.launches += 1
     check(lib().dpn_embed_fwd(ids.data_ptr(), tok.data_ptr(), pos.data_ptr(), out.data_ptr(), rows,
                               seq, tok.shape[1], _s(stream)), "dpn_embed_fwd")
 
 
 def embed_bwd(ids, dout, dtok, dpos, seq, stream=None):
     rows = ids.numel()
+    INSTR.launches += 1
     check(lib().dpn_embed_bwd(ids.data_ptr(), dout.data_ptr(), dtok.data_ptr(), dpos.data_ptr(),
                               rows, seq, dout.shape[1], _s(stream)), "dpn_embed_bwd")
 
 
 def adamw(w, m, v, g, out_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
+    INSTR.launches += 1
     check(lib().dpn_adamw(w.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
                           out_bf16.data_ptr(), w.numel(), lr, beta1, beta2, eps, wd, step,
                           _s(stream)), "dpn_adamw")

@@ -207,7 +207,7 @@ def test_gelu_add_cast_colsum():
     close(cs, dy.float().sum(0), rel=5e-3)
 
 
-@pytest.mark.parametrize("vocab,ld", [(1000, 1000), (30520, 30528)])
+@pytest.mark.parametrize("vocab,ld", [(1000, 1000), (30520, 30528), (30522, 30528), (50257, 50304)])
 def test_xent(vocab, ld):
     k = K()
     rows = 257
