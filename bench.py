@@ -215,8 +215,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     evs = K.INSTR.gemm_events
     K.INSTR.gemm_events = None
-    gemm_flops = sum(f for f, _, _ in evs)
-    gemm_ms = sum(a.elapsed_time(c) for _, a, c in evs)
+    gemm_flops = sum(e[0] for e in evs)
+    gemm_ms = sum(e[1].elapsed_time(e[2]) for e in evs)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12

@@ -70,6 +70,7 @@ typedef struct {
   void* aux;
   float alpha; int32_t gelu;
   int32_t block_n; /* 0 = heuristic, else 64 / 128 / 256 */
+  int32_t split_k; /* f32 output without bias/residual/GELU only: 0 = heuristic, 1 = off, n = n splits */
 } dpn_gemm_args;
 int dpn_gemm(const dpn_gemm_args* args, void* stream);
 

@@ -29,6 +29,7 @@ class GemmArgs(C.Structure):
         ("aux", _vp),
         ("alpha", _f32), ("gelu", _i32),
         ("block_n", _i32),
+        ("split_k", _i32),
     ]
 
 

@@ -14,29 +14,37 @@
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128, N=BN,
 //               K=16) into a double-buffered TMEM accumulator
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: tcgen05.ld -> alpha/bias/residual/GELU -> global
+//   warps 4-7   epilogue: tcgen05.ld (a 32-row x 32-column fp32 block per
+//               warp) -> shared-memory transpose -> alpha/bias/residual/GELU
+//               on row-contiguous 16-byte vectors -> coalesced global stores
 // Barriers: full/empty per smem stage (TMA <-> MMA), tmem_full/tmem_empty per
-// accumulator buffer (MMA <-> epilogue), so the epilogue of tile i overlaps
-// the mainloop of tile i+1.
+// accumulator buffer (MMA <-> epilogue), so the epilogue of one work unit
+// overlaps the mainloop of the next.
+//
+// Work units are (tile, k-split) pairs.  Split-K (f32 outputs only) lets the
+// small weight-gradient GEMMs (e.g. 1024 x 1024 x 4096: 32 tiles) fill all
+// 148 SMs; split partials are combined with vector red.global.add.f32.
 #include "common.cuh"
 #include "../../include/dawnpiper.h"
 
 #include <mutex>
-#include <unordered_map>
 
 namespace dpn {
 namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
-constexpr int kThreads = 256;
+constexpr int kEpiWarps = 8;  // two per SM sub-partition: each pair splits the columns
 constexpr int kEpiWarp0 = 4;
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
+constexpr int kEpiSmem = 0;
 
 struct GemmParams {
   int M, N, K;
   int Z1, Z;
   int tiles_m, tiles_n;
-  long long tiles_total;
+  int splits, kb_per_split;
+  long long units;  // tiles * splits
   void* C;
   long long ldc, c_s1, c_s2;
   int c_f32, accumulate;
@@ -55,11 +63,17 @@ struct Cfg {
   static constexpr int kBBytes = BN * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-__device__ __forceinline__ void decode_tile(const GemmParams& p, long long t, int& z1, int& z2,
-                                            int& m0, int& n0) {
+struct Unit {
+  int z1, z2, m0, nb, kb0, kb1;
+};
+
+__device__ __forceinline__ Unit decode(const GemmParams& p, long long u, int nk) {
+  Unit w;
+  const int split = (int)(u % p.splits);
+  const long long t = u / p.splits;
   const long long per_z = (long long)p.tiles_m * p.tiles_n;
   const int z = (int)(t / per_z);
   const int r = (int)(t - (long long)z * per_z);
@@ -70,12 +84,140 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, long long t, in
   const int first_m = g * G;
   const int gsize = min(p.tiles_m - first_m, G);
   const int in_g = r - g * per_group;
-  const int mb = first_m + in_g % gsize;
-  const int nb = in_g / gsize;
-  z1 = z % p.Z1;
-  z2 = z / p.Z1;
-  m0 = mb * BM;
-  n0 = nb;  // scaled by BN by the caller
+  w.m0 = (first_m + in_g % gsize) * BM;
+  w.nb = in_g / gsize;
+  w.z1 = z % p.Z1;
+  w.z2 = z / p.Z1;
+  w.kb0 = split * p.kb_per_split;
+  w.kb1 = min(nk, w.kb0 + p.kb_per_split);
+  return w;
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+// Epilogue of one 32-column chunk: this thread owns row `row` and the fp32
+// accumulators v[0..31] of columns [col0, col0+32).  Each row segment is 64 B
+// (bf16) / 128 B (f32) contiguous, so every 16-byte access fills whole sectors.
+__device__ __forceinline__ void epilogue_chunk(const GemmParams& p, float* v, int row, int col0,
+                                               long long c_base, long long r_base) {
+  if (row >= p.M || col0 >= p.N) return;
+  const bool full = col0 + 32 <= p.N;
+  if (p.alpha != 1.f) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] *= p.alpha;
+  }
+  const long long coff = c_base + (long long)row * p.ldc + col0;
+  if (p.c_f32) {
+    float* cp = reinterpret_cast<float*>(p.C) + coff;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        if (p.splits > 1) {
+          red_add_v4(cp + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else {
+          float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          if (p.accumulate) {
+            const float4 old = reinterpret_cast<const float4*>(cp)[q];
+            o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
+          }
+          reinterpret_cast<float4*>(cp)[q] = o;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (col0 + i < p.N) {
+          if (p.splits > 1) atomicAdd(cp + i, v[i]);
+          else cp[i] = p.accumulate ? cp[i] + v[i] : v[i];
+        }
+      }
+    }
+    return;
+  }
+  if (p.bias) {
+    const __nv_bfloat16* bp = p.bias + col0;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 u = reinterpret_cast<const uint4*>(bp)[q];
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(h[k]);
+          v[8 * q + 2 * k] += f.x;
+          v[8 * q + 2 * k + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < p.N) v[i] += __bfloat162float(bp[i]);
+    }
+  }
+  if (p.res) {
+    const __nv_bfloat16* rp = p.res + r_base + (long long)row * p.ldr + col0;
+    if (full) {
+      uint4 u[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) u[q] = reinterpret_cast<const uint4*>(rp)[q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[q]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(h[k]);
+          v[8 * q + 2 * k] += f.x;
+          v[8 * q + 2 * k + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < p.N) v[i] += __bfloat162float(rp[i]);
+    }
+  }
+  if (p.gelu) {
+    if (p.aux) {
+      __nv_bfloat16* ap = p.aux + coff;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+          u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+          u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+          u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+          reinterpret_cast<uint4*>(ap)[q] = u;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (col0 + i < p.N) ap[i] = __float2bfloat16(v[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+  }
+  __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + coff;
+  if (full) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 u;
+      u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+      u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+      u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+      u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+      reinterpret_cast<uint4*>(cp)[q] = u;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (col0 + i < p.N) cp[i] = __float2bfloat16(v[i]);
+  }
 }
 
 template <int BN, bool A_MN, bool B_MN>
@@ -88,7 +230,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + kEpiSmem);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::kStages;
   uint64_t* tfull = bars + 2 * C::kStages;
@@ -110,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps);  // one arrival per epilogue warp
     }
     fence_mbar_init();
   }
@@ -125,29 +267,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (long long t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
-        int z1, z2, m0, nb;
-        decode_tile(p, t, z1, z2, m0, nb);
-        const int n0 = nb * BN;
-        for (int kb = 0; kb < nk; ++kb) {
+      for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+        const Unit w = decode(p, u, nk);
+        const int n0 = w.nb * BN;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], C::kStageBytes);
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
           const int k0 = kb * BK;
           if (!A_MN) {
-            tma_load_4d(a_dst, &tmA, &full[stage], k0, z1, m0, z2);
+            tma_load_4d(a_dst, &tmA, &full[stage], k0, w.z1, w.m0, w.z2);
           } else {
 #pragma unroll
             for (int j = 0; j < BM / 64; ++j)
-              tma_load_4d(a_dst + j * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * j, z1, k0, z2);
+              tma_load_4d(a_dst + j * 64 * BK * 2, &tmA, &full[stage], w.m0 + 64 * j, w.z1, k0, w.z2);
           }
           if (!B_MN) {
-            tma_load_4d(b_dst, &tmB, &full[stage], k0, z1, n0, z2);
+            tma_load_4d(b_dst, &tmB, &full[stage], k0, w.z1, n0, w.z2);
           } else {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(b_dst + j * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * j, z1, k0, z2);
+              tma_load_4d(b_dst + j * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * j, w.z1, k0, w.z2);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -168,11 +309,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (long long t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
+    for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit w = decode(p, u, nk);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int kb = 0; kb < nk; ++kb) {
+      for (int kb = w.kb0; kb < w.kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -182,10 +324,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t ad = smem_desc_sw128(a_addr + k * a_kstep, a_lbo, 1024);
             const uint64_t bd = smem_desc_sw128(b_addr + k * b_kstep, b_lbo, 1024);
-            umma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_bf16(tmem_d, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
           }
           umma_commit(&empty[stage]);
-          if (kb == nk - 1) umma_commit(&tfull[acc]);
+          if (kb == w.kb1 - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == C::kStages) {
@@ -200,101 +342,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= kEpiWarp0) {
     // ---------------- epilogue ----------------
-    const int ew = warp - kEpiWarp0;  // == warp % 4: owns TMEM lanes 32*ew..
+    const int ew = warp - kEpiWarp0;
+    const int lanes = (warp & 3) * 32;  // TMEM lane quarter this warp may access
+    const int half = ew >> 2;           // which column chunks (even / odd) it owns
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (long long t = blockIdx.x; t < p.tiles_total; t += gridDim.x) {
-      int z1, z2, m0, nb;
-      decode_tile(p, t, z1, z2, m0, nb);
-      const int n0 = nb * BN;
+    for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+      const Unit w = decode(p, u, nk);
+      const int n0 = w.nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m0 + ew * 32 + lane;
-      const bool row_ok = row < p.M;
-      const long long c_off = (long long)z1 * p.c_s1 + (long long)z2 * p.c_s2 + (long long)row * p.ldc;
-      const long long r_off = (long long)z1 * p.r_s1 + (long long)z2 * p.r_s2 + (long long)row * p.ldr;
+      const int row = w.m0 + lanes + lane;
+      const long long c_base = (long long)w.z1 * p.c_s1 + (long long)w.z2 * p.c_s2;
+      const long long r_base = (long long)w.z1 * p.r_s1 + (long long)w.z2 * p.r_s2;
+      const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)lanes << 16);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = half; c < BN / 32; c += 2) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + acc * BN + c * 32 + ((uint32_t)(ew * 32) << 16), r);
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
-        const int col0 = n0 + c * 32;
-        if (!row_ok || col0 >= p.N) continue;
         float v[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * p.alpha;
-        const bool full_chunk = col0 + 32 <= p.N;
-        if (p.bias) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (full_chunk || col0 + i < p.N) v[i] += __bfloat162float(p.bias[col0 + i]);
-        }
-        if (p.res) {
-          const __nv_bfloat16* rp = p.res + r_off + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 u = reinterpret_cast<const uint4*>(rp)[q];
-              const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) v[q * 8 + i] += __bfloat162float(h[i]);
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) v[i] += __bfloat162float(rp[i]);
-          }
-        }
-        if (p.gelu) {
-          if (p.aux) {
-            __nv_bfloat16* ap = p.aux + c_off + col0;
-            if (full_chunk) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                uint4 u;
-                u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-                u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-                u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-                u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-                reinterpret_cast<uint4*>(ap)[q] = u;
-              }
-            } else {
-              for (int i = 0; i < 32 && col0 + i < p.N; ++i) ap[i] = __float2bfloat16(v[i]);
-            }
-          }
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-        }
-        if (p.c_f32) {
-          float* cp = reinterpret_cast<float*>(p.C) + c_off + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 o = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
-              if (p.accumulate) {
-                const float4 old = reinterpret_cast<const float4*>(cp)[q];
-                o.x += old.x; o.y += old.y; o.z += old.z; o.w += old.w;
-              }
-              reinterpret_cast<float4*>(cp)[q] = o;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i)
-              cp[i] = p.accumulate ? cp[i] + v[i] : v[i];
-          }
-        } else {
-          __nv_bfloat16* cp = reinterpret_cast<__nv_bfloat16*>(p.C) + c_off + col0;
-          if (full_chunk) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 u;
-              u.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-              u.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-              u.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-              u.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-              reinterpret_cast<uint4*>(cp)[q] = u;
-            }
-          } else {
-            for (int i = 0; i < 32 && col0 + i < p.N; ++i) cp[i] = __float2bfloat16(v[i]);
-          }
-        }
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        epilogue_chunk(p, v, row, n0 + c * 32, c_base, r_base);
       }
       tc_fence_before();
       __syncwarp();
@@ -387,14 +457,45 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
 
   GemmParams p = p0;
   p.tiles_n = (p.N + BN - 1) / BN;
-  p.tiles_total = (long long)p.tiles_m * p.tiles_n * p.Z;
+  const long long tiles = (long long)p.tiles_m * p.tiles_n * p.Z;
+  const int nk = (p.K + BK - 1) / BK;
+  int splits = 1;
+  if (p.c_f32 && !p.bias && !p.res && !p.gelu && g->split_k != 1) {
+    if (g->split_k > 1) {
+      splits = g->split_k;
+    } else {
+      // minimise waves * k-blocks-per-unit (+ a small charge per extra split)
+      const int sms = sm_count();
+      double best = 1e30;
+      for (int s = 1; s <= 8 && s <= nk; ++s) {
+        const long long units = tiles * s;
+        const double waves = (double)((units + sms - 1) / sms);
+        const double cost = waves * ((nk + s - 1) / s) * (1.0 + 0.04 * (s - 1));
+        if (cost < best - 1e-9) {
+          best = cost;
+          splits = s;
+        }
+      }
+    }
+  }
+  p.kb_per_split = (nk + splits - 1) / splits;
+  p.splits = (nk + p.kb_per_split - 1) / p.kb_per_split;
+  p.units = tiles * p.splits;
+  if (p.splits > 1 && !p.accumulate) {
+    // split partials are reduced with red.add into a zeroed output
+    for (long long z2 = 0; z2 < g->batch2; ++z2)
+      for (long long z1 = 0; z1 < g->batch1; ++z1) {
+        char* base = static_cast<char*>(g->C) + 4 * (z1 * g->c_s1 + z2 * g->c_s2);
+        DPN_CHECK_CUDA(cudaMemset2DAsync(base, g->ldc * 4, 0, g->N * 4, g->M, stream));
+      }
+  }
   auto kern = gemm_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
-  const long long grid = std::min<long long>(p.tiles_total, sm_count());
+  const long long grid = std::min<long long>(p.units, sm_count());
   kern<<<(unsigned)grid, kThreads, C::kSmem, stream>>>(ta, tb, p);
   DPN_LAUNCH_CHECK();
   return 0;
@@ -438,9 +539,10 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   DPN_REQUIRE(g->A && g->B && g->C, "null operand");
   DPN_REQUIRE(g->c_dtype == kF32 || g->c_dtype == kBF16, "c_dtype must be 0 (f32) or 1 (bf16)");
   DPN_REQUIRE(!g->accumulate || g->c_dtype == kF32, "accumulate requires an f32 output");
-  DPN_REQUIRE(g->ldc % 8 == 0 && g->N <= g->ldc || g->M == 1, "ldc must be >= N and a multiple of 8");
+  DPN_REQUIRE(g->ldc % 8 == 0 && g->N <= g->ldc, "ldc must be >= N and a multiple of 8");
   DPN_REQUIRE(!g->aux || g->gelu, "aux output is the pre-GELU value; requires gelu");
   DPN_REQUIRE((reinterpret_cast<uintptr_t>(g->C) & 15) == 0, "C must be 16-byte aligned");
+  DPN_REQUIRE(g->split_k >= 0 && g->split_k <= 64, "split_k must be in [0, 64]");
   GemmParams p{};
   p.M = (int)g->M;
   p.N = (int)g->N;

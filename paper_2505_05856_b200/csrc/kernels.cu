@@ -43,7 +43,10 @@ int grid_for(long long work_items, int per_block) {
 }
 
 // ---------------- LayerNorm ----------------
+// NV = 16-byte chunks per lane (cols = 8 * 32 * NV at most); keeps the row in
+// registers without spilling.
 
+template <int NV>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __restrict__ x,
                                                      const __nv_bfloat16* __restrict__ gamma,
                                                      const __nv_bfloat16* __restrict__ beta,
@@ -57,10 +60,10 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
        r += (long long)gridDim.x * warps) {
     const __nv_bfloat16* xr = x + r * cols;
-    float v[kMaxVec][8];
+    float v[NV][8];
     float s = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
         load8(xr + c * 8, v[j]);
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
     const float mu = warp_sum(s) / cols;
     float q = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
 #pragma unroll
@@ -83,7 +86,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
     }
     const float rs = rsqrtf(warp_sum(q) / cols + eps);
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
         float g[8], b[8], o[8];
@@ -101,9 +104,10 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   }
 }
 
-// dx = rstd * (dyg - mean(dyg) - xhat * mean(dyg * xhat)) [+ dx_in], dyg = dy * gamma.
-// dgamma += sum_rows dy * xhat, dbeta += sum_rows dy (fp32 atomics after an
-// in-CTA reduction).
+// dx = rstd * (dyg - mean(dyg) - xhat * mean(dyg * xhat)) [+ dx_add], dyg = dy * gamma.
+// dgamma += sum_rows dy * xhat, dbeta += sum_rows dy: per-lane register partials,
+// then one shared-memory reduction and one global atomic per column per CTA.
+template <int NV>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
@@ -115,18 +119,18 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
   const int nvec = cols >> 3;
   for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) red[i] = 0.f;
   __syncthreads();
-  float pg[kMaxVec][8], pb[kMaxVec][8];
+  float pg[NV][8], pb[NV][8];
 #pragma unroll
-  for (int j = 0; j < kMaxVec; ++j)
+  for (int j = 0; j < NV; ++j)
 #pragma unroll
     for (int i = 0; i < 8; ++i) pg[j][i] = pb[j][i] = 0.f;
   for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
        r += (long long)gridDim.x * warps) {
     const float mu = mean[r], rs = rstd[r];
-    float xh[kMaxVec][8], g[kMaxVec][8];
+    float xh[NV][8], g[NV][8];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
         float xv[8], dv[8], gm[8];
@@ -147,7 +151,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     s1 = warp_sum(s1) / cols;
     s2 = warp_sum(s2) / cols;
 #pragma unroll
-    for (int j = 0; j < kMaxVec; ++j) {
+    for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
         float o[8];
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     }
   }
 #pragma unroll
-  for (int j = 0; j < kMaxVec; ++j) {
+  for (int j = 0; j < NV; ++j) {
     const int c = lane + 32 * j;
     if (c < nvec) {
 #pragma unroll
@@ -320,29 +324,47 @@ __global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restri
     y[i] = __float2bfloat16(x[i]);
 }
 
-// column sums of a bf16 [rows, cols] matrix (bias gradients): each CTA sums a
-// 256-row band of 8-column strips held per thread, then one atomic per column.
+// column sums of a bf16 [rows, cols] matrix (bias gradients).  A CTA owns up to
+// 256 16-byte column chunks and a band of rows; when the matrix is narrower
+// than 2048 columns several row lanes share a chunk.  Partials are reduced in
+// shared memory, then one atomic per column per CTA.
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
                                                      long long rows, int cols, long long ld,
+                                                     long long rows_per_cta,
                                                      float* __restrict__ out) {
+  __shared__ float part[256 * 8];
   const int nvec = cols >> 3;
-  const long long band = 256;
-  for (long long t = blockIdx.x; t < ((rows + band - 1) / band) * ((nvec + 255) / 256);
-       t += gridDim.x) {
-    const long long rb = t / ((nvec + 255) / 256);
-    const int cb = (int)(t % ((nvec + 255) / 256));
-    const int c = cb * 256 + threadIdx.x;
-    if (c >= nvec) continue;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    const long long r1 = min(rows, (rb + 1) * band);
-    for (long long r = rb * band; r < r1; ++r) {
+  const int cw = min(nvec, 256);       // chunks per CTA
+  const int L = blockDim.x / cw;       // row lanes per chunk
+  const int ci = threadIdx.x % cw, lr = threadIdx.x / cw;
+  const int chunk = blockIdx.y * cw + ci;
+  const bool active = lr < L && chunk < nvec;
+  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  if (active) {
+    for (long long r = r0 + lr; r < r1; r += L) {
       float v[8];
-      load8(x + r * ld + c * 8, v);
+      load8(x + r * ld + chunk * 8, v);
 #pragma unroll
       for (int k = 0; k < 8; ++k) acc[k] += v[k];
     }
+  }
+  if (L > 1) {
+    if (lr < L) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) atomicAdd(&out[c * 8 + k], acc[k]);
+      for (int k = 0; k < 8; ++k) part[threadIdx.x * 8 + k] = acc[k];
+    }
+    __syncthreads();
+    if (lr == 0 && chunk < nvec) {
+      for (int q = 1; q < L; ++q)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] += part[(q * cw + ci) * 8 + k];
+    }
+  }
+  if (lr == 0 && chunk < nvec) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(&out[chunk * 8 + k], acc[k]);
   }
 }
 
@@ -508,15 +530,31 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 using namespace dpn;
 
+#define LN_DISPATCH(KERNEL, GRID, SMEM, ...)                                       \
+  do {                                                                             \
+    const int nv = (int)((cols / 8 + 31) / 32);                                    \
+    cudaStream_t st = (cudaStream_t)stream;                                        \
+    switch (nv) {                                                                  \
+      case 1: KERNEL<1><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      case 2: KERNEL<2><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      case 3: KERNEL<3><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      case 4: KERNEL<4><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      case 5: KERNEL<5><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      case 6: KERNEL<6><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      case 7: KERNEL<7><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
+      default: KERNEL<8><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;             \
+    }                                                                              \
+  } while (0)
+
 extern "C" int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y,
                                  float* mean, float* rstd, int64_t rows, int64_t cols, float eps,
                                  void* stream) {
   DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
   DPN_REQUIRE(aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta), "16-byte alignment");
   if (rows == 0) return 0;
-  ln_fwd_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)beta,
-      (__nv_bfloat16*)y, mean, rstd, rows, (int)cols, eps);
+  LN_DISPATCH(ln_fwd_kernel, grid_for(rows, 8), 0, (const __nv_bfloat16*)x,
+              (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)beta, (__nv_bfloat16*)y, mean, rstd,
+              rows, (int)cols, eps);
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -528,9 +566,9 @@ extern "C" int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamm
   DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
   if (rows == 0) return 0;
   const int grid = (int)std::min<long long>((rows + 7) / 8, 148 * 2);
-  ln_bwd_kernel<<<grid, 256, 2 * cols * sizeof(float), (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, mean, rstd,
-      (__nv_bfloat16*)dx, (const __nv_bfloat16*)dx_add, dgamma, dbeta, rows, (int)cols);
+  LN_DISPATCH(ln_bwd_kernel, grid, 2 * cols * sizeof(float), (const __nv_bfloat16*)dy,
+              (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, mean, rstd, (__nv_bfloat16*)dx,
+              (const __nv_bfloat16*)dx_add, dgamma, dbeta, rows, (int)cols);
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -606,9 +644,14 @@ extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld,
                           void* stream) {
   DPN_REQUIRE(cols % 8 == 0 && ld % 8 == 0, "cols and ld must be multiples of 8");
   if (rows == 0) return 0;
-  const long long tiles = ((rows + 255) / 256) * ((cols / 8 + 255) / 256);
-  colsum_kernel<<<(int)std::min<long long>(tiles, 148 * 8), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)x, rows, (int)cols, ld, out);
+  const long long nvec = cols / 8;
+  const int cw = (int)std::min<long long>(nvec, 256);
+  const int gy = (int)((nvec + cw - 1) / cw);
+  const long long bands = std::max<long long>(1, std::min<long long>((148 + gy - 1) / gy, (rows + 7) / 8));
+  const long long per = (rows + bands - 1) / bands;
+  dim3 grid((unsigned)((rows + per - 1) / per), (unsigned)gy);
+  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, rows, (int)cols, ld,
+                                                        per, out);
   DPN_LAUNCH_CHECK();
   return 0;
 }

@@ -49,7 +49,8 @@ def _s(stream) -> Optional[int]:
 
 def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batch1=1, batch2=1,
              a_s=(0, 0), b_s=(0, 0), c_s=(0, 0), bias=None, residual=None, ldr=None, r_s=None,
-             aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, stream=None) -> None:
+             aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, split_k=0,
+             stream=None) -> None:
     """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules."""
     assert A.dtype == BF16 and B.dtype == BF16 and Cout.dtype in (BF16, F32)
     g = GemmArgs()
@@ -70,6 +71,7 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
     g.alpha = float(alpha)
     g.gelu = int(gelu)
     g.block_n = int(block_n)
+    g.split_k = int(split_k)
     INSTR.launches += 1
     ev = INSTR.gemm_events
     if ev is not None:
@@ -78,7 +80,8 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
         e0.record(ts)
         check(lib().dpn_gemm(C.byref(g), _s(stream)), "dpn_gemm")
         e1.record(ts)
-        ev.append((2 * int(M) * int(N) * int(K) * int(batch1) * int(batch2), e0, e1))
+        ev.append((2 * int(M) * int(N) * int(K) * int(batch1) * int(batch2), e0, e1,
+                   (int(M), int(N), int(K), int(batch1) * int(batch2), int(a_mn), int(b_mn), Cout.dtype == F32)))
     else:
         check(lib().dpn_gemm(C.byref(g), _s(stream)), "dpn_gemm")
 

@@ -261,3 +261,29 @@ def test_adamw():
     torch.cuda.synchronize()
     assert torch.allclose(w, wr.detach(), rtol=1e-5, atol=1e-6)
     assert torch.equal(out, w.to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("split", [2, 3, 0])
+@pytest.mark.parametrize("accumulate", [False, True])
+def test_gemm_split_k_wgrad(split, accumulate):
+    """Split-K partials reduced with red.add.f32 (wgrad shapes with few tiles)."""
+    k = K()
+    M, N, Kd = 256, 384, 1000
+    dy, x = rnd(Kd, M), rnd(Kd, N)
+    dw = torch.randn(M, N, device="cuda")
+    base = dw.clone()
+    k.gemm_raw(M=M, N=N, K=Kd, A=dy, lda=M, a_mn=True, B=x, ldb=N, b_mn=True, Cout=dw, ldc=N,
+               accumulate=accumulate, split_k=split)
+    torch.cuda.synchronize()
+    ref = dy.float().t() @ x.float() + (base if accumulate else 0)
+    close(dw, ref, rel=5e-3)
+
+
+def test_colsum_shapes():
+    k = K()
+    for rows, cols in ((4096, 1024), (4096, 3072), (4096, 4096), (100, 64), (4096, 30528)):
+        x = rnd(rows, cols)
+        out = torch.zeros(cols, device="cuda")
+        k.colsum(x, out)
+        torch.cuda.synchronize()
+        close(out, x.float().sum(0), rel=5e-3)
