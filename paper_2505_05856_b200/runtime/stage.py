@@ -371,6 +371,12 @@ class StageExecutor:
                 self.grads[tid] = torch.empty(shape, dtype=BF16, device=self.device)
         return self.grads[tid]
 
+    def grad_like(self, tid: str) -> torch.Tensor:
+        """A fresh bf16 buffer shaped like tensor tid (receive buffer for a grad)."""
+        shape, _ = self._spec(tid)
+        with torch.cuda.stream(self.stream):
+            return torch.empty(shape, dtype=BF16, device=self.device)
+
     def set_recv_grad(self, tid: str, t: torch.Tensor) -> None:
         self.grads[tid] = t
         self.grad_init.add(tid)

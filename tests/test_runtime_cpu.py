@@ -1,0 +1,74 @@
+"""Host-side runtime logic that needs no GPU: profile graphs built from the
+model definition, the co-located issue order, plan <-> executor tensor naming."""
+import json
+
+import pytest
+
+from paper_2505_05856_b200 import planner as P
+from paper_2505_05856_b200.runtime.graph import out_tid, profile_graph, stats_tid
+from paper_2505_05856_b200.runtime.model import PRESETS, build_nodes, init_params, output_spec
+from paper_2505_05856_b200.runtime.pipeline import colocated_order
+
+
+@pytest.mark.parametrize("name", ["tiny", "bert-base", "bert-large", "gpt2-xl"])
+def test_profile_graph_is_a_valid_schema1_profile(name, tmp_path):
+    cfg = PRESETS[name]
+    g = profile_graph(cfg, 2)
+    assert len(g) == 3 + 10 * cfg.layers
+    f = tmp_path / "p.json"
+    P.save_profile(g, f)
+    g2 = P.load_profile(f)
+    assert P.canonical_hash(g2) == P.canonical_hash(g)
+    # canonical order equals the executor's node order
+    assert [n.id for n in g.nodes] == [n.id for n in build_nodes(cfg)]
+    # every saved tensor names a producer output or LN statistics
+    for n in g.nodes:
+        for t in n.saved:
+            assert t.id in (out_tid(n.id), stats_tid(n.id))
+
+
+def test_profile_loads_in_the_reference_format(tmp_path):
+    """Documents written by the B200 side parse with the strict reference schema
+    rules restated in planner.profile (unknown/missing fields rejected)."""
+    g = profile_graph(PRESETS["tiny"], 2)
+    doc = P.profile_doc(g)
+    doc["nodes"][0]["extra"] = 1
+    with pytest.raises(P.ProfileParseError, match="unknown node field"):
+        P.graph_from_doc(doc)
+
+
+def test_param_count_matches_model_definition():
+    cfg = PRESETS["bert-large"]
+    params = init_params(PRESETS["tiny"], 0)
+    assert sum(t.numel() for t in params.values()) == PRESETS["tiny"].n_params()
+    assert 330e6 < cfg.n_params() < 370e6
+    assert abs(cfg.flops_per_sample() / 1e12 - 1.101) < 0.01
+
+
+@pytest.mark.parametrize("stages,m", [(1, 1), (2, 3), (4, 16), (8, 32)])
+def test_colocated_order_respects_1f1b_and_dependencies(stages, m):
+    order = colocated_order(stages, m)
+    per_stage = {x: [(k, j) for (s, k, j) in order if s == x] for x in range(1, stages + 1)}
+    for x in range(1, stages + 1):
+        assert per_stage[x] == [(k, j) for k, j, _ in P.async_ops(stages, m, x)]
+    pos = {(s, k, j): i for i, (s, k, j) in enumerate(order)}
+    for (s, k, j), i in pos.items():
+        if k == "fwd" and s > 1:
+            assert pos[(s - 1, "fwd", j)] < i
+        if k == "bwd" and s < stages:
+            assert pos[(s + 1, "bwd", j)] < i
+        if k == "bwd":
+            assert pos[(s, "fwd", j)] < i
+
+
+def test_memopt_actions_name_executor_tensors():
+    """Every tensor the planner may evict is one the stage executor can place."""
+    cfg = PRESETS["tiny"]
+    g = profile_graph(cfg, 2)
+    cb = P.compute_balanced(g, 0, len(g) - 1, [1, 1])
+    top = max(s.sched_peak for s in P.stage_profiles(g, cb, 2, P.SCHEDULE_ASYNC))
+    p = P.plan(g, P.PlanConfig(2, P.SCHEDULE_ASYNC, int(0.55 * top), 50 << 20))
+    names = {out_tid(n.id) for n in build_nodes(cfg)} | {stats_tid(n.id) for n in build_nodes(cfg)}
+    acts = [a for m in p.memopt for a in m.actions]
+    assert acts
+    assert all(a.tensor_id in names for a in acts)
