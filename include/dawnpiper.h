@@ -55,7 +55,8 @@ int dpn_enable_peer(int dev, int peer);
  * C[z] = epi(alpha * A[z] B[z]^T), A[z]: M x K, B[z]: N x K, z = z1 + batch1*z2.
  * A K-major: element (m,k) at A + z1*a_s1 + z2*a_s2 + m*lda + k;
  * A MN-major: element (m,k) at A + z1*a_s1 + z2*a_s2 + k*lda + m (same for B).
- * Epilogue: + bias[n] (bf16), + residual (bf16, C layout with ldr/r_s*),
+ * Epilogue: + bias[n] (bf16), + residual (bf16, C layout with ldr/r_s*) or
+ * x gelu'(residual) (residual_mode 1),
  * optional tanh-GELU (aux, if set, receives the pre-GELU value), store as
  * bf16 or f32 (optionally accumulating into f32).  Operand bases 16-byte
  * aligned, lda/ldb/ldc and batch strides multiples of 8 elements. */
@@ -67,10 +68,12 @@ typedef struct {
   void* C; int64_t ldc, c_s1, c_s2; int32_t c_dtype; /* 0 f32, 1 bf16 */ int32_t accumulate;
   const void* bias;
   const void* residual; int64_t ldr, r_s1, r_s2;
+  int32_t residual_mode; /* 0: C += residual; 1: C *= gelu'(residual) (fused GELU backward) */
   void* aux;
   float alpha; int32_t gelu;
   int32_t block_n; /* 0 = heuristic, else 64 / 128 / 256 */
   int32_t split_k; /* f32 output without bias/residual/GELU only: 0 = heuristic, 1 = off, n = n splits */
+  int32_t cta_group; /* 0 = heuristic, 1 = one CTA per tile, 2 = CTA pair (tcgen05 cta_group::2, 256-row tile) */
 } dpn_gemm_args;
 int dpn_gemm(const dpn_gemm_args* args, void* stream);
 
@@ -78,10 +81,13 @@ int dpn_gemm(const dpn_gemm_args* args, void* stream);
 /* ln1 / ln2 / lnf: y = (x - mean) * rstd * gamma + beta; mean/rstd saved (f32 [rows]). */
 int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,
                       float* rstd, int64_t rows, int64_t cols, float eps, void* stream);
-/* dx = LN'(dy) (+ dx_add if non-NULL, may alias dx); dgamma/dbeta += (f32). */
+/* dx = LN'(dy) (+ dx_add if non-NULL, may alias dx); dgamma/dbeta += (f32).
+ * workspace: f32 scratch of >= min(ceil(rows/8), 296) * 2 * cols floats (per-CTA
+ * partials, reduced without atomics); owned by the caller, stream-ordered. */
 int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
                       const float* rstd, void* dx, const void* dx_add, float* dgamma, float* dbeta,
-                      int64_t rows, int64_t cols, void* stream);
+                      int64_t rows, int64_t cols, float* workspace, int64_t workspace_floats,
+                      void* stream);
 /* score: P = softmax(alpha * S) per row; causal masks key > (row % q_len). */
 int dpn_softmax_fwd(const void* s, void* p, int64_t rows, int64_t cols, int64_t q_len, float alpha,
                     int causal, void* stream);
@@ -92,8 +98,10 @@ int dpn_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
 int dpn_gelu_bwd(const void* dy, const void* x, void* dx, int64_t n, void* stream);
 int dpn_add(const void* a, const void* b, void* out, int64_t n, void* stream);
 int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
-/* out[c] += sum_r x[r, c]   (bias gradients) */
-int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out, void* stream);
+/* out[c] += sum_r x[r, c]   (bias gradients); workspace as for layernorm_bwd:
+ * >= min(ceil(296 / ceil(cols/2048)), ceil(rows/8)) * cols floats. */
+int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out, float* workspace,
+               int64_t workspace_floats, void* stream);
 /* head: *loss_sum += loss_scale * sum_r CE(logits[r, :vocab], labels[r]);
  * dlogits = (softmax - onehot) * grad_scale, pad columns [vocab, ld) zeroed.
  * dlogits may alias logits. */

@@ -26,10 +26,12 @@ class GemmArgs(C.Structure):
         ("accumulate", _i32),
         ("bias", _vp),
         ("residual", _vp), ("ldr", _i64), ("r_s1", _i64), ("r_s2", _i64),
+        ("residual_mode", _i32),
         ("aux", _vp),
         ("alpha", _f32), ("gelu", _i32),
         ("block_n", _i32),
         ("split_k", _i32),
+        ("cta_group", _i32),
     ]
 
 
@@ -46,14 +48,14 @@ SIGNATURES = {
     "dpn_enable_peer": [C.c_int, C.c_int],
     "dpn_gemm": [C.POINTER(GemmArgs), _vp],
     "dpn_layernorm_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp],
-    "dpn_layernorm_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp],
+    "dpn_layernorm_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "dpn_softmax_fwd": [_vp, _vp, _i64, _i64, _i64, _f32, C.c_int, _vp],
     "dpn_softmax_bwd": [_vp, _vp, _vp, _i64, _i64, _f32, _vp],
     "dpn_gelu_fwd": [_vp, _vp, _i64, _vp],
     "dpn_gelu_bwd": [_vp, _vp, _vp, _i64, _vp],
     "dpn_add": [_vp, _vp, _vp, _i64, _vp],
     "dpn_cast_f32_bf16": [_vp, _vp, _i64, _vp],
-    "dpn_colsum": [_vp, _i64, _i64, _i64, _vp, _vp],
+    "dpn_colsum": [_vp, _i64, _i64, _i64, _vp, _vp, _i64, _vp],
     "dpn_xent": [_vp, _i64, _vp, _i64, _i64, _f32, _f32, _vp, _vp, _vp],
     "dpn_embed_fwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_embed_bwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],

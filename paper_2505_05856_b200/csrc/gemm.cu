@@ -37,12 +37,11 @@ constexpr int BK = 64;  // one 128-byte swizzle row of bf16
 constexpr int kEpiWarps = 8;  // two per SM sub-partition: each pair splits the columns
 constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
-constexpr int kEpiSmem = 0;
 
 struct GemmParams {
   int M, N, K;
   int Z1, Z;
-  int tiles_m, tiles_n;
+  int tiles_m, tiles_n, tile_m;
   int splits, kb_per_split;
   long long units;  // tiles * splits
   void* C;
@@ -51,19 +50,21 @@ struct GemmParams {
   const __nv_bfloat16* bias;
   const __nv_bfloat16* res;
   long long ldr, r_s1, r_s2;
+  int res_mode;  // 0: + residual, 1: * gelu'(residual) (fused GELU backward)
   __nv_bfloat16* aux;
   float alpha;
   int gelu;
 };
 
-template <int BN>
+template <int BN, int CG>
 struct Cfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kBRows = BN / CG;  // rows of B this CTA loads (pair: half of N)
   static constexpr int kABytes = BM * BK * 2;
-  static constexpr int kBBytes = BN * BK * 2;
+  static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = (200 * 1024) / kStageBytes < 8 ? (200 * 1024) / kStageBytes : 8;
   static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-  static constexpr int kSmem = kStages * kStageBytes + kEpiSmem + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct Unit {
@@ -84,7 +85,7 @@ __device__ __forceinline__ Unit decode(const GemmParams& p, long long u, int nk)
   const int first_m = g * G;
   const int gsize = min(p.tiles_m - first_m, G);
   const int in_g = r - g * per_group;
-  w.m0 = (first_m + in_g % gsize) * BM;
+  w.m0 = (first_m + in_g % gsize) * p.tile_m;
   w.nb = in_g / gsize;
   w.z1 = z % p.Z1;
   w.z2 = z / p.Z1;
@@ -170,14 +171,22 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, float* v, in
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __bfloat1622float2(h[k]);
-          v[8 * q + 2 * k] += f.x;
-          v[8 * q + 2 * k + 1] += f.y;
+          if (p.res_mode == 0) {
+            v[8 * q + 2 * k] += f.x;
+            v[8 * q + 2 * k + 1] += f.y;
+          } else {
+            v[8 * q + 2 * k] *= gelu_tanh_grad(f.x);
+            v[8 * q + 2 * k + 1] *= gelu_tanh_grad(f.y);
+          }
         }
       }
     } else {
 #pragma unroll
       for (int i = 0; i < 32; ++i)
-        if (col0 + i < p.N) v[i] += __bfloat162float(rp[i]);
+        if (col0 + i < p.N) {
+          const float f = __bfloat162float(rp[i]);
+          v[i] = p.res_mode == 0 ? v[i] + f : v[i] * gelu_tanh_grad(f);
+        }
     }
   }
   if (p.gelu) {
@@ -220,17 +229,17 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, float* v, in
   }
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                 const GemmParams p) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes + kEpiSmem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::kStages;
   uint64_t* tfull = bars + 2 * C::kStages;
@@ -240,6 +249,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
+  // CTA pair (CG == 2): rank 0 leads -- it issues the MMAs and owns the
+  // full / tmem_empty barriers both CTAs' producers and epilogues report to.
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  const long long cluster_id = blockIdx.x / CG;
+  const long long n_clusters = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -247,18 +261,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], CG);  // one arrival per producer of the pair
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);  // one arrival per epilogue warp
+      mbar_init(&tempty[a], CG * kEpiWarps);  // one arrival per epilogue warp of the pair
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
+  if (warp == 2) tmem_alloc<C::kTmemCols, CG>(tmem_slot);
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -267,28 +281,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+      for (long long u = cluster_id; u < p.units; u += n_clusters) {
         const Unit w = decode(p, u, nk);
-        const int n0 = w.nb * BN;
+        const int m0 = w.m0 + BM * (int)rank;
+        const int n0 = w.nb * BN + C::kBRows * (int)rank;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], C::kStageBytes);
+          if (rank == 0) mbar_expect_tx(&full[stage], CG * C::kStageBytes);
+          else mbar_arrive_remote(&full[stage], 0);
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
           const int k0 = kb * BK;
+          auto load = [&](void* dst, const CUtensorMap* m, int c0, int c2) {
+            if constexpr (CG == 2) tma_load_4d_pair(dst, m, &full[stage], c0, w.z1, c2, w.z2);
+            else tma_load_4d(dst, m, &full[stage], c0, w.z1, c2, w.z2);
+          };
           if (!A_MN) {
-            tma_load_4d(a_dst, &tmA, &full[stage], k0, w.z1, w.m0, w.z2);
+            load(a_dst, &tmA, k0, m0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_4d(a_dst + j * 64 * BK * 2, &tmA, &full[stage], w.m0 + 64 * j, w.z1, k0, w.z2);
+            for (int j = 0; j < BM / 64; ++j) load(a_dst + j * 64 * BK * 2, &tmA, m0 + 64 * j, k0);
           }
           if (!B_MN) {
-            tma_load_4d(b_dst, &tmB, &full[stage], k0, w.z1, n0, w.z2);
+            load(b_dst, &tmB, k0, n0);
           } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(b_dst + j * 64 * BK * 2, &tmB, &full[stage], n0 + 64 * j, w.z1, k0, w.z2);
+            for (int j = 0; j < C::kBRows / 64; ++j) load(b_dst + j * 64 * BK * 2, &tmB, n0 + 64 * j, k0);
           }
           if (++stage == C::kStages) {
             stage = 0;
@@ -298,46 +316,55 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
-    // K-major SW128: rows of 128 B, 8-row atoms 1024 B apart; +32 B per K=16 step.
-    // MN-major SW128: 64-element MN atoms BK*128 B apart (LBO), 8-row K groups
-    // 1024 B apart (SBO); +16 rows * 128 B = 2048 B per K=16 step.
-    constexpr uint32_t a_lbo = A_MN ? BK * 128 : 16, b_lbo = B_MN ? BK * 128 : 16;
-    constexpr uint32_t a_kstep = A_MN ? 2048 : 32, b_kstep = B_MN ? 2048 : 32;
-    int stage = 0;
-    uint32_t phase = 0;
-    int acc = 0;
-    uint32_t acc_phase = 0;
-    for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
-      const Unit w = decode(p, u, nk);
-      mbar_wait(&tempty[acc], acc_phase ^ 1);
-      tc_fence_after();
-      const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int kb = w.kb0; kb < w.kb1; ++kb) {
-        mbar_wait(&full[stage], phase);
+    // ---------------- MMA issuer (pair leader only) ----------------
+    if (rank == 0) {
+      constexpr uint32_t idesc = idesc_bf16(BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      // K-major SW128: rows of 128 B, 8-row atoms 1024 B apart; +32 B per K=16 step.
+      // MN-major SW128: 64-element MN atoms BK*128 B apart (LBO), 8-row K groups
+      // 1024 B apart (SBO); +16 rows * 128 B = 2048 B per K=16 step.
+      constexpr uint32_t a_lbo = A_MN ? BK * 128 : 16, b_lbo = B_MN ? BK * 128 : 16;
+      constexpr uint32_t a_kstep = A_MN ? 2048 : 32, b_kstep = B_MN ? 2048 : 32;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (long long u = cluster_id; u < p.units; u += n_clusters) {
+        const Unit w = decode(p, u, nk);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
-          const uint32_t b_addr = smem_u32(sB + stage * C::kBBytes);
+        const uint32_t tmem_d = tmem_base + acc * BN;
+        for (int kb = w.kb0; kb < w.kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
+            const uint32_t b_addr = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = smem_desc_sw128(a_addr + k * a_kstep, a_lbo, 1024);
-            const uint64_t bd = smem_desc_sw128(b_addr + k * b_kstep, b_lbo, 1024);
-            umma_bf16(tmem_d, ad, bd, idesc, (kb > w.kb0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t ad = smem_desc_sw128(a_addr + k * a_kstep, a_lbo, 1024);
+              const uint64_t bd = smem_desc_sw128(b_addr + k * b_kstep, b_lbo, 1024);
+              const uint32_t accum = (kb > w.kb0 || k > 0) ? 1u : 0u;
+              if constexpr (CG == 2) umma_bf16_pair(tmem_d, ad, bd, idesc, accum);
+              else umma_bf16(tmem_d, ad, bd, idesc, accum);
+            }
+            if constexpr (CG == 2) {
+              umma_commit_pair(&empty[stage], 0x3);
+              if (kb == w.kb1 - 1) umma_commit_pair(&tfull[acc], 0x3);
+            } else {
+              umma_commit(&empty[stage]);
+              if (kb == w.kb1 - 1) umma_commit(&tfull[acc]);
+            }
           }
-          umma_commit(&empty[stage]);
-          if (kb == w.kb1 - 1) umma_commit(&tfull[acc]);
+          __syncwarp();
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-        __syncwarp();
-        if (++stage == C::kStages) {
-          stage = 0;
-          phase ^= 1;
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
         }
-      }
-      if (++acc == 2) {
-        acc = 0;
-        acc_phase ^= 1;
       }
     }
   } else if (warp >= kEpiWarp0) {
@@ -347,12 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;           // which column chunks (even / odd) it owns
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (long long u = blockIdx.x; u < p.units; u += gridDim.x) {
+    for (long long u = cluster_id; u < p.units; u += n_clusters) {
       const Unit w = decode(p, u, nk);
       const int n0 = w.nb * BN;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = w.m0 + lanes + lane;
+      const int row = w.m0 + BM * (int)rank + lanes + lane;
       const long long c_base = (long long)w.z1 * p.c_s1 + (long long)w.z2 * p.c_s2;
       const long long r_base = (long long)w.z1 * p.r_s1 + (long long)w.z2 * p.r_s2;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)lanes << 16);
@@ -368,7 +395,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -377,10 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_free<C::kTmemCols>(tmem_base);
+    tmem_free<C::kTmemCols, CG>(tmem_base);
   }
 }
 
@@ -438,9 +468,9 @@ int sm_count() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int CG>
 int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   CUtensorMap ta, tb;
   const int Z1 = (int)g->batch1, Z2 = (int)g->batch2;
   int rc;
@@ -450,26 +480,28 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
     rc = make_map(&ta, g->A, g->M, g->K, g->lda, Z1, g->a_s1, Z2, g->a_s2, BK);
   if (rc) return rc;
   if (!B_MN)
-    rc = make_map(&tb, g->B, g->K, g->N, g->ldb, Z1, g->b_s1, Z2, g->b_s2, BN);
+    rc = make_map(&tb, g->B, g->K, g->N, g->ldb, Z1, g->b_s1, Z2, g->b_s2, C::kBRows);
   else
     rc = make_map(&tb, g->B, g->N, g->K, g->ldb, Z1, g->b_s1, Z2, g->b_s2, BK);
   if (rc) return rc;
 
   GemmParams p = p0;
+  p.tile_m = BM * CG;
+  p.tiles_m = (p.M + p.tile_m - 1) / p.tile_m;
   p.tiles_n = (p.N + BN - 1) / BN;
   const long long tiles = (long long)p.tiles_m * p.tiles_n * p.Z;
   const int nk = (p.K + BK - 1) / BK;
+  const int clusters_max = sm_count() / CG;
   int splits = 1;
   if (p.c_f32 && !p.bias && !p.res && !p.gelu && g->split_k != 1) {
     if (g->split_k > 1) {
       splits = g->split_k;
     } else {
       // minimise waves * k-blocks-per-unit (+ a small charge per extra split)
-      const int sms = sm_count();
       double best = 1e30;
       for (int s = 1; s <= 8 && s <= nk; ++s) {
         const long long units = tiles * s;
-        const double waves = (double)((units + sms - 1) / sms);
+        const double waves = (double)((units + clusters_max - 1) / clusters_max);
         const double cost = waves * ((nk + s - 1) / s) * (1.0 + 0.04 * (s - 1));
         if (cost < best - 1e-9) {
           best = cost;
@@ -489,44 +521,57 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
         DPN_CHECK_CUDA(cudaMemset2DAsync(base, g->ldc * 4, 0, g->N * 4, g->M, stream));
       }
   }
-  auto kern = gemm_kernel<BN, A_MN, B_MN>;
+  auto kern = gemm_kernel<BN, A_MN, B_MN, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
     attr_set = true;
   }
-  const long long grid = std::min<long long>(p.units, sm_count());
-  kern<<<(unsigned)grid, kThreads, C::kSmem, stream>>>(ta, tb, p);
-  DPN_LAUNCH_CHECK();
+  const long long clusters = std::min<long long>(p.units, clusters_max);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(clusters * CG));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DPN_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return 0;
 }
 
-template <int BN>
+template <int BN, int CG>
 int dispatch_major(const dpn_gemm_args* g, const GemmParams& p, cudaStream_t s) {
-  if (!g->a_mn_major && !g->b_mn_major) return launch<BN, false, false>(g, p, s);
-  if (!g->a_mn_major && g->b_mn_major) return launch<BN, false, true>(g, p, s);
-  if (g->a_mn_major && !g->b_mn_major) return launch<BN, true, false>(g, p, s);
-  return launch<BN, true, true>(g, p, s);
+  if (!g->a_mn_major && !g->b_mn_major) return launch<BN, false, false, CG>(g, p, s);
+  if (!g->a_mn_major && g->b_mn_major) return launch<BN, false, true, CG>(g, p, s);
+  if (g->a_mn_major && !g->b_mn_major) return launch<BN, true, false, CG>(g, p, s);
+  return launch<BN, true, true, CG>(g, p, s);
 }
 
 }  // namespace
 
-int pick_bn(long long M, long long N, long long Z) {
-  if (N <= 64) return 64;
-  const long long tm = (M + BM - 1) / BM;
-  const int sms = sm_count();
-  long long best_cost = -1;
-  int best = 256;
-  for (int bn : {256, 128}) {
-    const long long tiles = tm * ((N + bn - 1) / bn) * Z;
-    const long long waves = (tiles + sms - 1) / sms;
-    const long long cost = waves * bn;
-    if (best_cost < 0 || cost < best_cost) {
-      best_cost = cost;
-      best = bn;
-    }
+// Tile configuration: (BN, CTA-group).  The 2-CTA 256 x 256 pair tile is the
+// fastest per FLOP (measured, tools/gemm_micro.py: 1065-1402 TFLOP/s vs
+// 700-880 for BN=128 at the pipeline shapes: a narrower tile pays the same
+// per-tile fill / epilogue costs for half the MMA work), so it is used
+// whenever N > 128; N <= 128 takes BN=128 (pair when M > 128); N <= 64 (the
+// attention products with N = head_dim) stays single-CTA BN=64.
+void pick_config(long long M, long long N, long long Z, int& bn, int& cg) {
+  (void)Z;
+  if (N <= 64) {
+    bn = 64;
+    cg = 1;
+  } else if (N <= 128) {
+    bn = 128;
+    cg = M > 128 ? 2 : 1;
+  } else {
+    bn = 256;
+    cg = M > 128 ? 2 : 1;
   }
-  return best;
 }
 
 }  // namespace dpn
@@ -541,6 +586,8 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   DPN_REQUIRE(!g->accumulate || g->c_dtype == kF32, "accumulate requires an f32 output");
   DPN_REQUIRE(g->ldc % 8 == 0 && g->N <= g->ldc, "ldc must be >= N and a multiple of 8");
   DPN_REQUIRE(!g->aux || g->gelu, "aux output is the pre-GELU value; requires gelu");
+  DPN_REQUIRE(g->residual_mode == 0 || (g->residual_mode == 1 && g->residual && !g->gelu),
+              "residual_mode 1 (x gelu'(residual)) needs a residual and no forward GELU");
   DPN_REQUIRE((reinterpret_cast<uintptr_t>(g->C) & 15) == 0, "C must be 16-byte aligned");
   DPN_REQUIRE(g->split_k >= 0 && g->split_k <= 64, "split_k must be in [0, 64]");
   GemmParams p{};
@@ -549,7 +596,6 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   p.K = (int)g->K;
   p.Z1 = (int)g->batch1;
   p.Z = (int)(g->batch1 * g->batch2);
-  p.tiles_m = (p.M + BM - 1) / BM;
   p.C = g->C;
   p.ldc = g->ldc;
   p.c_s1 = g->c_s1;
@@ -561,15 +607,26 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   p.ldr = g->ldr;
   p.r_s1 = g->r_s1;
   p.r_s2 = g->r_s2;
+  p.res_mode = g->residual_mode;
   p.aux = static_cast<__nv_bfloat16*>(g->aux);
   p.alpha = g->alpha;
   p.gelu = g->gelu;
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
-  const int bn = g->block_n > 0 ? g->block_n : pick_bn(g->M, g->N, p.Z);
-  switch (bn) {
-    case 64: return dispatch_major<64>(g, p, s);
-    case 128: return dispatch_major<128>(g, p, s);
-    case 256: return dispatch_major<256>(g, p, s);
-    default: DPN_REQUIRE(false, "block_n must be 0, 64, 128 or 256");
+  int bn = 0, cg = 1;
+  pick_config(g->M, g->N, p.Z, bn, cg);
+  if (g->block_n > 0) {
+    bn = g->block_n;
+    cg = g->cta_group > 0 ? g->cta_group : (bn >= 128 && g->M > 128 ? 2 : 1);
+  } else if (g->cta_group > 0) {
+    cg = g->cta_group;
+  }
+  DPN_REQUIRE(cg == 1 || (cg == 2 && bn >= 128), "cta_group 2 needs block_n 128 or 256");
+  switch (bn * 10 + cg) {
+    case 641: return dispatch_major<64, 1>(g, p, s);
+    case 1281: return dispatch_major<128, 1>(g, p, s);
+    case 2561: return dispatch_major<256, 1>(g, p, s);
+    case 1282: return dispatch_major<128, 2>(g, p, s);
+    case 2562: return dispatch_major<256, 2>(g, p, s);
+    default: DPN_REQUIRE(false, "block_n must be 0, 64, 128 or 256; cta_group 0, 1 or 2");
   }
 }

@@ -105,45 +105,47 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
 }
 
 // dx = rstd * (dyg - mean(dyg) - xhat * mean(dyg * xhat)) [+ dx_add], dyg = dy * gamma.
-// dgamma += sum_rows dy * xhat, dbeta += sum_rows dy: per-lane register partials,
-// then one shared-memory reduction and one global atomic per column per CTA.
+// Two passes over the row (the second hits L1): the row is not kept in
+// registers, so two CTAs fit per SM.  dgamma / dbeta partials live in
+// registers per lane, are combined across the CTA's warps in shared memory
+// (one slot per warp, no atomics) and written as this CTA's partial row.
 template <int NV>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(
+__global__ void __launch_bounds__(256, 2) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
-    float* __restrict__ dgamma, float* __restrict__ dbeta, long long rows, int cols) {
-  extern __shared__ float red[];  // [2][cols]
+    float* __restrict__ partial, long long rows, int cols) {
+  extern __shared__ float red[];  // [warps][2][cols]
   const int warps = blockDim.x >> 5;
+  const int wid = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
-  for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) red[i] = 0.f;
-  __syncthreads();
   float pg[NV][8], pb[NV][8];
 #pragma unroll
   for (int j = 0; j < NV; ++j)
 #pragma unroll
     for (int i = 0; i < 8; ++i) pg[j][i] = pb[j][i] = 0.f;
-  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+  for (long long r = (long long)blockIdx.x * warps + wid; r < rows;
        r += (long long)gridDim.x * warps) {
     const float mu = mean[r], rs = rstd[r];
-    float xh[NV][8], g[NV][8];
+    const __nv_bfloat16* xr = x + r * cols;
+    const __nv_bfloat16* dr = dy + r * cols;
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
         float xv[8], dv[8], gm[8];
-        load8(x + r * cols + c * 8, xv);
-        load8(dy + r * cols + c * 8, dv);
+        load8(xr + c * 8, xv);
+        load8(dr + c * 8, dv);
         load8(gamma + c * 8, gm);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          xh[j][i] = (xv[i] - mu) * rs;
-          g[j][i] = dv[i] * gm[i];
-          s1 += g[j][i];
-          s2 += g[j][i] * xh[j][i];
-          pg[j][i] += dv[i] * xh[j][i];
+          const float xh = (xv[i] - mu) * rs;
+          const float g = dv[i] * gm[i];
+          s1 += g;
+          s2 += g * xh;
+          pg[j][i] += dv[i] * xh;
           pb[j][i] += dv[i];
         }
       }
@@ -154,9 +156,12 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
     for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
-        float o[8];
+        float xv[8], dv[8], gm[8], o[8];
+        load8(xr + c * 8, xv);
+        load8(dr + c * 8, dv);
+        load8(gamma + c * 8, gm);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = rs * (g[j][i] - s1 - xh[j][i] * s2);
+        for (int i = 0; i < 8; ++i) o[i] = rs * (dv[i] * gm[i] - s1 - (xv[i] - mu) * rs * s2);
         if (dx_add) {
           float a[8];
           load8(dx_add + r * cols + c * 8, a);
@@ -167,21 +172,50 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(
       }
     }
   }
+  float* mine = red + (long long)wid * 2 * cols;
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     const int c = lane + 32 * j;
     if (c < nvec) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        atomicAdd(&red[c * 8 + i], pg[j][i]);
-        atomicAdd(&red[cols + c * 8 + i], pb[j][i]);
+        mine[c * 8 + i] = pg[j][i];
+        mine[cols + c * 8 + i] = pb[j][i];
       }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < cols; i += blockDim.x) {
-    atomicAdd(&dgamma[i], red[i]);
-    atomicAdd(&dbeta[i], red[cols + i]);
+  float* dst = partial + (long long)blockIdx.x * 2 * cols;
+  for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) {
+    float t = 0.f;
+    for (int w = 0; w < warps; ++w) t += red[(long long)w * 2 * cols + i];
+    dst[i] = t;
+  }
+}
+
+// out[c] += sum_b partial[b][c] over `nrows` partial rows of width `width`
+// (phase 2 of the atomic-free column reductions).  A CTA owns 32 columns; its
+// 32 warps stride over the partial rows (coalesced 128-byte row segments) and
+// combine through shared memory.
+__global__ void __launch_bounds__(1024) reduce_rows_kernel(const float* __restrict__ partial,
+                                                           int nrows, int width,
+                                                           float* __restrict__ out0,
+                                                           float* __restrict__ out1, int split) {
+  __shared__ float acc_s[32][33];
+  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  float acc = 0.f;
+  if (c < width) {
+    for (int b = wy; b < nrows; b += 32) acc += partial[(long long)b * width + c];
+  }
+  acc_s[wy][lane] = acc;
+  __syncthreads();
+  if (wy == 0 && c < width) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < 32; ++q) t += acc_s[q][lane];
+    if (c < split) out0[c] += t;
+    else out1[c - split] += t;
   }
 }
 
@@ -327,11 +361,12 @@ __global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restri
 // column sums of a bf16 [rows, cols] matrix (bias gradients).  A CTA owns up to
 // 256 16-byte column chunks and a band of rows; when the matrix is narrower
 // than 2048 columns several row lanes share a chunk.  Partials are reduced in
-// shared memory, then one atomic per column per CTA.
+// shared memory and written as this CTA's partial row; a second pass sums the
+// partial rows into the output (no contended atomics).
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
                                                      long long rows, int cols, long long ld,
                                                      long long rows_per_cta,
-                                                     float* __restrict__ out) {
+                                                     float* __restrict__ partial) {
   __shared__ float part[256 * 8];
   const int nvec = cols >> 3;
   const int cw = min(nvec, 256);       // chunks per CTA
@@ -363,8 +398,9 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
     }
   }
   if (lr == 0 && chunk < nvec) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) atomicAdd(&out[chunk * 8 + k], acc[k]);
+    float* dst = partial + (long long)blockIdx.x * cols + chunk * 8;
+    *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
 }
 
@@ -562,13 +598,32 @@ extern "C" int dpn_layernorm_fwd(const void* x, const void* gamma, const void* b
 extern "C" int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamma,
                                  const float* mean, const float* rstd, void* dx,
                                  const void* dx_add, float* dgamma, float* dbeta, int64_t rows,
-                                 int64_t cols, void* stream) {
+                                 int64_t cols, float* workspace, int64_t workspace_floats,
+                                 void* stream) {
   DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
   if (rows == 0) return 0;
   const int grid = (int)std::min<long long>((rows + 7) / 8, 148 * 2);
-  LN_DISPATCH(ln_bwd_kernel, grid, 2 * cols * sizeof(float), (const __nv_bfloat16*)dy,
+  DPN_REQUIRE(workspace != nullptr && workspace_floats >= (long long)grid * 2 * cols,
+              "workspace must hold min(ceil(rows/8), 296) * 2 * cols floats");
+  static bool smem_set = false;
+  if (!smem_set) {
+    const int mx = 8 * 2 * 2048 * (int)sizeof(float);
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    smem_set = true;
+  }
+  LN_DISPATCH(ln_bwd_kernel, grid, 8 * 2 * cols * sizeof(float), (const __nv_bfloat16*)dy,
               (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, mean, rstd, (__nv_bfloat16*)dx,
-              (const __nv_bfloat16*)dx_add, dgamma, dbeta, rows, (int)cols);
+              (const __nv_bfloat16*)dx_add, workspace, rows, (int)cols);
+  DPN_LAUNCH_CHECK();
+  reduce_rows_kernel<<<(unsigned)((2 * cols + 31) / 32), 1024, 0, (cudaStream_t)stream>>>(
+      workspace, grid, (int)(2 * cols), dgamma, dbeta, (int)cols);
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -641,17 +696,23 @@ extern "C" int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* strea
 }
 
 extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out,
-                          void* stream) {
+                          float* workspace, int64_t workspace_floats, void* stream) {
   DPN_REQUIRE(cols % 8 == 0 && ld % 8 == 0, "cols and ld must be multiples of 8");
   if (rows == 0) return 0;
   const long long nvec = cols / 8;
   const int cw = (int)std::min<long long>(nvec, 256);
   const int gy = (int)((nvec + cw - 1) / cw);
-  const long long bands = std::max<long long>(1, std::min<long long>((148 + gy - 1) / gy, (rows + 7) / 8));
+  const long long bands = std::max<long long>(1, std::min<long long>((296 + gy - 1) / gy, (rows + 7) / 8));
   const long long per = (rows + bands - 1) / bands;
-  dim3 grid((unsigned)((rows + per - 1) / per), (unsigned)gy);
+  const long long nb = (rows + per - 1) / per;
+  DPN_REQUIRE(workspace != nullptr && workspace_floats >= nb * cols,
+              "workspace must hold min(ceil(296 / ceil(cols/2048)), ceil(rows/8)) * cols floats");
+  dim3 grid((unsigned)nb, (unsigned)gy);
   colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, rows, (int)cols, ld,
-                                                        per, out);
+                                                        per, workspace);
+  DPN_LAUNCH_CHECK();
+  reduce_rows_kernel<<<(unsigned)((cols + 31) / 32), 1024, 0, (cudaStream_t)stream>>>(
+      workspace, (int)nb, (int)cols, out, out, (int)cols);
   DPN_LAUNCH_CHECK();
   return 0;
 }

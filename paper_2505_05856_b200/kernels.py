@@ -31,6 +31,20 @@ class _Instrument:
 INSTR = _Instrument()
 
 
+_WS = {}
+
+
+def _workspace(device, floats: int) -> torch.Tensor:
+    """Per-(device, stream) f32 scratch for two-phase column reductions.  Kernels
+    on one stream use it in stream order; streams never share one."""
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    t = _WS.get(key)
+    if t is None or t.numel() < floats:
+        t = torch.empty(max(floats, 1 << 20), dtype=F32, device=device)
+        _WS[key] = t
+    return t
+
+
 def _torch_stream(stream):
     if stream is None:
         return torch.cuda.current_stream()
@@ -50,7 +64,7 @@ def _s(stream) -> Optional[int]:
 def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batch1=1, batch2=1,
              a_s=(0, 0), b_s=(0, 0), c_s=(0, 0), bias=None, residual=None, ldr=None, r_s=None,
              aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, split_k=0,
-             stream=None) -> None:
+             cta_group=0, residual_mode=0, stream=None) -> None:
     """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules."""
     assert A.dtype == BF16 and B.dtype == BF16 and Cout.dtype in (BF16, F32)
     g = GemmArgs()
@@ -67,11 +81,13 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
         g.ldr = int(ldr if ldr is not None else ldc)
         rs = r_s if r_s is not None else c_s
         g.r_s1, g.r_s2 = int(rs[0]), int(rs[1])
+        g.residual_mode = int(residual_mode)
     g.aux = _p(aux)
     g.alpha = float(alpha)
     g.gelu = int(gelu)
     g.block_n = int(block_n)
     g.split_k = int(split_k)
+    g.cta_group = int(cta_group)
     INSTR.launches += 1
     ev = INSTR.gemm_events
     if ev is not None:
@@ -99,14 +115,17 @@ def linear_fwd(x, w, out, bias=None, residual=None, gelu=False, aux=None, stream
              stream=stream)
 
 
-def linear_dgrad(dy, w, dx, accumulate_into=None, stream=None):
+def linear_dgrad(dy, w, dx, accumulate_into=None, gelu_of=None, stream=None):
     """dx[M, K] = dy[M, N] @ w[N, K]  (w used MN-major: no transpose copy).
-    accumulate_into: a bf16 [M, K] tensor added to the result (may be dx)."""
+    accumulate_into: a bf16 [M, K] tensor added to the result (may be dx);
+    gelu_of: pre-activation f [M, K]: dx *= gelu'(f) (fused GELU backward)."""
     M, N = dy.shape
     K = w.shape[1]
+    assert accumulate_into is None or gelu_of is None
+    res = accumulate_into if gelu_of is None else gelu_of
     gemm_raw(M=M, N=K, K=N, A=dy, lda=dy.stride(0), B=w, ldb=w.stride(0), b_mn=True, Cout=dx,
-             ldc=dx.stride(0), residual=accumulate_into,
-             ldr=None if accumulate_into is None else accumulate_into.stride(0), stream=stream)
+             ldc=dx.stride(0), residual=res, ldr=None if res is None else res.stride(0),
+             residual_mode=0 if gelu_of is None else 1, stream=stream)
 
 
 def linear_wgrad(dy, x, dw, accumulate=False, stream=None):
@@ -130,10 +149,13 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
 
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stream=None):
     rows, cols = x.shape
-    INSTR.launches += 1
+    INSTR.launches += 2
+    with torch.cuda.stream(_torch_stream(stream)):
+        ws = _workspace(x.device, 296 * 2 * cols)
     check(lib().dpn_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                                   rstd.data_ptr(), dx.data_ptr(), _p(dx_add), dgamma.data_ptr(),
-                                  dbeta.data_ptr(), rows, cols, _s(stream)), "dpn_layernorm_bwd")
+                                  dbeta.data_ptr(), rows, cols, ws.data_ptr(), ws.numel(),
+                                  _s(stream)), "dpn_layernorm_bwd")
 
 
 def softmax_fwd(s, p, q_len, alpha, causal, stream=None):
@@ -176,9 +198,11 @@ def cast_f32_bf16(x, y, stream=None):
 
 def colsum(x, out, stream=None):
     rows, cols = x.shape
-    INSTR.launches += 1
-    check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), _s(stream)),
-          "dpn_colsum")
+    INSTR.launches += 2
+    with torch.cuda.stream(_torch_stream(stream)):
+        ws = _workspace(x.device, 296 * cols)
+    check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), ws.data_ptr(),
+                           ws.numel(), _s(stream)), "dpn_colsum")
 
 
 def xent(logits, labels, vocab, grad_scale, loss_sum, dlogits, loss_scale=1.0, stream=None):

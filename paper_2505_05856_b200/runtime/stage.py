@@ -225,6 +225,20 @@ class StageExecutor:
         self.grads: Dict[str, torch.Tensor] = {}
         self.grad_init: Set[str] = set()
         self.recv_grads: Dict[str, torch.Tensor] = {}
+        # GELU fused into its neighbours' GEMM epilogues when fc1 -> gelu -> fc2
+        # live in this stage: fc1's forward writes f (aux) and gelu(f); fc2's
+        # dgrad writes df = (dz W2) * gelu'(f) straight into f's gradient.
+        self.fwd_gelu_of: Dict[str, str] = {}   # fc1 id -> gelu id
+        self.bwd_gelu_of: Dict[str, str] = {}   # fc2 id -> gelu id
+        for n in self.nodes:
+            if n.kind == "gelu" and n.inputs[0] in in_stage:
+                src = self.node_by_id[n.inputs[0]]
+                if src.kind == "linear":
+                    self.fwd_gelu_of[src.id] = n.id
+                users = [c for c in self.nodes if n.id in c.inputs]
+                if len(users) == 1 and users[0].kind == "linear":
+                    self.bwd_gelu_of[users[0].id] = n.id
+        self._skip_bwd: Set[str] = set()
 
     # ---- helpers -------------------------------------------------------------------
 
@@ -293,7 +307,10 @@ class StageExecutor:
         return self.buf(tid, self.slot_of(mb), "fwd")
 
     def _outputs(self, n: NodeDef) -> List[str]:
-        return [out_tid(n.id)] + ([stats_tid(n.id)] if n.kind == "ln" else [])
+        outs = [out_tid(n.id)] + ([stats_tid(n.id)] if n.kind == "ln" else [])
+        if n.id in self.fwd_gelu_of:
+            outs.append(out_tid(self.fwd_gelu_of[n.id]))
+        return outs
 
     def _swap_out(self, tid: str, slot: int) -> None:
         ev = torch.cuda.Event()
@@ -321,11 +338,17 @@ class StageExecutor:
             K.layernorm_fwd(inp[0], W("gamma"), W("beta"), out, stats[0], stats[1], cfg.ln_eps,
                             stream=st)
         elif k == "linear":
-            K.linear_fwd(inp[0], W("weight"), out, bias=W("bias"), stream=st)
+            g_id = self.fwd_gelu_of.get(n.id) if phase == "fwd" else None
+            if g_id is not None:  # out = f (pre-activation), gelu node's buffer = gelu(f)
+                K.linear_fwd(inp[0], W("weight"), self.buf(out_tid(g_id), slot, phase),
+                             bias=W("bias"), gelu=True, aux=out, stream=st)
+            else:
+                K.linear_fwd(inp[0], W("weight"), out, bias=W("bias"), stream=st)
         elif k == "linear_res":
             K.linear_fwd(inp[0], W("weight"), out, bias=W("bias"), residual=inp[1], stream=st)
         elif k == "gelu":
-            K.gelu_fwd(inp[0], out, stream=st)
+            if not (phase == "fwd" and n.inputs[0] in self.fwd_gelu_of):
+                K.gelu_fwd(inp[0], out, stream=st)
         elif k == "add":
             K.add(inp[0], inp[1], out, stream=st)
         elif k == "score":
@@ -436,6 +459,7 @@ class StageExecutor:
             self.params.adamw(dst, self.opt, stream=self.stream)
         self.grads = {}
         self.grad_init = set()
+        self._skip_bwd = set()
 
     def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
         # outputs of a replayed node land in the backward scratch if evicted,
@@ -481,7 +505,16 @@ class StageExecutor:
         elif k in ("linear", "linear_res"):
             x_t = out_tid(n.inputs[0])
             x = self.buf(x_t, slot, "bwd")
-            if x_t in self.grad_init:
+            g_id = self.bwd_gelu_of.get(n.id)
+            if g_id is not None and x_t not in self.grad_init:
+                # fused GELU backward: the dgrad epilogue multiplies by gelu'(f) and
+                # lands in f's gradient; the gelu node's own backward is skipped
+                f_t = out_tid(self.node_by_id[g_id].inputs[0])
+                df = self.grad_buffer(f_t)
+                K.linear_dgrad(dy, W("weight"), df, gelu_of=self.buf(f_t, slot, "bwd"), stream=st)
+                self.grad_init.add(f_t)
+                self._skip_bwd.add(g_id)
+            elif x_t in self.grad_init:
                 dx = self.grads[x_t]
                 K.linear_dgrad(dy, W("weight"), dx, accumulate_into=dx, stream=st)
             else:
@@ -493,6 +526,8 @@ class StageExecutor:
             if k == "linear_res":
                 self._contribute_identity(out_tid(n.inputs[1]), dy)
         elif k == "gelu":
+            if n.id in self._skip_bwd:
+                return
             x_t = out_tid(n.inputs[0])
             x = self.buf(x_t, slot, "bwd")
             assert x_t not in self.grad_init

@@ -39,9 +39,12 @@ def rnd(*shape, dtype=torch.bfloat16, scale=1.0):
 
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
-@pytest.mark.parametrize("M,N,K_,bn", [(256, 256, 128, 0), (300, 200, 96, 0), (128, 64, 64, 64),
-                                        (512, 768, 1024, 256), (384, 1024, 512, 128), (77, 136, 40, 0)])
-def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn):
+@pytest.mark.parametrize("M,N,K_,bn,cg", [(256, 256, 128, 0, 0), (300, 200, 96, 0, 0), (128, 64, 64, 64, 1),
+                                           (512, 768, 1024, 256, 1), (384, 1024, 512, 128, 1),
+                                           (77, 136, 40, 0, 0), (512, 768, 1024, 256, 2),
+                                           (384, 1024, 512, 128, 2), (700, 520, 200, 256, 2),
+                                           (200, 384, 64, 128, 2)])
+def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn, cg):
     k = K()
     A = rnd(M, K_)
     B = rnd(N, K_)
@@ -53,7 +56,7 @@ def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn):
         pytest.skip("TMA needs 16-byte strides")
     C = torch.empty(M, (N + 7) // 8 * 8, device="cuda", dtype=torch.float32)
     k.gemm_raw(M=M, N=N, K=K_, A=As, lda=lda, a_mn=a_mn, B=Bs, ldb=ldb, b_mn=b_mn, Cout=C,
-               ldc=C.stride(0), block_n=bn)
+               ldc=C.stride(0), block_n=bn, cta_group=cg)
     torch.cuda.synchronize()
     ref = A.float() @ B.float().t()
     close(C[:, :N], ref, rel=5e-3)
@@ -287,3 +290,16 @@ def test_colsum_shapes():
         k.colsum(x, out)
         torch.cuda.synchronize()
         close(out, x.float().sum(0), rel=5e-3)
+
+
+def test_gemm_fused_gelu_backward():
+    """dgrad epilogue residual_mode 1: dx = (dy @ w) * gelu'(f)."""
+    k = K()
+    M, N, Kd = 512, 768, 256
+    dy, w, f = rnd(M, Kd), rnd(Kd, N, scale=0.05), rnd(M, N)
+    dx = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    k.linear_dgrad(dy, w, dx, gelu_of=f)
+    fr = f.float().requires_grad_()
+    torch.nn.functional.gelu(fr, approximate="tanh").backward(dy.float() @ w.float())
+    torch.cuda.synchronize()
+    close(dx, fr.grad)
