@@ -1,0 +1,199 @@
+"""Max trainable micro-batch under a per-GPU memory cap (the second half of
+BASELINE.json's metric; SURVEY.md 8(d) "Max-batch metric").
+
+For each micro-batch size b:
+  1. build the model's profile graph at b (runtime/graph.py; analytic or
+     measured node times),
+  2. plan it with the planner at the cap minus the memory the planner's model
+     does not see (fp32 master / Adam m / Adam v / grad: 16 B per parameter,
+     plus a fixed workspace reserve),
+  3. run every stage of the plan *on the GPU under the cap*: the stage's own
+     executor (weights, w = l-x+1 weight versions and activation slots, the
+     plan's swap / recompute actions) runs its real 1F1B op list for
+     m = w + 1 micro-batches with synthetic boundary activations / gradients
+     standing in for its neighbours.  The cap is enforced on the caching
+     allocator (torch.cuda.set_per_process_memory_fraction); an allocation
+     beyond it raises OutOfMemoryError.
+b is trainable iff the planner returns a plan and every stage completes.
+
+The baseline is the even-compute split: `compute_balanced` cuts with empty
+memopt plans (`plan_from_cuts(..., require_feasible=False)`, as the reference
+CLI's `compare` builds it, cli.py:276-300), checked the same way.
+"""
+
+from __future__ import annotations
+
+import gc
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Tuple
+
+import torch
+
+from .. import planner as P
+from .._lib import init_device
+from ..planner.memplan import MemOptPlan
+from ..planner.schedule import async_ops
+from .graph import profile_graph
+from .model import TransformerConfig, build_nodes, init_params
+from .stage import StageExecutor
+
+GIB = 1 << 30
+
+
+@dataclass
+class StageCheck:
+    stage: int
+    ok: bool
+    peak_bytes: int
+    error: str = ""
+
+
+def optimizer_reserve(model: TransformerConfig, g, stages: int, workspace: int = 3 * GIB) -> int:
+    """Bytes per GPU the planner's memory model leaves out: 16 B/param of fp32
+    state for the largest stage of the compute-balanced split, plus workspace."""
+    cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)
+    bounds = P.stage_bounds(cb, len(g))
+    max_params = max(g.segment_params(lo, hi) for lo, hi in bounds) // 2  # m_p = 2 B/param
+    return 16 * max_params + workspace
+
+
+def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, device: int = 0,
+                micro_batches: Optional[int] = None, init=None) -> StageCheck:
+    """Run stage x of `plan` alone under a `cap`-byte allocator limit."""
+    dev = torch.device("cuda", device)
+    init_device(device)
+    l = len(plan.stages)
+    lo, hi = P.stage_bounds(plan.cuts, len(g))[x - 1]
+    total = torch.cuda.get_device_properties(device).total_memory
+    gc.collect()
+    torch.cuda.empty_cache()
+    torch.cuda.reset_peak_memory_stats(device)
+    torch.cuda.set_per_process_memory_fraction(min(1.0, cap / total), device)
+    ex = None
+    try:
+        stream = torch.cuda.Stream(device=dev)
+        ex = StageExecutor(cfg=model, g=g, nodes=build_nodes(model), lo=lo, hi=hi, stage=x,
+                           stages=l, micro_batch=b, memopt=plan.memopt[x - 1],
+                           init=init if init is not None else init_params(model, 0),
+                           device=dev, stream=stream)
+        w = l - x + 1
+        m = micro_batches or (w + 1)
+        M = b * model.seq
+        gen = torch.Generator(device=dev).manual_seed(x)
+        ids = torch.randint(0, model.vocab, (m, M), device=dev, dtype=torch.int32, generator=gen)
+        loss = torch.zeros(m, device=dev)
+        with torch.cuda.stream(stream):
+            for kind, j, _ in async_ops(l, m, x):
+                if kind == "fwd":
+                    for tid in ex.recv_ids:
+                        buf = ex.recv_buffer(tid, j)
+                        buf.normal_(0, 1, generator=gen) if buf.is_floating_point() else None
+                    ex.forward(j, ids=ids[j - 1] if ex.is_first else None,
+                               labels=ids[j - 1] if ex.is_last else None,
+                               loss_out=loss[j - 1:j] if ex.is_last else None)
+                else:
+                    for tid in ex.send_ids:
+                        gbuf = ex.grad_like(tid)
+                        gbuf.normal_(0, 1e-3, generator=gen)
+                        ex.set_recv_grad(tid, gbuf)
+                    ex.backward(j)
+                    ex.finish_backward(j)
+        torch.cuda.synchronize(device)
+        return StageCheck(x, True, torch.cuda.max_memory_allocated(device))
+    except torch.OutOfMemoryError as e:
+        return StageCheck(x, False, torch.cuda.max_memory_allocated(device), str(e).split("\n")[0][:200])
+    finally:
+        del ex
+        gc.collect()
+        torch.cuda.synchronize(device)
+        torch.cuda.empty_cache()
+        torch.cuda.set_per_process_memory_fraction(1.0, device)
+
+
+def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth: int,
+              strategy: str, device: int = 0, times=None, run_gpu: bool = True) -> dict:
+    g = profile_graph(model, b, times=times)
+    reserve = optimizer_reserve(model, g, stages)
+    pcap = cap - reserve
+    rec = {"b": b, "strategy": strategy, "planner_capacity": pcap, "reserve": reserve}
+    cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=max(1, pcap),
+                       bandwidth=bandwidth)
+    if pcap <= 0:
+        rec.update(feasible=False, reason="optimizer state alone exceeds the cap")
+        return rec
+    if strategy == "dawnpiper":
+        try:
+            plan = P.plan(g, cfg)
+        except P.InfeasibleModelError as e:
+            rec.update(feasible=False, reason=f"planner: {e}")
+            return rec
+    elif strategy == "even_compute_memopt":
+        # even-compute cuts + the same per-stage memopt policy (cli.py:276-300 "compute_balanced")
+        cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)
+        try:
+            plan = P.plan_from_cuts(g, cfg, cb.positions, require_feasible=True)
+        except P.InfeasibleModelError as e:
+            rec.update(feasible=False, reason=f"planner: {e}", cuts=list(cb.positions))
+            return rec
+    elif strategy == "even_compute":
+        # even-compute cuts, no memory optimisation (PipeDream-style baseline)
+        cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)
+        ample = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=1 << 62,
+                             bandwidth=bandwidth)
+        plan = P.plan_from_cuts(g, ample, cb.positions)
+        over = [s.stage for s in plan.stages if s.sched_peak > pcap]
+        if over:
+            rec.update(feasible=False, reason=f"stages {over} exceed the capacity without memopt",
+                       cuts=list(plan.cuts.positions))
+            return rec
+    else:
+        raise ValueError(strategy)
+    rec["cuts"] = list(plan.cuts.positions)
+    rec["actions"] = [[a.kind for a in m.actions].count("swap") for m in plan.memopt]
+    rec["recomputes"] = [[a.kind for a in m.actions].count("recompute") for m in plan.memopt]
+    rec["sched_peak_gib"] = [round(s.sched_peak / GIB, 2) for s in plan.stages]
+    if not run_gpu:
+        rec["feasible"] = True
+        return rec
+    init = init_params(model, 0)
+    checks = [check_stage(model, g, plan, x, b, cap, device, init=init) for x in range(1, stages + 1)]
+    rec["stage_peak_gib"] = [round(c.peak_bytes / GIB, 2) for c in checks]
+    bad = [c for c in checks if not c.ok]
+    rec["feasible"] = not bad
+    if bad:
+        rec["reason"] = f"stage {bad[0].stage} OOM on GPU: {bad[0].error}"
+    return rec
+
+
+def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, strategy: str,
+              b_max: int = 64, device: int = 0, log=None) -> Tuple[int, List[dict]]:
+    """Largest feasible b (0 if none) by doubling then bisection."""
+    hist: List[dict] = []
+
+    def ok(b: int) -> bool:
+        r = try_batch(model, b, stages, cap, bandwidth, strategy, device)
+        hist.append(r)
+        if log:
+            log(r)
+        return bool(r.get("feasible"))
+
+    if not ok(1):
+        return 0, hist
+    lo, hi = 1, None
+    b = 2
+    while b <= b_max:
+        if ok(b):
+            lo = b
+            b *= 2
+        else:
+            hi = b
+            break
+    if hi is None:
+        return lo, hist
+    while hi - lo > 1:
+        mid = (lo + hi) // 2
+        if ok(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo, hist

@@ -239,6 +239,9 @@ class StageExecutor:
                 if len(users) == 1 and users[0].kind == "linear":
                     self.bwd_gelu_of[users[0].id] = n.id
         self._skip_bwd: Set[str] = set()
+        # profiler hook: when a list, every node forward / backward is bracketed
+        # with CUDA events on the compute stream -> (node id, "fwd"|"bwd", e0, e1)
+        self.node_timer: Optional[list] = None
 
     # ---- helpers -------------------------------------------------------------------
 
@@ -294,7 +297,14 @@ class StageExecutor:
                 for t in self._outputs(n):
                     if t in self.swap_out_done and t in self.swap_ids:
                         st.wait_event(self.swap_out_done[t])  # scratch reuse after D2H
+                if self.node_timer is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
                 self._node_fwd(n, slot, ver, "fwd", loss_out)
+                if self.node_timer is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(st)
+                    self.node_timer.append((n.id, "fwd", e0, e1))
                 if out_tid(n.id) in self.swap_ids:
                     self._swap_out(out_tid(n.id), slot)
                 if stats_tid(n.id) in self.swap_ids:
@@ -445,7 +455,14 @@ class StageExecutor:
             for tid in self.swap_ids:
                 st.wait_event(self.swap_in_done[tid])
             for n in reversed(self.nodes):
+                if self.node_timer is not None:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e0.record(st)
                 self._node_bwd(n, slot, ver)
+                if self.node_timer is not None:
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e1.record(st)
+                    self.node_timer.append((n.id, "bwd", e0, e1))
             out = {t: self.grads[t] for t in self.recv_ids if t in self.grads}
             self.bwd_done.record(st)
             self.bwd_done_recorded = True
