@@ -171,7 +171,7 @@ class Pipeline:
             tot += t.numel() * t.element_size()
         for d in s.slot_buf:
             tot += sum(t.numel() * t.element_size() for t in d.values())
-        for d in (s.fwd_scratch, s.bwd_scratch, s.work):
+        for d in (s.work,):
             tot += sum(t.numel() * t.element_size() for t in d.values())
         return tot
 

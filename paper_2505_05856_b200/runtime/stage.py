@@ -185,21 +185,27 @@ class StageExecutor:
         if unknown:
             raise ValueError(f"stage {stage}: memopt names tensors it does not hold: {sorted(unknown)}")
 
+        # Residency classes: resident saved tensors get one static buffer per
+        # in-flight slot; evicted tensors (memopt actions) are allocated only
+        # while alive -- from production until their last in-stage forward
+        # reader (and their D2H, for swaps), and from a just-in-time swap-in /
+        # recompute before their first backward reader until their last -- so
+        # they cost no device memory in between (the planner's
+        # w * (micro_peak - saved) model, memopt.py:156-158); transient
+        # un-saved tensors share one workspace buffer.
+        self.evicted = self.swap_ids | self.recompute_ids
         self.slot_buf: List[Dict[str, torch.Tensor]] = [{} for _ in range(self.w)]
-        self.fwd_scratch: Dict[str, torch.Tensor] = {}
-        self.bwd_scratch: Dict[str, torch.Tensor] = {}
         self.work: Dict[str, torch.Tensor] = {}
         self.host: Dict[str, List[torch.Tensor]] = {}
+        self.live: Dict[str, torch.Tensor] = {}
         ids_needed = {out_tid(n) for n in self._produced_or_received()}
         ids_needed |= {stats_tid(n.id) for n in self.nodes if n.kind == "ln"}
         for tid in sorted(ids_needed):
             shape, dt = self._spec(tid)
-            if tid in needed and tid not in self.swap_ids and tid not in self.recompute_ids:
+            if tid in needed and tid not in self.evicted:
                 for k in range(self.w):
                     self.slot_buf[k][tid] = torch.empty(shape, dtype=dt, device=device)
             elif tid in needed:
-                self.fwd_scratch[tid] = torch.empty(shape, dtype=dt, device=device)
-                self.bwd_scratch[tid] = torch.empty(shape, dtype=dt, device=device)
                 if tid in self.swap_ids:
                     self.host[tid] = [torch.empty(shape, dtype=dt, pin_memory=True)
                                       for _ in range(self.w)]
@@ -210,10 +216,7 @@ class StageExecutor:
         if self.is_last:
             self.labels = [torch.empty(self.M, dtype=torch.int32, device=device) for _ in range(self.w)]
             self.loss = torch.zeros(1, dtype=F32, device=device)
-        self.swap_out_done: Dict[str, torch.cuda.Event] = {}
         self.swap_in_done: Dict[str, torch.cuda.Event] = {}
-        self.bwd_done = torch.cuda.Event()
-        self.bwd_done_recorded = False
         # recompute chains (memopt.py:91-115), replayed in forward order
         self.chains: Dict[str, List[int]] = {}
         for tid in sorted(self.recompute_ids):
@@ -239,6 +242,29 @@ class StageExecutor:
                 if len(users) == 1 and users[0].kind == "linear":
                     self.bwd_gelu_of[users[0].id] = n.id
         self._skip_bwd: Set[str] = set()
+        # lifetimes of evicted tensors (positions within this stage's node list)
+        pos = {n.id: i for i, n in enumerate(self.nodes)}
+        self.fwd_last: Dict[str, float] = {}
+        for tid in self.evicted:
+            src, kind = tid.rsplit(".", 1)
+            users = [src] if kind == "stats" else [n.id for n in self.nodes if src in n.inputs]
+            last = max((pos[u] for u in users), default=-1)
+            self.fwd_last[tid] = math.inf if tid in self.send_ids else last
+        self.bwd_reads: Dict[str, List[str]] = {}
+        for n in self.nodes:
+            reads = [out_tid(src) for src, rd in self.readers.items() if n.id in rd]
+            if n.kind == "ln":
+                reads.append(stats_tid(n.id))
+            if n.id in self.bwd_gelu_of:  # fused GELU backward reads the pre-activation
+                reads.append(out_tid(self.node_by_id[self.bwd_gelu_of[n.id]].inputs[0]))
+            self.bwd_reads[n.id] = [t for t in reads if t in self.evicted]
+        self.bwd_last: Dict[str, int] = {}
+        self.bwd_first: Dict[str, int] = {}
+        for n in self.nodes:
+            for t in self.bwd_reads[n.id]:
+                self.bwd_last[t] = min(self.bwd_last.get(t, pos[n.id]), pos[n.id])
+                self.bwd_first[t] = max(self.bwd_first.get(t, pos[n.id]), pos[n.id])
+        self.swap_lookahead = 2
         # profiler hook: when a list, every node forward / backward is bracketed
         # with CUDA events on the compute stream -> (node id, "fwd"|"bwd", e0, e1)
         self.node_timer: Optional[list] = None
@@ -265,11 +291,25 @@ class StageExecutor:
     def buf(self, tid: str, slot: int, phase: str) -> torch.Tensor:
         if tid in self.slot_buf[slot]:
             return self.slot_buf[slot][tid]
-        if tid in self.fwd_scratch:
-            return self.fwd_scratch[tid] if phase == "fwd" else self.bwd_scratch[tid]
+        if tid in self.evicted:
+            if tid not in self.live:
+                raise KeyError(f"stage {self.stage}: evicted tensor {tid} is not materialised")
+            return self.live[tid]
         if tid in self.work:
             return self.work[tid]
         raise KeyError(f"stage {self.stage}: no buffer for {tid}")
+
+    def _alloc_live(self, tid: str) -> torch.Tensor:
+        shape, dt = self._spec(tid)
+        with torch.cuda.stream(self.stream):
+            t = torch.empty(shape, dtype=dt, device=self.device)
+        self.live[tid] = t
+        return t
+
+    def _drop_leftovers(self) -> None:
+        """Release evicted tensors a previous forward kept only for its sends."""
+        for t in [t for t in self.live if self.fwd_last.get(t) == math.inf]:
+            del self.live[t]
 
     def slot_of(self, mb: int) -> int:
         return (mb - 1) % self.w
@@ -293,10 +333,14 @@ class StageExecutor:
             for tid in self.recv_ids:
                 if tid in self.swap_ids:
                     self._swap_out(tid, slot)
-            for n in self.nodes:
-                for t in self._outputs(n):
-                    if t in self.swap_out_done and t in self.swap_ids:
-                        st.wait_event(self.swap_out_done[t])  # scratch reuse after D2H
+                if tid in self.evicted and self.fwd_last[tid] < 0:
+                    del self.live[tid]
+            fused_gelus = set(self.fwd_gelu_of.values())
+            for i, n in enumerate(self.nodes):
+                produced = [] if n.id in fused_gelus else self._outputs(n)  # fused: fc1 made it
+                for t in produced:
+                    if t in self.evicted:
+                        self._alloc_live(t)
                 if self.node_timer is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(st)
@@ -305,12 +349,16 @@ class StageExecutor:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(st)
                     self.node_timer.append((n.id, "fwd", e0, e1))
-                if out_tid(n.id) in self.swap_ids:
-                    self._swap_out(out_tid(n.id), slot)
-                if stats_tid(n.id) in self.swap_ids:
-                    self._swap_out(stats_tid(n.id), slot)
+                for t in produced:
+                    if t in self.swap_ids:
+                        self._swap_out(t, slot)
+                for t in [t for t in self.live if self.fwd_last.get(t, math.inf) <= i]:
+                    del self.live[t]  # last in-stage forward reader done (swaps: D2H ordered)
 
     def recv_buffer(self, tid: str, mb: int) -> torch.Tensor:
+        if tid in self.evicted:
+            self._drop_leftovers()
+            return self._alloc_live(tid)
         return self.buf(tid, self.slot_of(mb), "fwd")
 
     def send_buffer(self, tid: str, mb: int) -> torch.Tensor:
@@ -323,15 +371,28 @@ class StageExecutor:
         return outs
 
     def _swap_out(self, tid: str, slot: int) -> None:
+        """D2H of an evicted tensor on the copy stream (swap engine, memopt swap)."""
         ev = torch.cuda.Event()
         ev.record(self.stream)
         cs = self.copy_stream
         cs.wait_event(ev)
+        src = self.live[tid]
         with torch.cuda.stream(cs):
-            self.host[tid][slot].copy_(self.fwd_scratch[tid], non_blocking=True)
+            self.host[tid][slot].copy_(src, non_blocking=True)
+        src.record_stream(cs)  # memory is recycled only after the D2H completes
+
+    def _swap_in(self, tid: str, slot: int) -> None:
+        """H2D prefetch of a swapped tensor into a fresh device buffer."""
+        dst = self._alloc_live(tid)
+        ev = torch.cuda.Event()
+        ev.record(self.stream)  # the buffer's memory is free in compute-stream order
+        cs = self.copy_stream
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            dst.copy_(self.host[tid][slot], non_blocking=True)
         done = torch.cuda.Event()
         done.record(cs)
-        self.swap_out_done[tid] = done
+        self.swap_in_done[tid] = done
 
     def _node_fwd(self, n: NodeDef, slot: int, ver: int, phase: str,
                   loss_out: Optional[torch.Tensor] = None) -> None:
@@ -431,30 +492,40 @@ class StageExecutor:
         assert self.slot_mb[slot] == mb, "slot reused before its backward"
         ver = self.params.pinned(mb)
         with torch.cuda.stream(st):
+            self._drop_leftovers()
             self.params.zero_accum_grads(stream=st)
-            # swapped tensors: H2D into the backward scratch
-            if self.swap_ids:
-                cs = self.copy_stream
-                if self.bwd_done_recorded:
-                    cs.wait_event(self.bwd_done)  # previous backward is done with the scratch
-                for tid in sorted(self.swap_ids):
-                    with torch.cuda.stream(cs):
-                        self.bwd_scratch[tid].copy_(self.host[tid][slot], non_blocking=True)
-                    ev = torch.cuda.Event()
-                    ev.record(cs)
-                    self.swap_in_done[tid] = ev
-            # recomputed tensors: replay their producer chains (forward order)
-            if self.recompute_ids:
-                replayed: Set[int] = set()
-                for tid in sorted(self.recompute_ids, key=lambda t: self.index[t.rsplit(".", 1)[0]]):
-                    for i in self.chains[tid]:
-                        if i in replayed:
-                            continue
-                        replayed.add(i)
-                        self._node_fwd_replay(self.all_nodes[i], slot, ver)
-            for tid in self.swap_ids:
-                st.wait_event(self.swap_in_done[tid])
+            # swap-ins in first-use order (backward runs right to left), kept
+            # `swap_lookahead` tensors ahead of the node that needs them
+            queue = sorted(self.swap_ids, key=lambda t: (-self.bwd_first.get(t, -1), t))
+            issued: Set[str] = set()
+
+            def issue_next() -> None:
+                t = queue.pop(0)
+                if t not in self.live:
+                    self._swap_in(t, slot)
+                issued.add(t)
+
+            def prefetch(upto: int) -> None:
+                while queue and sum(1 for t in issued if t in self.live) < upto:
+                    issue_next()
+
+            prefetch(self.swap_lookahead)
+            pos = {n.id: i for i, n in enumerate(self.nodes)}
             for n in reversed(self.nodes):
+                for t in self.bwd_reads[n.id]:
+                    if t in self.live and t not in self.swap_in_done:
+                        continue
+                    if t in self.swap_ids:
+                        while t not in issued:
+                            if not queue:
+                                raise RuntimeError(f"stage {self.stage}: swap-in of {t} never issued")
+                            issue_next()
+                        if t in self.swap_in_done:
+                            st.wait_event(self.swap_in_done.pop(t))
+                    elif t not in self.live:  # recompute: replay its producer chain now
+                        self._alloc_live(t)
+                        for i in self.chains[t]:
+                            self._node_fwd_replay(self.all_nodes[i], slot, ver)
                 if self.node_timer is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(st)
@@ -463,9 +534,11 @@ class StageExecutor:
                     e1 = torch.cuda.Event(enable_timing=True)
                     e1.record(st)
                     self.node_timer.append((n.id, "bwd", e0, e1))
+                for t in self.bwd_reads[n.id]:
+                    if self.bwd_last.get(t) == pos[n.id] and t in self.live:
+                        del self.live[t]
+                prefetch(self.swap_lookahead)
             out = {t: self.grads[t] for t in self.recv_ids if t in self.grads}
-            self.bwd_done.record(st)
-            self.bwd_done_recorded = True
         return out
 
     def finish_backward(self, mb: int) -> None:
@@ -479,8 +552,11 @@ class StageExecutor:
         self._skip_bwd = set()
 
     def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
-        # outputs of a replayed node land in the backward scratch if evicted,
-        # else in its normal home (slot buffer or workspace)
+        # outputs of a replayed node land in a live buffer if evicted, else in
+        # their normal home (slot buffer or workspace)
+        for t in [out_tid(n.id)] + ([stats_tid(n.id)] if n.kind == "ln" else []):
+            if t in self.evicted and t not in self.live:
+                self._alloc_live(t)
         self._node_fwd(n, slot, ver, "bwd")
 
     def _node_bwd(self, n: NodeDef, slot: int, ver: int) -> None:
