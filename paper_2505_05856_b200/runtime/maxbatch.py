@@ -48,13 +48,25 @@ class StageCheck:
     error: str = ""
 
 
-def optimizer_reserve(model: TransformerConfig, g, stages: int, workspace: int = 3 * GIB) -> int:
-    """Bytes per GPU the planner's memory model leaves out: 16 B/param of fp32
-    state for the largest stage of the compute-balanced split, plus workspace."""
-    cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)
-    bounds = P.stage_bounds(cb, len(g))
-    max_params = max(g.segment_params(lo, hi) for lo, hi in bounds) // 2  # m_p = 2 B/param
-    return 16 * max_params + workspace
+def stage_overhead(model: TransformerConfig, g, lo: int, hi: int, b: int) -> int:
+    """Device bytes of a stage the planner's model (w x (micro_peak - saved),
+    memopt.py:156-158) does not see: fp32 master / Adam m / Adam v / grad
+    (16 B per parameter; the bf16 versions are the model's m_p), backward
+    gradient buffers (~2 of the stage's largest activation), the D2H
+    back-pressure window and workspace / allocator slack.  Calibrated against
+    measured per-stage peaks (tools/max_batch.py, profiles/r01_maxbatch_*)."""
+    params = g.segment_params(lo, hi) // 2  # m_p = 2 B / param (one bf16 version)
+    largest = max(g.nodes[k].m_a for k in range(lo, hi + 1))
+    return 16 * params + 2 * largest + 3 * GIB // 2
+
+
+def optimizer_reserve(model: TransformerConfig, g, stages: int, cuts=None) -> int:
+    """Max stage_overhead over the stages of `cuts` (default: compute-balanced)."""
+    if cuts is None:
+        cuts = P.compute_balanced(g, 0, len(g) - 1, [1] * stages).positions
+    bounds = P.stage_bounds(P.Cut(tuple(cuts)), len(g))
+    b = max(1, g.nodes[0].m_a // (2 * model.seq * model.hidden))
+    return max(stage_overhead(model, g, lo, hi, b) for lo, hi in bounds)
 
 
 def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, device: int = 0,
@@ -110,8 +122,16 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
         torch.cuda.set_per_process_memory_fraction(1.0, device)
 
 
+def host_bytes(plan, stages: int) -> List[int]:
+    """Pinned host bytes per stage: w = l-x+1 slots of every swapped tensor."""
+    return [(stages - x) * sum(a.size for a in m.actions if a.kind == "swap")
+            + sum(a.size for a in m.actions if a.kind == "swap")
+            for x, m in enumerate(plan.memopt)]
+
+
 def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth: int,
-              strategy: str, device: int = 0, times=None, run_gpu: bool = True) -> dict:
+              strategy: str, device: int = 0, times=None, run_gpu: bool = True,
+              host_cap: int = 96 * GIB) -> dict:
     g = profile_graph(model, b, times=times)
     reserve = optimizer_reserve(model, g, stages)
     pcap = cap - reserve
@@ -122,11 +142,24 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
         rec.update(feasible=False, reason="optimizer state alone exceeds the cap")
         return rec
     if strategy == "dawnpiper":
-        try:
-            plan = P.plan(g, cfg)
-        except P.InfeasibleModelError as e:
-            rec.update(feasible=False, reason=f"planner: {e}")
-            return rec
+        # plan, then re-plan with the reserve of the plan's own stages until the
+        # capacity handed to the planner covers every stage's overhead
+        for _ in range(4):
+            try:
+                plan = P.plan(g, cfg)
+            except P.InfeasibleModelError as e:
+                rec.update(feasible=False, reason=f"planner: {e}")
+                return rec
+            need = optimizer_reserve(model, g, stages, plan.cuts.positions)
+            if cap - need >= cfg.capacity:
+                break
+            pcap = cap - need
+            if pcap <= 0:
+                rec.update(feasible=False, reason="stage overhead alone exceeds the cap")
+                return rec
+            cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=pcap,
+                               bandwidth=bandwidth)
+            rec["planner_capacity"] = pcap
     elif strategy == "even_compute_memopt":
         # even-compute cuts + the same per-stage memopt policy (cli.py:276-300 "compute_balanced")
         cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)
@@ -152,6 +185,12 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
     rec["actions"] = [[a.kind for a in m.actions].count("swap") for m in plan.memopt]
     rec["recomputes"] = [[a.kind for a in m.actions].count("recompute") for m in plan.memopt]
     rec["sched_peak_gib"] = [round(s.sched_peak / GIB, 2) for s in plan.stages]
+    hb = host_bytes(plan, stages)
+    rec["host_pinned_gib"] = [round(h / GIB, 1) for h in hb]
+    if max(hb) > host_cap:
+        # swap slots live in pinned host memory, which the planner does not model
+        rec.update(feasible=False, reason=f"pinned host memory {max(hb) / GIB:.1f} GiB > {host_cap / GIB:.0f} GiB per GPU")
+        return rec
     if not run_gpu:
         rec["feasible"] = True
         return rec
@@ -166,12 +205,14 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
 
 
 def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, strategy: str,
-              b_max: int = 64, device: int = 0, log=None) -> Tuple[int, List[dict]]:
+              b_max: int = 64, device: int = 0, log=None, host_cap: int = 96 * GIB,
+              run_gpu: bool = True) -> Tuple[int, List[dict]]:
     """Largest feasible b (0 if none) by doubling then bisection."""
     hist: List[dict] = []
 
     def ok(b: int) -> bool:
-        r = try_batch(model, b, stages, cap, bandwidth, strategy, device)
+        r = try_batch(model, b, stages, cap, bandwidth, strategy, device, host_cap=host_cap,
+                      run_gpu=run_gpu)
         hist.append(r)
         if log:
             log(r)

@@ -217,6 +217,11 @@ class StageExecutor:
             self.labels = [torch.empty(self.M, dtype=torch.int32, device=device) for _ in range(self.w)]
             self.loss = torch.zeros(1, dtype=F32, device=device)
         self.swap_in_done: Dict[str, torch.cuda.Event] = {}
+        # D2H back-pressure: memory of a swapped tensor is recycled only once its
+        # D2H completes; if the host link falls behind compute, the forward
+        # waits for the oldest transfer instead of piling up device memory
+        self.d2h_pending: List[Tuple[torch.cuda.Event, int]] = []
+        self.d2h_budget = 1 << 30
         # recompute chains (memopt.py:91-115), replayed in forward order
         self.chains: Dict[str, List[int]] = {}
         for tid in sorted(self.recompute_ids):
@@ -338,6 +343,8 @@ class StageExecutor:
             fused_gelus = set(self.fwd_gelu_of.values())
             for i, n in enumerate(self.nodes):
                 produced = [] if n.id in fused_gelus else self._outputs(n)  # fused: fc1 made it
+                if any(t in self.swap_ids for t in produced):
+                    self._d2h_backpressure()
                 for t in produced:
                     if t in self.evicted:
                         self._alloc_live(t)
@@ -380,6 +387,14 @@ class StageExecutor:
         with torch.cuda.stream(cs):
             self.host[tid][slot].copy_(src, non_blocking=True)
         src.record_stream(cs)  # memory is recycled only after the D2H completes
+        done = torch.cuda.Event()
+        done.record(cs)
+        self.d2h_pending.append((done, src.numel() * src.element_size()))
+
+    def _d2h_backpressure(self) -> None:
+        while self.d2h_pending and sum(b for _, b in self.d2h_pending) > self.d2h_budget:
+            ev, _ = self.d2h_pending.pop(0)
+            self.stream.wait_event(ev)
 
     def _swap_in(self, tid: str, slot: int) -> None:
         """H2D prefetch of a swapped tensor into a fresh device buffer."""
@@ -537,6 +552,9 @@ class StageExecutor:
                 for t in self.bwd_reads[n.id]:
                     if self.bwd_last.get(t) == pos[n.id] and t in self.live:
                         del self.live[t]
+                # n's output gradient is consumed: drop it (memory is recycled once
+                # every alias is gone, in compute-stream order)
+                self.grads.pop(out_tid(n.id), None)
                 prefetch(self.swap_lookahead)
             out = {t: self.grads[t] for t in self.recv_ids if t in self.grads}
         return out

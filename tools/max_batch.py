@@ -14,14 +14,17 @@ ap.add_argument("--cap-gib", type=float, default=40.0)
 ap.add_argument("--bandwidth-gbs", type=float, default=48.0, help="host link for swaps (GB/s)")
 ap.add_argument("--b-max", type=int, default=64)
 ap.add_argument("--out", default=None)
+ap.add_argument("--host-cap-gib", type=float, default=96.0)
+ap.add_argument("--no-gpu", action="store_true")
 args = ap.parse_args()
 cfg = PRESETS[args.model]
 cap = int(args.cap_gib * (1 << 30))
-res = {"model": args.model, "stages": args.stages, "cap_bytes": cap, "swap_bandwidth_Bps": int(args.bandwidth_gbs * 1e9)}
+res = {"host_cap_bytes": int(args.host_cap_gib * (1 << 30)), "model": args.model, "stages": args.stages, "cap_bytes": cap, "swap_bandwidth_Bps": int(args.bandwidth_gbs * 1e9)}
 for strat in ("even_compute", "even_compute_memopt", "dawnpiper"):
     t0 = time.time()
     best, hist = max_batch(cfg, args.stages, cap, int(args.bandwidth_gbs * 1e9), strat, b_max=args.b_max,
-                           log=lambda r: print(json.dumps(r), flush=True))
+                           log=lambda r: print(json.dumps(r), flush=True),
+                           host_cap=int(args.host_cap_gib * (1 << 30)), run_gpu=not args.no_gpu)
     res[strat] = {"max_micro_batch": best, "search_s": round(time.time() - t0, 1), "trials": hist}
 res["ratio"] = (res["dawnpiper"]["max_micro_batch"] / res["even_compute"]["max_micro_batch"]
                 if res["even_compute"]["max_micro_batch"] else None)
