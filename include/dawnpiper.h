@@ -77,6 +77,18 @@ typedef struct {
 } dpn_gemm_args;
 int dpn_gemm(const dpn_gemm_args* args, void* stream);
 
+/* ---- fused attention (tcgen05 flash-style; head_dim 64) ------------------
+ * qkv: [batch*seq, 3*heads*64] bf16 (Q | K | V column blocks, head-major within
+ * each), out: [batch*seq, heads*64] bf16, lse: [batch, heads, seq] f32 (natural
+ * log-sum-exp of scale * QK^T per query, saved for the backward).  seq % 64 == 0. */
+int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batch, int64_t seq, int64_t heads,
+                 int64_t head_dim, float scale, int causal, void* stream);
+/* Backward: writes all of dqkv (dQ | dK | dV) from qkv, out, dout (= dL/dout) and
+ * the forward's lse.  workspace: >= batch*seq*heads*64 + batch*heads*seq floats. */
+int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
+                 float* workspace, int64_t workspace_floats, int64_t batch, int64_t seq,
+                 int64_t heads, int64_t head_dim, float scale, int causal, void* stream);
+
 /* ---- node kernels (bf16 storage, fp32 math) ------------------------------ */
 /* ln1 / ln2 / lnf: y = (x - mean) * rstd * gamma + beta; mean/rstd saved (f32 [rows]). */
 int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,

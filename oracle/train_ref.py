@@ -47,15 +47,17 @@ def one_f_one_b(stages: int, m: int, x: int) -> List[Tuple[str, int]]:
     return ops
 
 
-def node_ids(layers: int) -> List[str]:
+def node_ids(layers: int, fused: bool = True) -> List[str]:
+    """Node ids; with fused attention `attn` reads qkv directly (no `score`)."""
     ids = ["embed"]
+    block = ("ln1", "qkv", "attn", "proj", "ln2", "fc1", "gelu", "fc2", "add") if fused else \
+        ("ln1", "qkv", "score", "attn", "proj", "ln2", "fc1", "gelu", "fc2", "add")
     for b in range(layers):
-        ids += [f"b{b}.{k}" for k in ("ln1", "qkv", "score", "attn", "proj", "ln2", "fc1",
-                                      "gelu", "fc2", "add")]
+        ids += [f"b{b}.{k}" for k in block]
     return ids + ["lnf", "head"]
 
 
-def _inputs(nid: str, layers: int) -> Tuple[str, ...]:
+def _inputs(nid: str, layers: int, fused: bool = True) -> Tuple[str, ...]:
     if nid == "embed":
         return ()
     if nid == "lnf":
@@ -67,7 +69,8 @@ def _inputs(nid: str, layers: int) -> Tuple[str, ...]:
     x = "embed" if blk == 0 else f"b{blk - 1}.add"
     p = f"b{blk}."
     return {
-        "ln1": (x,), "qkv": (p + "ln1",), "score": (p + "qkv",), "attn": (p + "score", p + "qkv"),
+        "ln1": (x,), "qkv": (p + "ln1",), "score": (p + "qkv",),
+        "attn": (p + "qkv",) if fused else (p + "score", p + "qkv"),
         "proj": (p + "attn", x), "ln2": (p + "proj",), "fc1": (p + "ln2",), "gelu": (p + "fc1",),
         "fc2": (p + "gelu",), "add": (p + "fc2", p + "proj"),
     }[k]
@@ -91,7 +94,8 @@ class RefStage:
         H, A, s = d["hidden"], d["heads"], d["seq"]
         hd = H // A
         kind = nid.split(".")[-1] if nid not in ("embed", "lnf", "head") else nid
-        ins = [env[u] for u in _inputs(nid, d["layers"])]
+        fused = d.get("fused_attention", True)
+        ins = [env[u] for u in _inputs(nid, d["layers"], fused)]
         w = lambda pn: W[f"{nid}.{pn}"]
         if kind == "embed":
             M = ids.numel()
@@ -115,6 +119,16 @@ class RefStage:
             if d["causal"]:
                 sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), float("-inf"))
             return torch.softmax(sc, -1)
+        if kind == "attn" and fused:
+            qkv = ins[0]
+            b = qkv.shape[0] // s
+            q = qkv[:, :H].reshape(b, s, A, hd).transpose(1, 2)
+            k = qkv[:, H:2 * H].reshape(b, s, A, hd).transpose(1, 2)
+            v = qkv[:, 2 * H:].reshape(b, s, A, hd).transpose(1, 2)
+            sc = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
+            if d["causal"]:
+                sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), float("-inf"))
+            return (torch.softmax(sc, -1) @ v).transpose(1, 2).reshape(b * s, H)
         if kind == "attn":
             P, qkv = ins
             b = qkv.shape[0] // s
@@ -162,11 +176,11 @@ class RefStage:
             p.addcdiv_(self.exp_avg[k] / bc1, denom, value=-o["lr"])
 
 
-def boundary(stage_nodes: List[List[str]], x: int, layers: int) -> List[str]:
+def boundary(stage_nodes: List[List[str]], x: int, layers: int, fused: bool = True) -> List[str]:
     """Outputs produced at or before stage x that a later stage reads."""
     before = [n for st in stage_nodes[:x + 1] for n in st]
     after = {n for st in stage_nodes[x + 1:] for n in st}
-    return [u for u in before if any(u in _inputs(v, layers) for v in after)]
+    return [u for u in before if any(u in _inputs(v, layers, fused) for v in after)]
 
 
 def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor,
@@ -176,7 +190,8 @@ def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor
     Returns (losses [steps][m], final fp32 parameters)."""
     l, m = len(stage_nodes), ids.shape[0]
     stages = [RefStage(dims, init, nodes, opt) for nodes in stage_nodes]
-    sends = [boundary(stage_nodes, x, dims["layers"]) for x in range(l)]
+    sends = [boundary(stage_nodes, x, dims["layers"], dims.get("fused_attention", True))
+             for x in range(l)]
     all_losses = []
     for _ in range(steps):
         losses = [0.0] * m

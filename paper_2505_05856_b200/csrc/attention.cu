@@ -1,0 +1,709 @@
+// Fused attention (flash-style) for sm_100a: tcgen05 MMAs with S / O tiles in
+// TMEM, online softmax in registers, P staged in shared memory (128-byte
+// swizzled, the layout the next MMA reads), Q/K/V tiles fetched by TMA straight
+// out of the fused [b*s, 3H] QKV buffer.  The s x s probability matrix never
+// touches HBM (the unfused `score` node writes b*heads*s^2 bf16 and reads it
+// back three times).
+//
+// Forward, one CTA per (batch, head, 128-query tile), 256 threads:
+//   warp 0   TMA: Q once, then K_j / V_j tiles into a 3-deep ring
+//   warp 1   MMA issuer: S_j = Q K_j^T (M=128,N=128,K=64) into TMEM S[j%2];
+//            O_j = P_j V_j (M=128,N=64,K=128) into TMEM O[j%2]
+//   warp 2   TMEM allocator
+//   warps 4-7 softmax: thread t owns query row t; reads S_j (tcgen05.ld),
+//            masks (causal, key < seq), updates running max / sum, writes
+//            P_j = exp(S_j - m) as bf16 into smem, accumulates
+//            O = O * exp(m_old - m_new) + O_j in registers; finally writes
+//            O / l (bf16) and the log-sum-exp (fp32, for the backward).
+// head_dim is 64 (one 128-byte swizzle row).
+#include "common.cuh"
+#include "../../include/dawnpiper.h"
+
+#include <mutex>
+
+namespace dpn {
+namespace {
+
+constexpr int kTile = 128;  // queries per CTA and keys per KV tile
+constexpr int kD = 64;
+constexpr int kKVStages = 3;
+constexpr int kTileBytes = kTile * kD * 2;  // 16 KB (128 rows x 128 B)
+constexpr int kPBytes = kTile * kTile * 2;  // 32 KB (two 64-key swizzle atoms)
+constexpr int kFwdThreads = 256;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct AttnParams {
+  int batch, seq, heads, H;  // H = heads * 64
+  float scale_log2;          // softmax scale * log2(e)
+  float scale;
+  int causal;
+  __nv_bfloat16* out;  // [b*s, H]
+  float* lse;          // [b, heads, s] natural-log LSE of scale * S
+};
+
+// byte offset of (row, 16-byte chunk) inside a 128-row x 128-byte SW128 atom
+__device__ __forceinline__ uint32_t sw128(int row, int chunk) {
+  return (uint32_t)(row * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTileBytes;                  // [stage] 16 KB
+  uint8_t* sV = sK + kKVStages * kTileBytes;      // [stage] 16 KB
+  uint8_t* sP = sV + kKVStages * kTileBytes;      // [2] 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + kKVStages;
+  uint64_t* s_full = kv_empty + kKVStages;  // [2]
+  uint64_t* s_empty = s_full + 2;           // [2]
+  uint64_t* p_full = s_empty + 2;           // [2]
+  uint64_t* p_empty = p_full + 2;           // [2]
+  uint64_t* o_full = p_empty + 2;           // [2]
+  uint64_t* o_empty = o_full + 2;           // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int qt = blockIdx.x, h = blockIdx.y, bb = blockIdx.z;
+  const int q0 = qt * kTile;
+  const int n_kv_all = (p.seq + kTile - 1) / kTile;
+  const int n_kv = p.causal ? min(n_kv_all, qt + 1) : n_kv_all;
+  const int row0 = bb * p.seq;  // first token row of this sequence in [b*s, 3H]
+
+  if (warp == 0 && lane == 0) prefetch_tmap(&tm_qkv);
+  if (warp == 1 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int s = 0; s < kKVStages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);  // one arrival per softmax warp
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S[0] 0..127, S[1] 128..255, O[0] 256..319, O[1] 320..383
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(q_full, kTileBytes);
+      tma_load_2d(sQ, &tm_qkv, q_full, h * kD, row0 + q0);
+      for (int j = 0; j < n_kv; ++j) {
+        const int st = j % kKVStages;
+        mbar_wait(&kv_empty[st], ((j / kKVStages) & 1) ^ 1);
+        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+        tma_load_2d(sK + st * kTileBytes, &tm_qkv, &kv_full[st], p.H + h * kD, row0 + j * kTile);
+        tma_load_2d(sV + st * kTileBytes, &tm_qkv, &kv_full[st], 2 * p.H + h * kD, row0 + j * kTile);
+      }
+    }
+  } else if (warp == 1) {
+    // S = Q K^T: A = Q (K-major, K = d), B = K_j (K-major over d)
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+    // O = P V: A = P (K-major over keys: two 64-key atoms), B = V_j (MN-major: d contiguous)
+    constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);
+    auto issue_o = [&](int j) {
+      const int i = j & 1;
+      mbar_wait(&p_full[i], (j >> 1) & 1);
+      mbar_wait(&o_empty[i], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const int st = j % kKVStages;
+        const uint32_t pa = smem_u32(sP + i * kPBytes), vb = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k) {
+          const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(vb + k * 2048, kD * 128, 1024);
+          umma_bf16(tmem + 256 + i * 64, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&o_full[i]);
+        umma_commit(&p_empty[i]);
+        umma_commit(&kv_empty[st]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(q_full, 0);
+    for (int j = 0; j < n_kv; ++j) {
+      const int st = j % kKVStages, i = j & 1;
+      mbar_wait(&kv_full[st], (j / kKVStages) & 1);
+      mbar_wait(&s_empty[i], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(kb + k * 32, 16, 1024);
+          umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[i]);
+      }
+      __syncwarp();
+      if (j >= 1) issue_o(j - 1);
+    }
+    issue_o(n_kv - 1);
+  } else if (warp >= 4) {
+    // ---------------- softmax / correction ----------------
+    const int r = (warp - 4) * 32 + lane;  // query row within the tile (== TMEM lane)
+    const int q = q0 + r;
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    float o[kD];
+#pragma unroll
+    for (int c = 0; c < kD; ++c) o[c] = 0.f;
+    float alpha_prev = 0.f;
+    for (int j = 0; j <= n_kv; ++j) {
+      if (j < n_kv) {
+        const int i = j & 1;
+        mbar_wait(&s_full[i], (j >> 1) & 1);
+        tc_fence_after();
+        float s[kTile];
+#pragma unroll
+        for (int c = 0; c < kTile / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(tmem + i * 128 + c * 32 + lane_off, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(u[e]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[i]);
+        const int k0 = j * kTile;
+        float mx = m;
+#pragma unroll
+        for (int c = 0; c < kTile; ++c) {
+          const int key = k0 + c;
+          const bool ok = key < p.seq && (!p.causal || key <= q);
+          s[c] = ok ? s[c] * p.scale_log2 : -INFINITY;
+          mx = fmaxf(mx, s[c]);
+        }
+        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mx);
+        const float base = (mx == -INFINITY) ? 0.f : mx;
+        float sum = 0.f;
+        // P_j into shared memory: 128-byte swizzled, two 64-key atoms
+        mbar_wait(&p_empty[i], ((j >> 1) & 1) ^ 1);
+        uint8_t* pt = sP + i * kPBytes;
+#pragma unroll
+        for (int c = 0; c < kTile / 8; ++c) {
+          float e8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            e8[e] = exp2f(s[c * 8 + e] - base);
+            sum += e8[e];
+          }
+          uint4 w;
+          w.x = pack_bf16(e8[0], e8[1]);
+          w.y = pack_bf16(e8[2], e8[3]);
+          w.z = pack_bf16(e8[4], e8[5]);
+          w.w = pack_bf16(e8[6], e8[7]);
+          *reinterpret_cast<uint4*>(pt + (c >> 3) * (kPBytes / 2) + sw128(r, c & 7)) = w;
+        }
+        l = l * alpha + sum;
+        m = mx;
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
+        // accumulate the previous O tile with its own correction factor
+        if (j >= 1) {
+          const int pi = (j - 1) & 1;
+          mbar_wait(&o_full[pi], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < kD / 32; ++c) {
+            uint32_t u[32];
+            tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + c * 32 + lane_off, u);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha_prev + __uint_as_float(u[e]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_empty[pi]);
+        }
+        alpha_prev = alpha;
+      } else {
+        const int pi = (j - 1) & 1;
+        mbar_wait(&o_full[pi], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < kD / 32; ++c) {
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + c * 32 + lane_off, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha_prev + __uint_as_float(u[e]);
+        }
+        tc_fence_before();
+      }
+    }
+    if (q < p.seq) {
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD;
+#pragma unroll
+      for (int c = 0; c < kD / 8; ++c) {
+        uint4 w;
+        w.x = pack_bf16(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
+        w.y = pack_bf16(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
+        w.z = pack_bf16(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
+        w.w = pack_bf16(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
+        reinterpret_cast<uint4*>(op)[c] = w;
+      }
+      // natural-log LSE of scale * S:  (m + log2 l) / log2(e)
+      p.lse[((long long)bb * p.heads + h) * p.seq + q] = (m + log2f(l)) / kLog2e;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode2() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult r;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &q, cudaEnableDefault, &r) == cudaSuccess &&
+        r == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(q);
+  });
+  return fn;
+}
+
+// 2-D map over a bf16 [rows, cols] buffer, box 64 columns x 128 rows, SW128.
+int map_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols) {
+  EncodeFn enc = encode2();
+  DPN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  DPN_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && cols % 8 == 0, "16-byte alignment");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 2)};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DPN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed");
+  return 0;
+}
+
+constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256;
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Backward, one CTA per (batch, head, 128-key tile) -- K_j, V_j stay in smem
+// while the CTA walks the query tiles i (causal: i >= j):
+//   S = Q_i K_j^T, dP = dO_i V_j^T                  (TMEM, M = queries)
+//   P = exp(scale*S - lse), dS = scale * P * (dP - D_i)   (softmax warps ->
+//       bf16 in 128-byte swizzled smem, one thread per query row)
+//   dV += P^T dO_i, dK += dS^T Q_i                   (TMEM accumulators, M = keys;
+//       P^T / dS^T are the same smem tiles read MN-major)
+//   dQ_i = dS K_j                                    (TMEM -> red.global.add.v4.f32)
+// D_i = rowsum(dO_i * O_i) comes from attn_bwd_prep.
+namespace {
+
+constexpr int kBwdThreads = 256;
+
+struct AttnBwdParams {
+  int seq, heads, H;
+  float scale, scale_log2;
+  int causal;
+  const float* lse;  // [b, heads, s]
+  const float* D;    // [b, heads, s]
+  float* dq;         // [b*s, H] f32 accumulator (zeroed)
+  __nv_bfloat16* dqkv;  // [b*s, 3H]
+};
+
+__device__ __forceinline__ void red_add_v4f(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+               "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                    const __grid_constant__ CUtensorMap tm_do, const AttnBwdParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + kTileBytes;
+  uint8_t* sQ = sV + kTileBytes;          // [2]
+  uint8_t* sdO = sQ + 2 * kTileBytes;     // [2]
+  uint8_t* sP = sdO + 2 * kTileBytes;     // 32 KB
+  uint8_t* sdS = sP + kPBytes;            // 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + kPBytes);
+  uint64_t* kv_full = bars;
+  uint64_t* q_full = bars + 1;    // [2]
+  uint64_t* q_empty = q_full + 2; // [2]
+  uint64_t* sp_full = q_empty + 2;
+  uint64_t* sp_empty = sp_full + 1;
+  uint64_t* ds_full = sp_empty + 1;
+  uint64_t* ds_empty = ds_full + 1;
+  uint64_t* dq_full = ds_empty + 1;
+  uint64_t* dq_empty = dq_full + 1;
+  uint64_t* dkv_full = dq_empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kt = blockIdx.x, h = blockIdx.y, bb = blockIdx.z;
+  const int k0 = kt * kTile;
+  const int n_q = (p.seq + kTile - 1) / kTile;
+  const int i0 = p.causal ? kt : 0;
+  const int row0 = bb * p.seq;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_qkv);
+    prefetch_tmap(&tm_do);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+    }
+    mbar_init(sp_full, 1);
+    mbar_init(sp_empty, 4);
+    mbar_init(ds_full, 4);
+    mbar_init(ds_empty, 1);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 4);
+    mbar_init(dkv_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S 0..127, dP 128..255, dV 256..319, dK 320..383, dQ 384..447
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_expect_tx(kv_full, 2 * kTileBytes);
+      tma_load_2d(sK, &tm_qkv, kv_full, p.H + h * kD, row0 + k0);
+      tma_load_2d(sV, &tm_qkv, kv_full, 2 * p.H + h * kD, row0 + k0);
+      for (int i = i0, it = 0; i < n_q; ++i, ++it) {
+        const int st = it & 1;
+        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[st], 2 * kTileBytes);
+        tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], h * kD, row0 + i * kTile);
+        tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], h * kD, row0 + i * kTile);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // S, dP
+    constexpr uint32_t id_kv = idesc_bf16(128, 64, 1, 1);   // dV, dK: A^T and B MN-major
+    constexpr uint32_t id_q = idesc_bf16(128, 64, 0, 1);    // dQ: dS K-major, K_j MN-major
+    mbar_wait(kv_full, 0);
+    for (int i = i0, it = 0; i < n_q; ++i, ++it) {
+      const int st = it & 1;
+      mbar_wait(&q_full[st], (it >> 1) & 1);
+      mbar_wait(sp_empty, (it & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
+      if (lane == 0) {
+        const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+#pragma unroll
+        for (int k = 0; k < kD / 16; ++k) {
+          umma_bf16(tmem, smem_desc_sw128(qa + k * 32, 16, 1024), smem_desc_sw128(kb + k * 32, 16, 1024),
+                    id_s, k > 0 ? 1u : 0u);
+          umma_bf16(tmem + 128, smem_desc_sw128(doa + k * 32, 16, 1024),
+                    smem_desc_sw128(vb + k * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(sp_full);
+      }
+      __syncwarp();
+      mbar_wait(ds_full, it & 1);
+      mbar_wait(dq_empty, (it & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS), kb = smem_u32(sK);
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k) {
+          // K = queries: MN-major A (keys contiguous, two 64-key atoms 16 KB apart)
+          const uint64_t a_p = smem_desc_sw128(pa + k * 2048, kPBytes / 2, 1024);
+          const uint64_t a_ds = smem_desc_sw128(dsa + k * 2048, kPBytes / 2, 1024);
+          const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+          umma_bf16(tmem + 256, a_p, smem_desc_sw128(doa + k * 2048, kD * 128, 1024), id_kv, acc);
+          umma_bf16(tmem + 320, a_ds, smem_desc_sw128(qa + k * 2048, kD * 128, 1024), id_kv, acc);
+          // dQ: K = keys: dS K-major (two atoms), K_j MN-major
+          umma_bf16(tmem + 384, smem_desc_sw128(dsa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024),
+                    smem_desc_sw128(kb + k * 2048, kD * 128, 1024), id_q, k > 0 ? 1u : 0u);
+        }
+        umma_commit(dq_full);
+        umma_commit(ds_empty);
+        umma_commit(&q_empty[st]);
+      }
+      __syncwarp();
+    }
+    if (lane == 0) umma_commit(dkv_full);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int r = (warp - 4) * 32 + lane;  // query row (S, dP, dQ) / key row (dV, dK)
+    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    const float lse_scale = 1.4426950408889634f;
+    for (int i = i0, it = 0; i < n_q; ++i, ++it) {
+      const int q = i * kTile + r;
+      const bool qok = q < p.seq;
+      const long long sidx = ((long long)bb * p.heads + h) * p.seq + (qok ? q : 0);
+      const float lse2 = qok ? p.lse[sidx] * lse_scale : 0.f;
+      const float Dq = qok ? p.D[sidx] : 0.f;
+      mbar_wait(sp_full, it & 1);
+      mbar_wait(ds_empty, (it & 1) ^ 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < kTile / 32; ++c) {
+        uint32_t us[32], ud[32];
+        tmem_ld_32x32b_x32(tmem + c * 32 + lane_off, us);
+        tmem_ld_32x32b_x32(tmem + 128 + c * 32 + lane_off, ud);
+        tmem_ld_wait();
+        float pv[32], dsv[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int key = k0 + c * 32 + e;
+          const bool ok = qok && key < p.seq && (!p.causal || key <= q);
+          const float pr = ok ? exp2f(__uint_as_float(us[e]) * p.scale_log2 - lse2) : 0.f;
+          pv[e] = pr;
+          dsv[e] = pr * (__uint_as_float(ud[e]) - Dq) * p.scale;
+        }
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const int cc = c * 4 + w;  // 16-byte chunk index over the 128 keys
+          uint4 a, b2;
+          a.x = pack_bf16(pv[w * 8 + 0], pv[w * 8 + 1]);
+          a.y = pack_bf16(pv[w * 8 + 2], pv[w * 8 + 3]);
+          a.z = pack_bf16(pv[w * 8 + 4], pv[w * 8 + 5]);
+          a.w = pack_bf16(pv[w * 8 + 6], pv[w * 8 + 7]);
+          b2.x = pack_bf16(dsv[w * 8 + 0], dsv[w * 8 + 1]);
+          b2.y = pack_bf16(dsv[w * 8 + 2], dsv[w * 8 + 3]);
+          b2.z = pack_bf16(dsv[w * 8 + 4], dsv[w * 8 + 5]);
+          b2.w = pack_bf16(dsv[w * 8 + 6], dsv[w * 8 + 7]);
+          const uint32_t off = (cc >> 3) * (kPBytes / 2) + sw128(r, cc & 7);
+          *reinterpret_cast<uint4*>(sP + off) = a;
+          *reinterpret_cast<uint4*>(sdS + off) = b2;
+        }
+      }
+      tc_fence_before();
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(sp_empty);
+        mbar_arrive(ds_full);
+      }
+      // dQ_i (this KV tile's contribution) -> f32 accumulator
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t u[32];
+        tmem_ld_32x32b_x32(tmem + 384 + c * 32 + lane_off, u);
+        tmem_ld_wait();
+        if (qok) {
+          float* dst = p.dq + (long long)(row0 + q) * p.H + h * kD + c * 32;
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            red_add_v4f(dst + e, __uint_as_float(u[e]), __uint_as_float(u[e + 1]),
+                        __uint_as_float(u[e + 2]), __uint_as_float(u[e + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+    }
+    // dV, dK of this key tile (TMEM lane = key row)
+    mbar_wait(dkv_full, 0);
+    tc_fence_after();
+    const int key = k0 + r;
+    const bool any = i0 < n_q;
+    if (key < p.seq) {
+      __nv_bfloat16* dk = p.dqkv + (long long)(row0 + key) * 3 * p.H + p.H + h * kD;
+      __nv_bfloat16* dv = p.dqkv + (long long)(row0 + key) * 3 * p.H + 2 * p.H + h * kD;
+#pragma unroll
+      for (int c = 0; c < kD / 32; ++c) {
+        uint32_t uv[32], uk[32];
+        tmem_ld_32x32b_x32(tmem + 256 + c * 32 + lane_off, uv);
+        tmem_ld_32x32b_x32(tmem + 320 + c * 32 + lane_off, uk);
+        tmem_ld_wait();
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          uint4 a, b2;
+          float fv[8], fk[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            fv[e] = any ? __uint_as_float(uv[w * 8 + e]) : 0.f;
+            fk[e] = any ? __uint_as_float(uk[w * 8 + e]) : 0.f;
+          }
+          a.x = pack_bf16(fv[0], fv[1]); a.y = pack_bf16(fv[2], fv[3]);
+          a.z = pack_bf16(fv[4], fv[5]); a.w = pack_bf16(fv[6], fv[7]);
+          b2.x = pack_bf16(fk[0], fk[1]); b2.y = pack_bf16(fk[2], fk[3]);
+          b2.z = pack_bf16(fk[4], fk[5]); b2.w = pack_bf16(fk[6], fk[7]);
+          reinterpret_cast<uint4*>(dv + c * 32)[w] = a;
+          reinterpret_cast<uint4*>(dk + c * 32)[w] = b2;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
+// D[b, h, q] = sum_c dO[row, h*64 + c] * O[row, h*64 + c]; one warp per (row, head)
+__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+                                     const __nv_bfloat16* __restrict__ dout, float* __restrict__ D,
+                                     long long rows, int seq, int heads) {
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= rows * heads) return;
+  const long long row = w / heads;
+  const int h = (int)(w % heads);
+  const long long base = row * heads * kD + h * kD + lane * 2;
+  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + base));
+  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + base));
+  const float s = warp_sum(a.x * b.x + a.y * b.y);
+  if (lane == 0) {
+    const long long bb = row / seq, q = row % seq;
+    D[(bb * heads + h) * seq + q] = s;
+  }
+}
+
+// dqkv[:, 0:H] = bf16(dq)
+__global__ void attn_dq_store_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
+                                     long long rows, int H) {
+  const long long n4 = rows * H / 4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 v = reinterpret_cast<const float4*>(dq)[i];
+    const long long e = i * 4, row = e / H, col = e % H;
+    uint2 w;
+    w.x = pack_bf16(v.x, v.y);
+    w.y = pack_bf16(v.z, v.w);
+    *reinterpret_cast<uint2*>(dqkv + row * 3 * H + col) = w;
+  }
+}
+
+constexpr int kBwdSmem = 1024 + kTileBytes * 6 + 2 * kPBytes + 256;
+
+}  // namespace
+}  // namespace dpn
+
+using namespace dpn;
+
+extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batch, int64_t seq,
+                            int64_t heads, int64_t head_dim, float scale, int causal,
+                            void* stream) {
+  DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
+  DPN_REQUIRE(seq % 64 == 0 && seq > 0, "seq must be a positive multiple of 64");
+  DPN_REQUIRE(qkv && out && lse, "null pointer");
+  CUtensorMap tm;
+  const long long H = heads * head_dim;
+  int rc = map_2d(&tm, qkv, batch * seq, 3 * H);
+  if (rc) return rc;
+  AttnParams p{};
+  p.batch = (int)batch;
+  p.seq = (int)seq;
+  p.heads = (int)heads;
+  p.H = (int)H;
+  p.scale = scale;
+  p.scale_log2 = scale * kLog2e;
+  p.causal = causal;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.lse = lse;
+  static bool set = false;
+  if (!set) {
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kFwdSmem));
+    set = true;
+  }
+  dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
+  attn_fwd_kernel<<<grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream>>>(tm, p);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                            void* dqkv, float* workspace, int64_t workspace_floats, int64_t batch,
+                            int64_t seq, int64_t heads, int64_t head_dim, float scale, int causal,
+                            void* stream) {
+  DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
+  DPN_REQUIRE(seq % 64 == 0 && seq > 0, "seq must be a positive multiple of 64");
+  const long long H = heads * head_dim, rows = batch * seq;
+  DPN_REQUIRE(workspace != nullptr && workspace_floats >= rows * H + batch * heads * seq,
+              "workspace must hold batch*seq*(heads*64) + batch*heads*seq floats");
+  cudaStream_t st = (cudaStream_t)stream;
+  float* dq = workspace;
+  float* D = workspace + rows * H;
+  DPN_CHECK_CUDA(cudaMemsetAsync(dq, 0, sizeof(float) * rows * H, st));
+  const long long warps = rows * heads;
+  attn_bwd_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
+      (const __nv_bfloat16*)out, (const __nv_bfloat16*)dout, D, rows, (int)seq, (int)heads);
+  DPN_LAUNCH_CHECK();
+  CUtensorMap tq, td;
+  int rc = map_2d(&tq, qkv, rows, 3 * H);
+  if (rc) return rc;
+  rc = map_2d(&td, dout, rows, H);
+  if (rc) return rc;
+  AttnBwdParams p{};
+  p.seq = (int)seq;
+  p.heads = (int)heads;
+  p.H = (int)H;
+  p.scale = scale;
+  p.scale_log2 = scale * kLog2e;
+  p.causal = causal;
+  p.lse = lse;
+  p.D = D;
+  p.dq = dq;
+  p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  static bool set = false;
+  if (!set) {
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kBwdSmem));
+    set = true;
+  }
+  dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
+  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, st>>>(tq, td, p);
+  DPN_LAUNCH_CHECK();
+  attn_dq_store_kernel<<<(unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0, st>>>(
+      dq, (__nv_bfloat16*)dqkv, rows, (int)H);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}

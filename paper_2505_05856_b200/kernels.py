@@ -139,6 +139,28 @@ def linear_wgrad(dy, x, dw, accumulate=False, stream=None):
 # ---- node kernels -----------------------------------------------------------------
 
 
+def attn_fwd(qkv, out, lse, batch, seq, heads, causal, scale=None, stream=None):
+    """Fused attention forward from the [b*s, 3H] QKV buffer (head_dim 64)."""
+    d = 64
+    INSTR.launches += 1
+    check(lib().dpn_attn_fwd(qkv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch, seq, heads, d,
+                             scale if scale is not None else d ** -0.5, int(causal), _s(stream)),
+          "dpn_attn_fwd")
+
+
+def attn_bwd(qkv, out, dout, lse, dqkv, batch, seq, heads, causal, scale=None, stream=None):
+    """Fused attention backward -> dqkv [b*s, 3H] (dQ | dK | dV)."""
+    d = 64
+    H = heads * d
+    INSTR.launches += 3
+    with torch.cuda.stream(_torch_stream(stream)):
+        ws = _workspace(qkv.device, batch * seq * H + batch * heads * seq)
+    check(lib().dpn_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
+                             dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads, d,
+                             scale if scale is not None else d ** -0.5, int(causal), _s(stream)),
+          "dpn_attn_bwd")
+
+
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
     INSTR.launches += 1

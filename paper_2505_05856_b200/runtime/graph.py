@@ -18,8 +18,8 @@ from __future__ import annotations
 from typing import Dict, List, Optional, Tuple
 
 from ..planner.profile import ComputationGraph, ProfiledNode, TensorRef
-from .model import (NodeDef, TransformerConfig, backward_readers, build_nodes, output_spec,
-                    saved_for_backward, stats_bytes)
+from .model import (NodeDef, TransformerConfig, backward_readers, build_nodes, has_stats,
+                    output_spec, saved_for_backward, stats_bytes)
 
 
 def tensor_bytes(shape, dtype) -> int:
@@ -64,6 +64,8 @@ def analytic_times(cfg: TransformerConfig, b: int, tflops: float = 900.0,
             fl = 2 * M * cfg.vocab_padded * H
         elif n.kind in ("score", "attn"):
             fl = 2 * b * cfg.heads * s * s * cfg.head_dim
+        elif n.kind == "attn_fused":
+            fl = 4 * b * cfg.heads * s * s * cfg.head_dim
         tf = max(1, int(round(max(fl / (tflops * 1e6), 2 * byt / (gbs * 1e3)))))
         tb = max(1, int(round(max(2 * fl / (tflops * 1e6), 3 * byt / (gbs * 1e3)))))
         out[n.id] = (tf, tb)
@@ -102,10 +104,10 @@ def profile_graph(cfg: TransformerConfig, b: int,
         m_a = tensor_bytes(shape, dt) + stats_bytes(cfg, n, b)
         saved = []
         if saved_for_backward(n):
-            rd = [index[r] for r in readers[n.id] if r != n.id or n.kind in ("score", "head")]
+            rd = [index[r] for r in readers[n.id]]
             if rd:
                 saved.append(TensorRef(out_tid(n.id), tensor_bytes(shape, dt), n.id, min(rd)))
-        if n.kind == "ln":
+        if has_stats(n):
             saved.append(TensorRef(stats_tid(n.id), stats_bytes(cfg, n, b), n.id, i))
         t_f, t_b = times[n.id]
         out.append(ProfiledNode(

@@ -33,6 +33,9 @@ class TransformerConfig:
     seq: int
     causal: bool = False
     ln_eps: float = 1e-5
+    # one fused flash-style `attn` node (QKV -> context, P never materialised)
+    # instead of the reference vocabulary's `score` + `attn` pair
+    fused_attention: bool = True
 
     @property
     def head_dim(self) -> int:
@@ -69,6 +72,7 @@ PRESETS: Dict[str, TransformerConfig] = {
     # small shapes for parity tests
     "tiny": TransformerConfig("tiny", 2, 128, 2, 512, 1000, 64),
     "tiny-causal": TransformerConfig("tiny-causal", 3, 128, 2, 256, 512, 128, causal=True),
+    "tiny-unfused": TransformerConfig("tiny-unfused", 2, 128, 2, 512, 1000, 64, fused_attention=False),
 }
 
 
@@ -90,8 +94,13 @@ def build_nodes(cfg: TransformerConfig) -> List[NodeDef]:
         nodes += [
             NodeDef(p + "ln1", "ln", (x,), (("gamma", (H,)), ("beta", (H,))), b),
             NodeDef(p + "qkv", "linear", (p + "ln1",), (("weight", (3 * H, H)), ("bias", (3 * H,))), b),
-            NodeDef(p + "score", "score", (p + "qkv",), (), b),
-            NodeDef(p + "attn", "attn", (p + "score", p + "qkv"), (), b),
+        ]
+        if cfg.fused_attention:
+            nodes.append(NodeDef(p + "attn", "attn_fused", (p + "qkv",), (), b))
+        else:
+            nodes += [NodeDef(p + "score", "score", (p + "qkv",), (), b),
+                      NodeDef(p + "attn", "attn", (p + "score", p + "qkv"), (), b)]
+        nodes += [
             NodeDef(p + "proj", "linear_res", (p + "attn", x), (("weight", (H, H)), ("bias", (H,))), b),
             NodeDef(p + "ln2", "ln", (p + "proj",), (("gamma", (H,)), ("beta", (H,))), b),
             NodeDef(p + "fc1", "linear", (p + "ln2",), (("weight", (F, H)), ("bias", (F,))), b),
@@ -109,7 +118,7 @@ def output_spec(cfg: TransformerConfig, node: NodeDef, b: int) -> Tuple[Tuple[in
     """Shape/dtype of a node's forward output for micro-batch size b."""
     M, H = b * cfg.seq, cfg.hidden
     k = node.kind
-    if k in ("embed", "ln", "attn", "linear_res", "add"):
+    if k in ("embed", "ln", "attn", "attn_fused", "linear_res", "add"):
         return (M, H), torch.bfloat16
     if k == "linear":
         return (M, dict(node.params)["weight"][0]), torch.bfloat16
@@ -123,8 +132,17 @@ def output_spec(cfg: TransformerConfig, node: NodeDef, b: int) -> Tuple[Tuple[in
 
 
 def stats_bytes(cfg: TransformerConfig, node: NodeDef, b: int) -> int:
-    """Per-row LayerNorm statistics (mean, rstd fp32) saved next to the output."""
-    return 8 * b * cfg.seq if node.kind == "ln" else 0
+    """Side statistics saved next to the output: LayerNorm (mean, rstd) per row,
+    fused attention's log-sum-exp per (batch, head, query); fp32."""
+    if node.kind == "ln":
+        return 8 * b * cfg.seq
+    if node.kind == "attn_fused":
+        return 4 * b * cfg.heads * cfg.seq
+    return 0
+
+
+def has_stats(node: NodeDef) -> bool:
+    return node.kind in ("ln", "attn_fused")
 
 
 def saved_for_backward(node: NodeDef) -> bool:
@@ -149,6 +167,9 @@ def backward_readers(nodes: List[NodeDef]) -> Dict[str, List[str]]:
         elif n.kind == "attn":
             readers[n.inputs[0]].append(n.id)         # P for dV
             readers[n.inputs[1]].append(n.id)         # V for dP
+        elif n.kind == "attn_fused":
+            readers[n.inputs[0]].append(n.id)         # Q, K, V (S and P are recomputed)
+            readers[n.id].append(n.id)                # O for D = rowsum(dO * O)
     # (LayerNorm statistics are a separate tensor, read only by their own node)
     return readers
 

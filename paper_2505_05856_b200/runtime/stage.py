@@ -39,8 +39,8 @@ from .. import kernels as K
 from ..planner.memplan import MemOptPlan, producer_chain
 from ..planner.profile import ComputationGraph
 from .graph import out_tid, stats_tid
-from .model import (AdamWConfig, NodeDef, TransformerConfig, backward_readers, output_spec,
-                    saved_for_backward)
+from .model import (AdamWConfig, NodeDef, TransformerConfig, backward_readers, has_stats,
+                    output_spec, saved_for_backward)
 
 BF16 = torch.bfloat16
 F32 = torch.float32
@@ -172,7 +172,7 @@ class StageExecutor:
         # tensors some backward in this stage reads
         needed: Set[str] = set()
         for n in self.nodes:
-            if n.kind == "ln":
+            if has_stats(n):
                 needed.add(stats_tid(n.id))
         for src, rd in self.readers.items():
             if any(r in in_stage for r in rd) and saved_for_backward(self.node_by_id[src]):
@@ -199,7 +199,7 @@ class StageExecutor:
         self.host: Dict[str, List[torch.Tensor]] = {}
         self.live: Dict[str, torch.Tensor] = {}
         ids_needed = {out_tid(n) for n in self._produced_or_received()}
-        ids_needed |= {stats_tid(n.id) for n in self.nodes if n.kind == "ln"}
+        ids_needed |= {stats_tid(n.id) for n in self.nodes if has_stats(n)}
         for tid in sorted(ids_needed):
             shape, dt = self._spec(tid)
             if tid in needed and tid not in self.evicted:
@@ -258,7 +258,7 @@ class StageExecutor:
         self.bwd_reads: Dict[str, List[str]] = {}
         for n in self.nodes:
             reads = [out_tid(src) for src, rd in self.readers.items() if n.id in rd]
-            if n.kind == "ln":
+            if has_stats(n):
                 reads.append(stats_tid(n.id))
             if n.id in self.bwd_gelu_of:  # fused GELU backward reads the pre-activation
                 reads.append(out_tid(self.node_by_id[self.bwd_gelu_of[n.id]].inputs[0]))
@@ -290,6 +290,8 @@ class StageExecutor:
         nid, kind = tid.rsplit(".", 1)
         node = self.node_by_id[nid]
         if kind == "stats":
+            if node.kind == "attn_fused":
+                return (self.b, self.cfg.heads, self.cfg.seq), F32
             return (2, self.M), F32
         return output_spec(self.cfg, node, self.b)
 
@@ -372,7 +374,7 @@ class StageExecutor:
         return self.buf(tid, self.slot_of(mb), "fwd")
 
     def _outputs(self, n: NodeDef) -> List[str]:
-        outs = [out_tid(n.id)] + ([stats_tid(n.id)] if n.kind == "ln" else [])
+        outs = [out_tid(n.id)] + ([stats_tid(n.id)] if has_stats(n) else [])
         if n.id in self.fwd_gelu_of:
             outs.append(out_tid(self.fwd_gelu_of[n.id]))
         return outs
@@ -442,6 +444,9 @@ class StageExecutor:
             K.softmax_fwd(out, out, cfg.seq, 1.0 / math.sqrt(cfg.head_dim), cfg.causal, stream=st)
         elif k == "attn":
             self._pv(inp[0], inp[1], out)
+        elif k == "attn_fused":
+            lse = self.buf(stats_tid(n.id), slot, phase)
+            K.attn_fwd(inp[0], out, lse, self.b, cfg.seq, cfg.heads, cfg.causal, stream=st)
         elif k == "head":
             K.linear_fwd(inp[0], W("weight"), out, stream=st)
             # fused loss + dlogits; on a recompute replay the loss is discarded
@@ -572,7 +577,7 @@ class StageExecutor:
     def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
         # outputs of a replayed node land in a live buffer if evicted, else in
         # their normal home (slot buffer or workspace)
-        for t in [out_tid(n.id)] + ([stats_tid(n.id)] if n.kind == "ln" else []):
+        for t in [out_tid(n.id)] + ([stats_tid(n.id)] if has_stats(n) else []):
             if t in self.evicted and t not in self.live:
                 self._alloc_live(t)
         self._node_fwd(n, slot, ver, "bwd")
@@ -664,6 +669,14 @@ class StageExecutor:
                        b_mn=True, b_s=(d, s * H), batch1=A, batch2=b, Cout=dqkv[:, 2 * H:],
                        ldc=3 * H, c_s=(d, s * 3 * H), stream=st)
             self.grad_init.add(P_t)
+        elif k == "attn_fused":
+            qkv_t = out_tid(n.inputs[0])
+            assert qkv_t not in self.grad_init
+            dqkv = self.grad_buffer(qkv_t)
+            K.attn_bwd(self.buf(qkv_t, slot, "bwd"), self.buf(tid, slot, "bwd"), dy,
+                       self.buf(stats_tid(n.id), slot, "bwd"), dqkv, self.b, cfg.seq, cfg.heads,
+                       cfg.causal, stream=st)
+            self.grad_init.add(qkv_t)
         elif k == "score":
             qkv_t = out_tid(n.inputs[0])
             Pm = self.buf(tid, slot, "bwd")

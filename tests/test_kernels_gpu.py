@@ -303,3 +303,50 @@ def test_gemm_fused_gelu_backward():
     torch.nn.functional.gelu(fr, approximate="tanh").backward(dy.float() @ w.float())
     torch.cuda.synchronize()
     close(dx, fr.grad)
+
+
+def _attn_ref(qkv, b, s, A, causal):
+    H = A * 64
+    q = qkv[:, :H].float().reshape(b, s, A, 64).transpose(1, 2)
+    k = qkv[:, H:2 * H].float().reshape(b, s, A, 64).transpose(1, 2)
+    v = qkv[:, 2 * H:].float().reshape(b, s, A, 64).transpose(1, 2)
+    sc = q @ k.transpose(-1, -2) / 8.0
+    if causal:
+        sc = sc.masked_fill(torch.ones(s, s, device="cuda", dtype=torch.bool).triu(1), float("-inf"))
+    lse = torch.logsumexp(sc, -1)
+    o = torch.softmax(sc, -1) @ v
+    return o.transpose(1, 2).reshape(b * s, H), lse
+
+
+@pytest.mark.parametrize("b,s,A,causal", [(2, 128, 2, False), (2, 512, 3, False), (1, 512, 2, True),
+                                          (3, 64, 2, False), (2, 192, 2, True), (2, 1024, 1, True)])
+def test_fused_attention_forward(b, s, A, causal):
+    k = K()
+    qkv = rnd(b * s, 3 * A * 64, scale=1.5)
+    out = torch.empty(b * s, A * 64, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, A, s, device="cuda")
+    k.attn_fwd(qkv, out, lse, b, s, A, causal)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = _attn_ref(qkv, b, s, A, causal)
+    close(out, o_ref)
+    assert (lse - lse_ref).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("b,s,A,causal", [(2, 128, 2, False), (2, 512, 2, False), (1, 512, 2, True),
+                                          (3, 64, 2, False), (2, 192, 1, True), (1, 1024, 1, True)])
+def test_fused_attention_backward(b, s, A, causal):
+    k = K()
+    H = A * 64
+    qkv = rnd(b * s, 3 * H, scale=1.5)
+    out = torch.empty(b * s, H, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, A, s, device="cuda")
+    k.attn_fwd(qkv, out, lse, b, s, A, causal)
+    dout = rnd(b * s, H)
+    dqkv = torch.empty_like(qkv)
+    k.attn_bwd(qkv, out, dout, lse, dqkv, b, s, A, causal)
+    torch.cuda.synchronize()
+    x = qkv.float().requires_grad_()
+    o_ref, _ = _attn_ref(x, b, s, A, causal)
+    o_ref.backward(dout.float())
+    for part in range(3):
+        close(dqkv[:, part * H:(part + 1) * H], x.grad[:, part * H:(part + 1) * H])

@@ -50,7 +50,8 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
     nodes = [n.id for n in build_nodes(cfg)]
     stage_nodes = [nodes[lo:hi + 1] for lo, hi in stage_bounds(plan.cuts, len(g))]
     dims = dict(layers=cfg.layers, hidden=cfg.hidden, heads=cfg.heads, seq=cfg.seq,
-                vocab=cfg.vocab, causal=cfg.causal, ln_eps=cfg.ln_eps)
+                vocab=cfg.vocab, causal=cfg.causal, ln_eps=cfg.ln_eps,
+                fused_attention=cfg.fused_attention)
     init = init_params(cfg, 0)
     ref_losses, ref_params = reference_train(
         dims, init, ids, labels, stage_nodes,
@@ -99,11 +100,25 @@ def test_pipeline_matches_oracle_causal_three_stages():
     _compare(cfg, g, plan)
 
 
-@pytest.mark.parametrize("bw", [16 << 30, 50 << 20])
-def test_pipeline_executes_memopt_actions(bw):
-    """A tight capacity makes the planner pick swaps (fast link) or recomputes
+@pytest.mark.parametrize("stages", [2, 3])
+def test_pipeline_unfused_attention_vocabulary(stages):
+    """The reference vocabulary's materialised `score` + `attn` pair."""
+    cfg, g, plan = _setup("tiny-unfused", stages, 4.0, 16 << 30)
+    assert any(n.id.endswith(".score") for n in g.nodes)
+    _compare(cfg, g, plan)
+
+
+def test_pipeline_memopt_causal_four_stages():
+    cfg, g, plan = _setup("tiny-causal", 4, 0.5, 16 << 30)
+    assert any(m.actions for m in plan.memopt)
+    _compare(cfg, g, plan)
+
+
+@pytest.mark.parametrize("frac,bw", [(0.6, 16 << 30), (0.6, 50 << 20), (0.7, 16 << 30)])
+def test_pipeline_executes_memopt_actions(frac, bw):
+    """A tight capacity makes the planner pick swaps (fast link) and recomputes
     (slow link); the run must execute them and still match the oracle."""
-    cfg, g, plan = _setup("tiny", 2, 0.55, bw)
+    cfg, g, plan = _setup("tiny", 2, frac, bw)
     kinds = {a.kind for m in plan.memopt for a in m.actions}
     assert kinds, "expected memopt actions at this capacity"
     _compare(cfg, g, plan)

@@ -10,11 +10,11 @@ from paper_2505_05856_b200.runtime.model import PRESETS, build_nodes, init_param
 from paper_2505_05856_b200.runtime.pipeline import colocated_order
 
 
-@pytest.mark.parametrize("name", ["tiny", "bert-base", "bert-large", "gpt2-xl"])
+@pytest.mark.parametrize("name", ["tiny", "tiny-unfused", "bert-base", "bert-large", "gpt2-xl"])
 def test_profile_graph_is_a_valid_schema1_profile(name, tmp_path):
     cfg = PRESETS[name]
     g = profile_graph(cfg, 2)
-    assert len(g) == 3 + 10 * cfg.layers
+    assert len(g) == 3 + (9 if cfg.fused_attention else 10) * cfg.layers
     f = tmp_path / "p.json"
     P.save_profile(g, f)
     g2 = P.load_profile(f)
