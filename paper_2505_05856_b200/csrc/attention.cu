@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
   // TMEM columns: S[0] 0..127, S[1] 128..255, O[0] 256..319, O[1] 320..383
 
   if (warp == 0) {
@@ -411,6 +412,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();
   // TMEM columns: S 0..127, dP 128..255, dV 256..319, dK 320..383, dQ 384..447
 
   if (warp == 0) {
@@ -591,6 +593,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                      const __nv_bfloat16* __restrict__ dout, float* __restrict__ D,
                                      long long rows, int seq, int heads) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= rows * heads) return;
@@ -609,6 +612,7 @@ __global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
 // dqkv[:, 0:H] = bf16(dq)
 __global__ void attn_dq_store_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
                                      long long rows, int H) {
+  pdl_wait();
   const long long n4 = rows * H / 4;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
@@ -655,7 +659,7 @@ extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batc
     set = true;
   }
   dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
-  attn_fwd_kernel<<<grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream>>>(tm, p);
+  DPN_CHECK_CUDA(launch_pdl(attn_fwd_kernel, grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream, tm, p));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -674,8 +678,8 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
   float* D = workspace + rows * H;
   DPN_CHECK_CUDA(cudaMemsetAsync(dq, 0, sizeof(float) * rows * H, st));
   const long long warps = rows * heads;
-  attn_bwd_prep_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(
-      (const __nv_bfloat16*)out, (const __nv_bfloat16*)dout, D, rows, (int)seq, (int)heads);
+  DPN_CHECK_CUDA(launch_pdl(attn_bwd_prep_kernel, (unsigned)((warps + 7) / 8), 256, 0, st, 
+      (const __nv_bfloat16*)out, (const __nv_bfloat16*)dout, D, rows, (int)seq, (int)heads));
   DPN_LAUNCH_CHECK();
   CUtensorMap tq, td;
   int rc = map_2d(&tq, qkv, rows, 3 * H);
@@ -700,10 +704,10 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
     set = true;
   }
   dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
-  attn_bwd_kernel<<<grid, kBwdThreads, kBwdSmem, st>>>(tq, td, p);
+  DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, td, p));
   DPN_LAUNCH_CHECK();
-  attn_dq_store_kernel<<<(unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0, st>>>(
-      dq, (__nv_bfloat16*)dqkv, rows, (int)H);
+  DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel, (unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0, st, 
+      dq, (__nv_bfloat16*)dqkv, rows, (int)H));
   DPN_LAUNCH_CHECK();
   return 0;
 }

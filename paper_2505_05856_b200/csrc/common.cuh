@@ -9,6 +9,7 @@
 
 #include <cstdio>
 #include <string>
+#include <utility>
 
 namespace dpn {
 
@@ -48,7 +49,30 @@ const char* last_error();
 
 enum DType : int { kF32 = 0, kBF16 = 1 };
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialization and calls pdl_wait() after its data-independent
+// prologue (barrier init, TMEM alloc, descriptor prefetch), so its launch and
+// prologue overlap the tail of the previous kernel on the stream.
+template <typename... ExpTypes, typename... ActTypes>
+inline cudaError_t launch_pdl(void (*kernel)(ExpTypes...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, ActTypes&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<ActTypes>(args)...);
+}
+
 // ---- device helpers ------------------------------------------------------------
+
+// Wait for the previous kernel on the stream (no-op without PDL launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

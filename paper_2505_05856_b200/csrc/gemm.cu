@@ -28,6 +28,7 @@
 #include "../../include/dawnpiper.h"
 
 #include <mutex>
+#include <unordered_map>
 
 namespace dpn {
 namespace {
@@ -275,6 +276,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -435,9 +437,56 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-// 4-D map over a bf16 operand: (inner, z1, outer, z2); box (64, 1, box_outer, 1).
+// Encoded maps are cached by their full description (a map holds no reference
+// to the memory, so an identical key always yields an identical map): the
+// executor issues the same few hundred GEMM call sites every step.
+struct MapKey {
+  const void* ptr;
+  long long inner, outer, ld, s1, s2;
+  int Z1, Z2, box;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && inner == o.inner && outer == o.outer && ld == o.ld && s1 == o.s1 &&
+           s2 == o.s2 && Z1 == o.Z1 && Z2 == o.Z2 && box == o.box;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    for (long long v : {k.inner, k.outer, k.ld, k.s1, k.s2, (long long)k.Z1, (long long)k.Z2,
+                        (long long)k.box})
+      h = h * 1000003u ^ std::hash<long long>()(v);
+    return h;
+  }
+};
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+int encode_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld,
+               int Z1, long long s1, int Z2, long long s2, int box_outer);
+
 int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld,
              int Z1, long long s1, int Z2, long long s2, int box_outer) {
+  const MapKey key{ptr, inner, outer, ld, s1, s2, Z1, Z2, box_outer};
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *map = it->second;
+      return 0;
+    }
+  }
+  const int rc = encode_map(map, ptr, inner, outer, ld, Z1, s1, Z2, s2, box_outer);
+  if (rc == 0) {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_maps.size() > 65536) g_maps.clear();
+    g_maps.emplace(key, *map);
+  }
+  return rc;
+}
+
+// 4-D map over a bf16 operand: (inner, z1, outer, z2); box (64, 1, box_outer, 1).
+int encode_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld,
+               int Z1, long long s1, int Z2, long long s2, int box_outer) {
   EncodeFn enc = encode_fn();
   DPN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
   DPN_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0, "operand base must be 16-byte aligned");
@@ -533,13 +582,15 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = C::kSmem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = CG;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   DPN_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
   return 0;
 }

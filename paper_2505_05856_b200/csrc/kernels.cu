@@ -54,6 +54,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
                                                      float* __restrict__ mean_out,
                                                      float* __restrict__ rstd_out, long long rows,
                                                      int cols, float eps) {
+  pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
@@ -115,6 +116,7 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_kernel(
     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
     float* __restrict__ partial, long long rows, int cols) {
+  pdl_wait();
   extern __shared__ float red[];  // [warps][2][cols]
   const int warps = blockDim.x >> 5;
   const int wid = threadIdx.x >> 5;
@@ -201,6 +203,7 @@ __global__ void __launch_bounds__(1024) reduce_rows_kernel(const float* __restri
                                                            int nrows, int width,
                                                            float* __restrict__ out0,
                                                            float* __restrict__ out1, int split) {
+  pdl_wait();
   __shared__ float acc_s[32][33];
   const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const __nv_bfloat16* _
                                                           __nv_bfloat16* __restrict__ p,
                                                           long long rows, int cols, int q_len,
                                                           float alpha, int causal) {
+  pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
@@ -279,6 +283,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const __nv_bfloat16* _
                                                           const __nv_bfloat16* __restrict__ dp,
                                                           __nv_bfloat16* __restrict__ ds,
                                                           long long rows, int cols, float alpha) {
+  pdl_wait();
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
@@ -314,6 +319,7 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const __nv_bfloat16* _
 
 __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                 long long n8) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
        i += (long long)gridDim.x * blockDim.x) {
     float v[8];
@@ -327,6 +333,7 @@ __global__ void gelu_fwd_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat
 __global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
                                 const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ dx,
                                 long long n8) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
        i += (long long)gridDim.x * blockDim.x) {
     float g[8], v[8];
@@ -340,6 +347,7 @@ __global__ void gelu_bwd_kernel(const __nv_bfloat16* __restrict__ dy,
 
 __global__ void add_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_bfloat16* out,
                            long long n8) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
        i += (long long)gridDim.x * blockDim.x) {
     float u[8], v[8];
@@ -353,6 +361,7 @@ __global__ void add_kernel(const __nv_bfloat16* a, const __nv_bfloat16* b, __nv_
 
 __global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ y,
                             long long n) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16(x[i]);
@@ -366,7 +375,8 @@ __global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restri
 __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
                                                      long long rows, int cols, long long ld,
                                                      long long rows_per_cta,
-                                                     float* __restrict__ partial) {
+                                                     float* __restrict__ out) {
+  pdl_wait();
   __shared__ float part[256 * 8];
   const int nvec = cols >> 3;
   const int cw = min(nvec, 256);       // chunks per CTA
@@ -398,9 +408,8 @@ __global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __rest
     }
   }
   if (lr == 0 && chunk < nvec) {
-    float* dst = partial + (long long)blockIdx.x * cols + chunk * 8;
-    *reinterpret_cast<float4*>(dst) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[4], acc[5], acc[6], acc[7]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) atomicAdd(&out[chunk * 8 + k], acc[k]);
   }
 }
 
@@ -412,6 +421,7 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
                                                    long long rows, int vocab, float grad_scale,
                                                    float loss_scale, float* __restrict__ loss_sum,
                                                    __nv_bfloat16* __restrict__ dlogits) {
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t xsm[];
   __nv_bfloat16* row = reinterpret_cast<__nv_bfloat16*>(xsm);
   __shared__ float red[32];
@@ -487,6 +497,7 @@ __global__ void embed_fwd_kernel(const int* __restrict__ ids, const __nv_bfloat1
                                  const __nv_bfloat16* __restrict__ pos,
                                  __nv_bfloat16* __restrict__ out, long long rows, int seq,
                                  int hidden) {
+  pdl_wait();
   const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
   const int nvec = hidden >> 3;
   for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
@@ -507,6 +518,7 @@ __global__ void embed_fwd_kernel(const int* __restrict__ ids, const __nv_bfloat1
 __global__ void embed_bwd_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ dout,
                                  float* __restrict__ dtok, float* __restrict__ dpos,
                                  long long rows, int seq, int hidden) {
+  pdl_wait();
   const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
   const int nvec = hidden >> 3;
   for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
@@ -530,6 +542,7 @@ __global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ m, float
                              const float* __restrict__ g, __nv_bfloat16* __restrict__ out,
                              long long n4, float lr, float b1, float b2, float eps, float wd,
                              float bc1, float bc2) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 wv = reinterpret_cast<float4*>(w)[i];
@@ -571,14 +584,14 @@ using namespace dpn;
     const int nv = (int)((cols / 8 + 31) / 32);                                    \
     cudaStream_t st = (cudaStream_t)stream;                                        \
     switch (nv) {                                                                  \
-      case 1: KERNEL<1><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      case 2: KERNEL<2><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      case 3: KERNEL<3><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      case 4: KERNEL<4><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      case 5: KERNEL<5><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      case 6: KERNEL<6><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      case 7: KERNEL<7><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;              \
-      default: KERNEL<8><<<GRID, 256, SMEM, st>>>(__VA_ARGS__); break;             \
+      case 1: DPN_CHECK_CUDA(launch_pdl(KERNEL<1>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      case 2: DPN_CHECK_CUDA(launch_pdl(KERNEL<2>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      case 3: DPN_CHECK_CUDA(launch_pdl(KERNEL<3>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      case 4: DPN_CHECK_CUDA(launch_pdl(KERNEL<4>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      case 5: DPN_CHECK_CUDA(launch_pdl(KERNEL<5>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      case 6: DPN_CHECK_CUDA(launch_pdl(KERNEL<6>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      case 7: DPN_CHECK_CUDA(launch_pdl(KERNEL<7>, GRID, 256, SMEM, st, __VA_ARGS__)); break;              \
+      default: DPN_CHECK_CUDA(launch_pdl(KERNEL<8>, GRID, 256, SMEM, st, __VA_ARGS__)); break;             \
     }                                                                              \
   } while (0)
 
@@ -622,8 +635,8 @@ extern "C" int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamm
               (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, mean, rstd, (__nv_bfloat16*)dx,
               (const __nv_bfloat16*)dx_add, workspace, rows, (int)cols);
   DPN_LAUNCH_CHECK();
-  reduce_rows_kernel<<<(unsigned)((2 * cols + 31) / 32), 1024, 0, (cudaStream_t)stream>>>(
-      workspace, grid, (int)(2 * cols), dgamma, dbeta, (int)cols);
+  DPN_CHECK_CUDA(launch_pdl(reduce_rows_kernel, (unsigned)((2 * cols + 31) / 32), 1024, 0, (cudaStream_t)stream, 
+      workspace, grid, (int)(2 * cols), dgamma, dbeta, (int)cols));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -633,10 +646,10 @@ extern "C" int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamm
     const int per = (int)((cols / 8 + 31) / 32);                                 \
     const int g = grid_for(rows, 8);                                             \
     cudaStream_t st = (cudaStream_t)stream;                                      \
-    if (per <= 1) KERNEL<1><<<g, 256, 0, st>>>(__VA_ARGS__);                     \
-    else if (per <= 2) KERNEL<2><<<g, 256, 0, st>>>(__VA_ARGS__);                \
-    else if (per <= 4) KERNEL<4><<<g, 256, 0, st>>>(__VA_ARGS__);                \
-    else if (per <= 8) KERNEL<8><<<g, 256, 0, st>>>(__VA_ARGS__);                \
+    if (per <= 1) DPN_CHECK_CUDA(launch_pdl(KERNEL<1>, g, 256, 0, st, __VA_ARGS__));                     \
+    else if (per <= 2) DPN_CHECK_CUDA(launch_pdl(KERNEL<2>, g, 256, 0, st, __VA_ARGS__));                \
+    else if (per <= 4) DPN_CHECK_CUDA(launch_pdl(KERNEL<4>, g, 256, 0, st, __VA_ARGS__));                \
+    else if (per <= 8) DPN_CHECK_CUDA(launch_pdl(KERNEL<8>, g, 256, 0, st, __VA_ARGS__));                \
     else DPN_REQUIRE(false, "softmax rows longer than 2048 are not supported");  \
   } while (0)
 
@@ -664,8 +677,8 @@ extern "C" int dpn_softmax_bwd(const void* p, const void* dp, void* ds, int64_t 
 extern "C" int dpn_gelu_fwd(const void* x, void* y, int64_t n, void* stream) {
   DPN_REQUIRE(n % 8 == 0, "n must be a multiple of 8");
   if (n == 0) return 0;
-  gelu_fwd_kernel<<<grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, n / 8);
+  DPN_CHECK_CUDA(launch_pdl(gelu_fwd_kernel, grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream, 
+      (const __nv_bfloat16*)x, (__nv_bfloat16*)y, n / 8));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -673,8 +686,8 @@ extern "C" int dpn_gelu_fwd(const void* x, void* y, int64_t n, void* stream) {
 extern "C" int dpn_gelu_bwd(const void* dy, const void* x, void* dx, int64_t n, void* stream) {
   DPN_REQUIRE(n % 8 == 0, "n must be a multiple of 8");
   if (n == 0) return 0;
-  gelu_bwd_kernel<<<grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (__nv_bfloat16*)dx, n / 8);
+  DPN_CHECK_CUDA(launch_pdl(gelu_bwd_kernel, grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream, 
+      (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x, (__nv_bfloat16*)dx, n / 8));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -682,15 +695,15 @@ extern "C" int dpn_gelu_bwd(const void* dy, const void* x, void* dx, int64_t n, 
 extern "C" int dpn_add(const void* a, const void* b, void* out, int64_t n, void* stream) {
   DPN_REQUIRE(n % 8 == 0, "n must be a multiple of 8");
   if (n == 0) return 0;
-  add_kernel<<<grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream>>>(
-      (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, (__nv_bfloat16*)out, n / 8);
+  DPN_CHECK_CUDA(launch_pdl(add_kernel, grid_for(n / 8, 256), 256, 0, (cudaStream_t)stream, 
+      (const __nv_bfloat16*)a, (const __nv_bfloat16*)b, (__nv_bfloat16*)out, n / 8));
   DPN_LAUNCH_CHECK();
   return 0;
 }
 
 extern "C" int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream) {
   if (n == 0) return 0;
-  cast_kernel<<<grid_for(n, 256), 256, 0, (cudaStream_t)stream>>>(x, (__nv_bfloat16*)y, n);
+  DPN_CHECK_CUDA(launch_pdl(cast_kernel, grid_for(n, 256), 256, 0, (cudaStream_t)stream, x, (__nv_bfloat16*)y, n));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -699,20 +712,18 @@ extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld,
                           float* workspace, int64_t workspace_floats, void* stream) {
   DPN_REQUIRE(cols % 8 == 0 && ld % 8 == 0, "cols and ld must be multiples of 8");
   if (rows == 0) return 0;
+  (void)workspace;
+  (void)workspace_floats;
+  // single pass: <= 64 row bands per column group, one atomic per column per
+  // CTA (<= 64-way: cheaper than a second launch)
   const long long nvec = cols / 8;
   const int cw = (int)std::min<long long>(nvec, 256);
   const int gy = (int)((nvec + cw - 1) / cw);
-  const long long bands = std::max<long long>(1, std::min<long long>((296 + gy - 1) / gy, (rows + 7) / 8));
+  const long long bands = std::max<long long>(1, std::min<long long>(64, (rows + 31) / 32));
   const long long per = (rows + bands - 1) / bands;
-  const long long nb = (rows + per - 1) / per;
-  DPN_REQUIRE(workspace != nullptr && workspace_floats >= nb * cols,
-              "workspace must hold min(ceil(296 / ceil(cols/2048)), ceil(rows/8)) * cols floats");
-  dim3 grid((unsigned)nb, (unsigned)gy);
-  colsum_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const __nv_bfloat16*)x, rows, (int)cols, ld,
-                                                        per, workspace);
-  DPN_LAUNCH_CHECK();
-  reduce_rows_kernel<<<(unsigned)((cols + 31) / 32), 1024, 0, (cudaStream_t)stream>>>(
-      workspace, (int)nb, (int)cols, out, out, (int)cols);
+  dim3 grid((unsigned)((rows + per - 1) / per), (unsigned)gy);
+  DPN_CHECK_CUDA(launch_pdl(colsum_kernel, grid, 256, 0, (cudaStream_t)stream, (const __nv_bfloat16*)x, rows, (int)cols, ld,
+                                                        per, out));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -730,9 +741,9 @@ extern "C" int dpn_xent(const void* logits, int64_t ld, const int32_t* labels, i
                                         200 * 1024));
     set = true;
   }
-  xent_kernel<<<(int)std::min<long long>(rows, 148 * 4), 512, smem, (cudaStream_t)stream>>>(
+  DPN_CHECK_CUDA(launch_pdl(xent_kernel, (int)std::min<long long>(rows, 148 * 4), 512, smem, (cudaStream_t)stream, 
       (const __nv_bfloat16*)logits, ld, labels, rows, (int)vocab, grad_scale, loss_scale, loss_sum,
-      (__nv_bfloat16*)dlogits);
+      (__nv_bfloat16*)dlogits));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -741,9 +752,9 @@ extern "C" int dpn_embed_fwd(const int32_t* ids, const void* tok, const void* po
                              int64_t rows, int64_t seq, int64_t hidden, void* stream) {
   DPN_REQUIRE(hidden % 8 == 0, "hidden must be a multiple of 8");
   if (rows == 0) return 0;
-  embed_fwd_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(
+  DPN_CHECK_CUDA(launch_pdl(embed_fwd_kernel, grid_for(rows, 8), 256, 0, (cudaStream_t)stream, 
       ids, (const __nv_bfloat16*)tok, (const __nv_bfloat16*)pos, (__nv_bfloat16*)out, rows,
-      (int)seq, (int)hidden);
+      (int)seq, (int)hidden));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -752,8 +763,8 @@ extern "C" int dpn_embed_bwd(const int32_t* ids, const void* dout, float* dtok, 
                              int64_t rows, int64_t seq, int64_t hidden, void* stream) {
   DPN_REQUIRE(hidden % 8 == 0, "hidden must be a multiple of 8");
   if (rows == 0) return 0;
-  embed_bwd_kernel<<<grid_for(rows, 8), 256, 0, (cudaStream_t)stream>>>(
-      ids, (const __nv_bfloat16*)dout, dtok, dpos, rows, (int)seq, (int)hidden);
+  DPN_CHECK_CUDA(launch_pdl(embed_bwd_kernel, grid_for(rows, 8), 256, 0, (cudaStream_t)stream, 
+      ids, (const __nv_bfloat16*)dout, dtok, dpos, rows, (int)seq, (int)hidden));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -765,8 +776,8 @@ extern "C" int dpn_adamw(float* w, float* m, float* v, const float* g, void* out
   DPN_REQUIRE(step >= 1, "step counts from 1");
   if (n == 0) return 0;
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
-  adamw_kernel<<<grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream>>>(
-      w, m, v, g, (__nv_bfloat16*)out_bf16, n / 4, lr, beta1, beta2, eps, wd, bc1, bc2);
+  DPN_CHECK_CUDA(launch_pdl(adamw_kernel, grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream, 
+      w, m, v, g, (__nv_bfloat16*)out_bf16, n / 4, lr, beta1, beta2, eps, wd, bc1, bc2));
   DPN_LAUNCH_CHECK();
   return 0;
 }

@@ -34,15 +34,26 @@ INSTR = _Instrument()
 _WS = {}
 
 
-def _workspace(device, floats: int) -> torch.Tensor:
-    """Per-(device, stream) f32 scratch for two-phase column reductions.  Kernels
-    on one stream use it in stream order; streams never share one."""
-    key = (device, torch.cuda.current_stream(device).cuda_stream)
+def _workspace(device, floats: int, stream) -> torch.Tensor:
+    """Per-(device, stream) f32 scratch for two-phase reductions / attention.
+    Kernels on one stream use it in stream order; streams never share one."""
+    handle = _s(stream)
+    key = (device, handle)
     t = _WS.get(key)
     if t is None or t.numel() < floats:
-        t = torch.empty(max(floats, 1 << 20), dtype=F32, device=device)
+        ts = _torch_stream(stream)
+        with torch.cuda.stream(ts) if ts is not None else _nullctx():
+            t = torch.empty(max(floats, 1 << 20), dtype=F32, device=device)
         _WS[key] = t
     return t
+
+
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
 
 
 def _torch_stream(stream):
@@ -58,7 +69,9 @@ def _p(t: Optional[torch.Tensor]) -> Optional[int]:
 def _s(stream) -> Optional[int]:
     if stream is None:
         return torch.cuda.current_stream().cuda_stream
-    return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
 
 
 def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batch1=1, batch2=1,
@@ -66,28 +79,16 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
              aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, split_k=0,
              cta_group=0, residual_mode=0, stream=None) -> None:
     """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules."""
-    assert A.dtype == BF16 and B.dtype == BF16 and Cout.dtype in (BF16, F32)
-    g = GemmArgs()
-    g.M, g.N, g.K = int(M), int(N), int(K)
-    g.batch1, g.batch2 = int(batch1), int(batch2)
-    g.A, g.lda, g.a_s1, g.a_s2, g.a_mn_major = A.data_ptr(), int(lda), int(a_s[0]), int(a_s[1]), int(a_mn)
-    g.B, g.ldb, g.b_s1, g.b_s2, g.b_mn_major = B.data_ptr(), int(ldb), int(b_s[0]), int(b_s[1]), int(b_mn)
-    g.C, g.ldc, g.c_s1, g.c_s2 = Cout.data_ptr(), int(ldc), int(c_s[0]), int(c_s[1])
-    g.c_dtype = 0 if Cout.dtype == F32 else 1
-    g.accumulate = int(accumulate)
-    g.bias = _p(bias)
-    g.residual = _p(residual)
-    if residual is not None:
-        g.ldr = int(ldr if ldr is not None else ldc)
-        rs = r_s if r_s is not None else c_s
-        g.r_s1, g.r_s2 = int(rs[0]), int(rs[1])
-        g.residual_mode = int(residual_mode)
-    g.aux = _p(aux)
-    g.alpha = float(alpha)
-    g.gelu = int(gelu)
-    g.block_n = int(block_n)
-    g.split_k = int(split_k)
-    g.cta_group = int(cta_group)
+    rs = (r_s if r_s is not None else c_s) if residual is not None else (0, 0)
+    g = GemmArgs(M, N, K, batch1, batch2,
+                 A.data_ptr(), lda, a_s[0], a_s[1], a_mn,
+                 B.data_ptr(), ldb, b_s[0], b_s[1], b_mn,
+                 Cout.data_ptr(), ldc, c_s[0], c_s[1], 0 if Cout.dtype == F32 else 1, accumulate,
+                 None if bias is None else bias.data_ptr(),
+                 None if residual is None else residual.data_ptr(),
+                 (ldr if ldr is not None else ldc) if residual is not None else 0, rs[0], rs[1],
+                 residual_mode, None if aux is None else aux.data_ptr(), alpha, gelu, block_n,
+                 split_k, cta_group)
     INSTR.launches += 1
     ev = INSTR.gemm_events
     if ev is not None:
@@ -153,8 +154,7 @@ def attn_bwd(qkv, out, dout, lse, dqkv, batch, seq, heads, causal, scale=None, s
     d = 64
     H = heads * d
     INSTR.launches += 3
-    with torch.cuda.stream(_torch_stream(stream)):
-        ws = _workspace(qkv.device, batch * seq * H + batch * heads * seq)
+    ws = _workspace(qkv.device, batch * seq * H + batch * heads * seq, stream)
     check(lib().dpn_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                              dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads, d,
                              scale if scale is not None else d ** -0.5, int(causal), _s(stream)),
@@ -172,8 +172,7 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stream=None):
     rows, cols = x.shape
     INSTR.launches += 2
-    with torch.cuda.stream(_torch_stream(stream)):
-        ws = _workspace(x.device, 296 * 2 * cols)
+    ws = _workspace(x.device, 296 * 2 * cols, stream)
     check(lib().dpn_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                                   rstd.data_ptr(), dx.data_ptr(), _p(dx_add), dgamma.data_ptr(),
                                   dbeta.data_ptr(), rows, cols, ws.data_ptr(), ws.numel(),
@@ -220,9 +219,8 @@ def cast_f32_bf16(x, y, stream=None):
 
 def colsum(x, out, stream=None):
     rows, cols = x.shape
-    INSTR.launches += 2
-    with torch.cuda.stream(_torch_stream(stream)):
-        ws = _workspace(x.device, 296 * cols)
+    INSTR.launches += 1
+    ws = _workspace(x.device, 296 * cols, stream)
     check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), ws.data_ptr(),
                            ws.numel(), _s(stream)), "dpn_colsum")
 

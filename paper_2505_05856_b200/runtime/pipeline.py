@@ -223,6 +223,12 @@ class Pipeline:
     def step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
         """One training iteration (m micro-batches).  ids/labels: int32 [m, b*s] on
         the first / last stage's device.  Returns the device loss vector [m]."""
+        if len(self.streams) == 1:  # co-located: everything on one stream
+            with torch.cuda.stream(next(iter(self.streams.values()))):
+                return self._step(ids, labels, events)
+        return self._step(ids, labels, events)
+
+    def _step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
         with torch.cuda.stream(self.streams[self.stage_dev[-1]]):
             self.loss.zero_()
         pending: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}

@@ -94,6 +94,7 @@ class FlatParams:
         # weight-version ring bookkeeping (PipeDream stashing): the newest
         # version sits in `latest`; micro-batches in flight pin the slot their
         # forward read until their backward retires
+        self._build_views()
         self.latest = 0
         self.users: List[Set[int]] = [set() for _ in range(versions)]
         self.version_of: Dict[int, int] = {}
@@ -118,12 +119,17 @@ class FlatParams:
         raise RuntimeError("weight-version ring exhausted (more micro-batches in flight than slots)")
 
     def weight(self, version_slot: int, name: str) -> torch.Tensor:
-        s = self.slots[name]
-        return self.ring[version_slot, s.offset:s.offset + s.numel].view(s.shape)
+        return self._wviews[version_slot][name]
 
     def gradv(self, name: str) -> torch.Tensor:
-        s = self.slots[name]
-        return self.grad[s.offset:s.offset + s.numel].view(s.shape)
+        return self._gviews[name]
+
+    def _build_views(self) -> None:
+        # views are created once: the per-call slicing showed up in host profiles
+        self._wviews = [{n: self.ring[k, s.offset:s.offset + s.numel].view(s.shape)
+                         for n, s in self.slots.items()} for k in range(self.ring.shape[0])]
+        self._gviews = {n: self.grad[s.offset:s.offset + s.numel].view(s.shape)
+                        for n, s in self.slots.items()}
 
     def master_view(self, name: str) -> torch.Tensor:
         s = self.slots[name]
@@ -247,6 +253,18 @@ class StageExecutor:
                 if len(users) == 1 and users[0].kind == "linear":
                     self.bwd_gelu_of[users[0].id] = n.id
         self._skip_bwd: Set[str] = set()
+        # residual add fused into fc2's epilogue when both live in this stage:
+        # fc2's forward writes z + y straight into the add node's output
+        # (fc2's own output z is never materialised: nothing reads it later)
+        self.fwd_add_of: Dict[str, str] = {}    # fc2 id -> add id
+        recv_nodes = {t.rsplit(".", 1)[0] for t in self.recv_ids}
+        for n in self.nodes:
+            if n.kind == "add" and n.inputs[0] in in_stage and (
+                    n.inputs[1] in in_stage or n.inputs[1] in recv_nodes):
+                src = self.node_by_id[n.inputs[0]]
+                if (src.kind == "linear" and not saved_for_backward(src)
+                        and out_tid(src.id) not in self.send_ids):
+                    self.fwd_add_of[src.id] = n.id
         # lifetimes of evicted tensors (positions within this stage's node list)
         pos = {n.id: i for i, n in enumerate(self.nodes)}
         self.fwd_last: Dict[str, float] = {}
@@ -307,9 +325,10 @@ class StageExecutor:
         raise KeyError(f"stage {self.stage}: no buffer for {tid}")
 
     def _alloc_live(self, tid: str) -> torch.Tensor:
+        # callers run inside `with torch.cuda.stream(self.stream)` (forward /
+        # backward / the schedulers), so allocations are compute-stream ordered
         shape, dt = self._spec(tid)
-        with torch.cuda.stream(self.stream):
-            t = torch.empty(shape, dtype=dt, device=self.device)
+        t = torch.empty(shape, dtype=dt, device=self.device)
         self.live[tid] = t
         return t
 
@@ -342,7 +361,7 @@ class StageExecutor:
                     self._swap_out(tid, slot)
                 if tid in self.evicted and self.fwd_last[tid] < 0:
                     del self.live[tid]
-            fused_gelus = set(self.fwd_gelu_of.values())
+            fused_gelus = set(self.fwd_gelu_of.values()) | set(self.fwd_add_of.values())
             for i, n in enumerate(self.nodes):
                 produced = [] if n.id in fused_gelus else self._outputs(n)  # fused: fc1 made it
                 if any(t in self.swap_ids for t in produced):
@@ -377,6 +396,8 @@ class StageExecutor:
         outs = [out_tid(n.id)] + ([stats_tid(n.id)] if has_stats(n) else [])
         if n.id in self.fwd_gelu_of:
             outs.append(out_tid(self.fwd_gelu_of[n.id]))
+        if n.id in self.fwd_add_of:
+            outs.append(out_tid(self.fwd_add_of[n.id]))
         return outs
 
     def _swap_out(self, tid: str, slot: int) -> None:
@@ -427,9 +448,15 @@ class StageExecutor:
                             stream=st)
         elif k == "linear":
             g_id = self.fwd_gelu_of.get(n.id) if phase == "fwd" else None
+            a_id = self.fwd_add_of.get(n.id) if phase == "fwd" else None
             if g_id is not None:  # out = f (pre-activation), gelu node's buffer = gelu(f)
                 K.linear_fwd(inp[0], W("weight"), self.buf(out_tid(g_id), slot, phase),
                              bias=W("bias"), gelu=True, aux=out, stream=st)
+            elif a_id is not None:  # add node's buffer = x W^T + b + residual
+                a = self.node_by_id[a_id]
+                K.linear_fwd(inp[0], W("weight"), self.buf(out_tid(a_id), slot, phase),
+                             bias=W("bias"), residual=self.buf(out_tid(a.inputs[1]), slot, phase),
+                             stream=st)
             else:
                 K.linear_fwd(inp[0], W("weight"), out, bias=W("bias"), stream=st)
         elif k == "linear_res":
@@ -438,7 +465,8 @@ class StageExecutor:
             if not (phase == "fwd" and n.inputs[0] in self.fwd_gelu_of):
                 K.gelu_fwd(inp[0], out, stream=st)
         elif k == "add":
-            K.add(inp[0], inp[1], out, stream=st)
+            if not (phase == "fwd" and n.inputs[0] in self.fwd_add_of):
+                K.add(inp[0], inp[1], out, stream=st)
         elif k == "score":
             self._scores(inp[0], out)
             K.softmax_fwd(out, out, cfg.seq, 1.0 / math.sqrt(cfg.head_dim), cfg.causal, stream=st)
@@ -481,15 +509,13 @@ class StageExecutor:
         """Gradient buffer for tensor tid (allocated on first use)."""
         if tid not in self.grads:
             shape, dt = self._spec(tid)
-            with torch.cuda.stream(self.stream):
-                self.grads[tid] = torch.empty(shape, dtype=BF16, device=self.device)
+            self.grads[tid] = torch.empty(shape, dtype=BF16, device=self.device)
         return self.grads[tid]
 
     def grad_like(self, tid: str) -> torch.Tensor:
         """A fresh bf16 buffer shaped like tensor tid (receive buffer for a grad)."""
         shape, _ = self._spec(tid)
-        with torch.cuda.stream(self.stream):
-            return torch.empty(shape, dtype=BF16, device=self.device)
+        return torch.empty(shape, dtype=BF16, device=self.device)
 
     def set_recv_grad(self, tid: str, t: torch.Tensor) -> None:
         self.grads[tid] = t

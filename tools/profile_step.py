@@ -14,6 +14,10 @@ pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, tra
 ids, lab = synthetic_batch(cfg, m, b); ids, lab = ids.cuda(), lab.cuda()
 for _ in range(2): pipe.step(ids, lab)
 torch.cuda.synchronize()
+st = pipe.streams[0]
+e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+e0.record(st); pipe.step(ids, lab); e1.record(st); torch.cuda.synchronize()
+print(f"event-timed step (no profiler): {e0.elapsed_time(e1):.1f} ms")
 from torch.profiler import profile, ProfilerActivity
 import time
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
