@@ -93,9 +93,9 @@ int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float
 /* ln1 / ln2 / lnf: y = (x - mean) * rstd * gamma + beta; mean/rstd saved (f32 [rows]). */
 int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,
                       float* rstd, int64_t rows, int64_t cols, float eps, void* stream);
-/* dx = LN'(dy) (+ dx_add if non-NULL, may alias dx); dgamma/dbeta += (f32).
- * workspace: f32 scratch of >= min(ceil(rows/8), 296) * 2 * cols floats (per-CTA
- * partials, reduced without atomics); owned by the caller, stream-ordered. */
+/* dx = LN'(dy) (+ dx_add if non-NULL, may alias dx); dgamma/dbeta += (f32), both
+ * NULL to skip the parameter gradients.  workspace: unused since ABI 1.1 (pass
+ * NULL / 0); kept so the signature is stable. */
 int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamma, const float* mean,
                       const float* rstd, void* dx, const void* dx_add, float* dgamma, float* dbeta,
                       int64_t rows, int64_t cols, float* workspace, int64_t workspace_floats,
@@ -110,8 +110,8 @@ int dpn_gelu_fwd(const void* x, void* y, int64_t n, void* stream);
 int dpn_gelu_bwd(const void* dy, const void* x, void* dx, int64_t n, void* stream);
 int dpn_add(const void* a, const void* b, void* out, int64_t n, void* stream);
 int dpn_cast_f32_bf16(const float* x, void* y, int64_t n, void* stream);
-/* out[c] += sum_r x[r, c]   (bias gradients); workspace as for layernorm_bwd:
- * >= min(ceil(296 / ceil(cols/2048)), ceil(rows/8)) * cols floats. */
+/* out[c] += sum_r x[r, c]   (bias gradients; single pass, vector atomics).
+ * workspace: unused since ABI 1.1 (pass NULL / 0). */
 int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld, float* out, float* workspace,
                int64_t workspace_floats, void* stream);
 /* head: *loss_sum += loss_scale * sum_r CE(logits[r, :vocab], labels[r]);

@@ -590,22 +590,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 // D[b, h, q] = sum_c dO[row, h*64 + c] * O[row, h*64 + c]; one warp per (row, head)
-__global__ void attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
+// D[b,h,q] = rowsum(dO * O) over the head's 64 columns; also zeroes the fp32
+// dQ accumulator (replaces a separate memset).  8 threads per (row, head), one
+// 16-byte chunk of O and dO each.
+__global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16* __restrict__ o,
                                      const __nv_bfloat16* __restrict__ dout, float* __restrict__ D,
-                                     long long rows, int seq, int heads) {
+                                     float* __restrict__ dq, long long rows, int seq, int heads) {
   pdl_wait();
-  const int lane = threadIdx.x & 31;
-  const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= rows * heads) return;
-  const long long row = w / heads;
-  const int h = (int)(w % heads);
-  const long long base = row * heads * kD + h * kD + lane * 2;
-  const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(o + base));
-  const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(dout + base));
-  const float s = warp_sum(a.x * b.x + a.y * b.y);
-  if (lane == 0) {
-    const long long bb = row / seq, q = row % seq;
-    D[(bb * heads + h) * seq + q] = s;
+  const long long total = rows * heads * 8;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    // total is a multiple of 8 and so is the grid stride: all 8 lanes of a
+    // group stay in the loop together
+    const long long e = i * 8;  // element offset in [rows, heads*64]
+    const uint4 ou = *reinterpret_cast<const uint4*>(o + e);
+    const uint4 du = *reinterpret_cast<const uint4*>(dout + e);
+    const __nv_bfloat162* oh = reinterpret_cast<const __nv_bfloat162*>(&ou);
+    const __nv_bfloat162* dh = reinterpret_cast<const __nv_bfloat162*>(&du);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(oh[k]), b = __bfloat1622float2(dh[k]);
+      acc += a.x * b.x + a.y * b.y;
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    reinterpret_cast<float4*>(dq + e)[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+    reinterpret_cast<float4*>(dq + e)[1] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((threadIdx.x & 7) == 0) {
+      const long long rh = i >> 3, row = rh / heads, bb = row / seq, q = row % seq;
+      const int h = (int)(rh % heads);
+      D[(bb * heads + h) * seq + q] = acc;
+    }
   }
 }
 
@@ -676,11 +693,13 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
   cudaStream_t st = (cudaStream_t)stream;
   float* dq = workspace;
   float* D = workspace + rows * H;
-  DPN_CHECK_CUDA(cudaMemsetAsync(dq, 0, sizeof(float) * rows * H, st));
-  const long long warps = rows * heads;
-  DPN_CHECK_CUDA(launch_pdl(attn_bwd_prep_kernel, (unsigned)((warps + 7) / 8), 256, 0, st, 
-      (const __nv_bfloat16*)out, (const __nv_bfloat16*)dout, D, rows, (int)seq, (int)heads));
-  DPN_LAUNCH_CHECK();
+  {
+    const long long threads = rows * heads * 8;
+    const unsigned g = (unsigned)std::min<long long>((threads + 255) / 256, 148 * 8);
+    DPN_CHECK_CUDA(launch_pdl(attn_bwd_prep_kernel, g, 256, 0, st, (const __nv_bfloat16*)out,
+                              (const __nv_bfloat16*)dout, D, dq, rows, (int)seq, (int)heads));
+    DPN_LAUNCH_CHECK();
+  }
   CUtensorMap tq, td;
   int rc = map_2d(&tq, qkv, rows, 3 * H);
   if (rc) return rc;

@@ -1,11 +1,11 @@
 // HBM-bound kernels of the stage executor (sm_100a).  All are single-pass,
 // 16-byte vectorised, warp-shuffle reduced; fp32 statistics, bf16 storage.
 //
-//   layernorm fwd/bwd   ln1 / ln2 / lnf nodes        warp per row
+//   layernorm fwd/bwd   ln1 / ln2 / lnf nodes        warp per row (+ colred for dgamma/dbeta)
 //   softmax fwd/bwd     score node (scaled, causal)   warp per row
 //   gelu fwd/bwd        gelu node                     grid-stride, 8 elem/thread
 //   add                 add node (residual)           grid-stride
-//   colsum              bias gradients                column tiles + atomics
+//   colsum (colred)     bias gradients                column tiles, 4 rows in flight, vector reds
 //   xent                head node loss + dlogits      CTA per row, row cached in smem
 //   embed fwd/bwd       embed node                    warp per token
 //   adamw               optimizer over a stage's flat parameter buffer
@@ -106,49 +106,46 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
 }
 
 // dx = rstd * (dyg - mean(dyg) - xhat * mean(dyg * xhat)) [+ dx_add], dyg = dy * gamma.
-// Two passes over the row (the second hits L1): the row is not kept in
-// registers, so two CTAs fit per SM.  dgamma / dbeta partials live in
-// registers per lane, are combined across the CTA's warps in shared memory
-// (one slot per warp, no atomics) and written as this CTA's partial row.
+// One warp per row; the row of x and dy stays in registers as packed bf16 (no
+// second read), so many warps per SM keep enough loads in flight for HBM.
+// dgamma / dbeta come from colred_kernel<1> (a column reduction, below).
 template <int NV>
-__global__ void __launch_bounds__(256, 2) ln_bwd_kernel(
+__global__ void __launch_bounds__(256) ln_dx_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
-    float* __restrict__ partial, long long rows, int cols) {
+    long long rows, int cols) {
   pdl_wait();
-  extern __shared__ float red[];  // [warps][2][cols]
   const int warps = blockDim.x >> 5;
-  const int wid = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
-  float pg[NV][8], pb[NV][8];
-#pragma unroll
-  for (int j = 0; j < NV; ++j)
-#pragma unroll
-    for (int i = 0; i < 8; ++i) pg[j][i] = pb[j][i] = 0.f;
-  for (long long r = (long long)blockIdx.x * warps + wid; r < rows;
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
        r += (long long)gridDim.x * warps) {
     const float mu = mean[r], rs = rstd[r];
-    const __nv_bfloat16* xr = x + r * cols;
-    const __nv_bfloat16* dr = dy + r * cols;
+    uint4 xr[NV], dr[NV], ar[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        xr[j] = *reinterpret_cast<const uint4*>(x + r * cols + c * 8);
+        dr[j] = *reinterpret_cast<const uint4*>(dy + r * cols + c * 8);
+        if (dx_add) ar[j] = *reinterpret_cast<const uint4*>(dx_add + r * cols + c * 8);
+      }
+    }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
         float xv[8], dv[8], gm[8];
-        load8(xr + c * 8, xv);
-        load8(dr + c * 8, dv);
+        load8(reinterpret_cast<const __nv_bfloat16*>(&xr[j]), xv);
+        load8(reinterpret_cast<const __nv_bfloat16*>(&dr[j]), dv);
         load8(gamma + c * 8, gm);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float xh = (xv[i] - mu) * rs;
           const float g = dv[i] * gm[i];
           s1 += g;
-          s2 += g * xh;
-          pg[j][i] += dv[i] * xh;
-          pb[j][i] += dv[i];
+          s2 += g * (xv[i] - mu) * rs;
         }
       }
     }
@@ -159,14 +156,14 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_kernel(
       const int c = lane + 32 * j;
       if (c < nvec) {
         float xv[8], dv[8], gm[8], o[8];
-        load8(xr + c * 8, xv);
-        load8(dr + c * 8, dv);
+        load8(reinterpret_cast<const __nv_bfloat16*>(&xr[j]), xv);
+        load8(reinterpret_cast<const __nv_bfloat16*>(&dr[j]), dv);
         load8(gamma + c * 8, gm);
 #pragma unroll
         for (int i = 0; i < 8; ++i) o[i] = rs * (dv[i] * gm[i] - s1 - (xv[i] - mu) * rs * s2);
         if (dx_add) {
           float a[8];
-          load8(dx_add + r * cols + c * 8, a);
+          load8(reinterpret_cast<const __nv_bfloat16*>(&ar[j]), a);
 #pragma unroll
           for (int i = 0; i < 8; ++i) o[i] += a[i];
         }
@@ -174,52 +171,118 @@ __global__ void __launch_bounds__(256, 2) ln_bwd_kernel(
       }
     }
   }
-  float* mine = red + (long long)wid * 2 * cols;
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, const float* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v[0]), "f"(v[1]),
+               "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+
+// Column reductions over a row-major [rows, cols] bf16 matrix (bias and
+// LayerNorm parameter gradients).  CTA (band, group) owns 8*cw columns and a
+// band of rows; its 512 threads are cw column chunks x L row lanes, each lane
+// keeping 4 rows (16 B each) in flight.  Lanes combine in shared memory and
+// the CTA adds its partial with one vector red per 4 columns.
+//   MODE 0: out0 += sum_r a[r]
+//   MODE 1: out0 += sum_r a[r] * (x[r] - mean[r]) * rstd[r],  out1 += sum_r a[r]
+constexpr int kColThreads = 512;
+constexpr int kColUnroll = 4;
+template <int MODE>
+__global__ void __launch_bounds__(kColThreads) colred_kernel(
+    const __nv_bfloat16* __restrict__ a, long long lda, const __nv_bfloat16* __restrict__ x,
+    const float* __restrict__ mean, const float* __restrict__ rstd, long long rows, int cols,
+    long long rows_per_cta, float* __restrict__ out0, float* __restrict__ out1) {
+  pdl_wait();
+  __shared__ float part[kColThreads * 8];
+  const int nvec = cols >> 3;
+  const int cw = min(nvec, 128);
+  const int L = kColThreads / cw;
+  const int ci = threadIdx.x % cw, lr = threadIdx.x / cw;
+  const int chunk = blockIdx.y * cw + ci;
+  const bool active = lr < L && chunk < nvec;
+  float acc0[8] = {0, 0, 0, 0, 0, 0, 0, 0}, acc1[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  if (active) {
+    for (long long r = r0 + lr; r < r1; r += kColUnroll * L) {
+      uint4 av[kColUnroll], xv[kColUnroll];
+      float mu[kColUnroll], rs[kColUnroll];
 #pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int c = lane + 32 * j;
-    if (c < nvec) {
+      for (int u = 0; u < kColUnroll; ++u) {
+        const long long rr = r + (long long)u * L;
+        if (rr < r1) {
+          av[u] = *reinterpret_cast<const uint4*>(a + rr * lda + chunk * 8);
+          if (MODE == 1) {
+            xv[u] = *reinterpret_cast<const uint4*>(x + rr * cols + chunk * 8);
+            mu[u] = mean[rr];
+            rs[u] = rstd[rr];
+          }
+        } else {
+          av[u] = make_uint4(0, 0, 0, 0);
+          if (MODE == 1) {
+            xv[u] = make_uint4(0, 0, 0, 0);
+            mu[u] = 0.f;
+            rs[u] = 0.f;
+          }
+        }
+      }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        mine[c * 8 + i] = pg[j][i];
-        mine[cols + c * 8 + i] = pb[j][i];
+      for (int u = 0; u < kColUnroll; ++u) {
+        float v[8];
+        load8(reinterpret_cast<const __nv_bfloat16*>(&av[u]), v);
+        if (MODE == 1) {
+          float xf[8];
+          load8(reinterpret_cast<const __nv_bfloat16*>(&xv[u]), xf);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            acc0[k] += v[k] * (xf[k] - mu[u]) * rs[u];
+            acc1[k] += v[k];
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc0[k] += v[k];
+        }
       }
     }
   }
-  __syncthreads();
-  float* dst = partial + (long long)blockIdx.x * 2 * cols;
-  for (int i = threadIdx.x; i < 2 * cols; i += blockDim.x) {
-    float t = 0.f;
-    for (int w = 0; w < warps; ++w) t += red[(long long)w * 2 * cols + i];
-    dst[i] = t;
+#pragma unroll
+  for (int pass = 0; pass < (MODE == 1 ? 2 : 1); ++pass) {
+    float* acc = pass == 0 ? acc0 : acc1;
+    float* out = pass == 0 ? out0 : out1;
+    if (pass) __syncthreads();
+    if (L > 1) {
+      if (lr < L) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) part[threadIdx.x * 8 + k] = acc[k];
+      }
+      __syncthreads();
+      if (lr == 0 && chunk < nvec) {
+        for (int q = 1; q < L; ++q)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] += part[(q * cw + ci) * 8 + k];
+      }
+    }
+    if (lr == 0 && chunk < nvec) {
+      red_add_v4(out + chunk * 8, acc);
+      red_add_v4(out + chunk * 8 + 4, acc + 4);
+    }
   }
 }
 
-// out[c] += sum_b partial[b][c] over `nrows` partial rows of width `width`
-// (phase 2 of the atomic-free column reductions).  A CTA owns 32 columns; its
-// 32 warps stride over the partial rows (coalesced 128-byte row segments) and
-// combine through shared memory.
-__global__ void __launch_bounds__(1024) reduce_rows_kernel(const float* __restrict__ partial,
-                                                           int nrows, int width,
-                                                           float* __restrict__ out0,
-                                                           float* __restrict__ out1, int split) {
-  pdl_wait();
-  __shared__ float acc_s[32][33];
-  const int lane = threadIdx.x & 31, wy = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;
-  float acc = 0.f;
-  if (c < width) {
-    for (int b = wy; b < nrows; b += 32) acc += partial[(long long)b * width + c];
-  }
-  acc_s[wy][lane] = acc;
-  __syncthreads();
-  if (wy == 0 && c < width) {
-    float t = 0.f;
-#pragma unroll
-    for (int q = 0; q < 32; ++q) t += acc_s[q][lane];
-    if (c < split) out0[c] += t;
-    else out1[c - split] += t;
-  }
+// grid for colred_kernel: column groups x row bands, ~2 CTAs per SM in total,
+// but at least `min_rows` rows per band so the atomics stay a small fraction
+// of the bytes read.
+dim3 colred_grid(long long rows, long long cols, long long* rows_per_cta) {
+  const long long nvec = cols / 8;
+  const long long cw = std::min<long long>(nvec, 128);
+  const long long gy = (nvec + cw - 1) / cw;
+  const long long min_rows = 32;
+  long long bands = std::max<long long>(1, std::min<long long>((296 + gy - 1) / gy,
+                                                               (rows + min_rows - 1) / min_rows));
+  const long long per = (rows + bands - 1) / bands;
+  *rows_per_cta = per;
+  return dim3((unsigned)((rows + per - 1) / per), (unsigned)gy);
 }
 
 // ---------------- softmax over attention scores ----------------
@@ -365,52 +428,6 @@ __global__ void cast_kernel(const float* __restrict__ x, __nv_bfloat16* __restri
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] = __float2bfloat16(x[i]);
-}
-
-// column sums of a bf16 [rows, cols] matrix (bias gradients).  A CTA owns up to
-// 256 16-byte column chunks and a band of rows; when the matrix is narrower
-// than 2048 columns several row lanes share a chunk.  Partials are reduced in
-// shared memory and written as this CTA's partial row; a second pass sums the
-// partial rows into the output (no contended atomics).
-__global__ void __launch_bounds__(256) colsum_kernel(const __nv_bfloat16* __restrict__ x,
-                                                     long long rows, int cols, long long ld,
-                                                     long long rows_per_cta,
-                                                     float* __restrict__ out) {
-  pdl_wait();
-  __shared__ float part[256 * 8];
-  const int nvec = cols >> 3;
-  const int cw = min(nvec, 256);       // chunks per CTA
-  const int L = blockDim.x / cw;       // row lanes per chunk
-  const int ci = threadIdx.x % cw, lr = threadIdx.x / cw;
-  const int chunk = blockIdx.y * cw + ci;
-  const bool active = lr < L && chunk < nvec;
-  float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  const long long r0 = (long long)blockIdx.x * rows_per_cta;
-  const long long r1 = min(rows, r0 + rows_per_cta);
-  if (active) {
-    for (long long r = r0 + lr; r < r1; r += L) {
-      float v[8];
-      load8(x + r * ld + chunk * 8, v);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) acc[k] += v[k];
-    }
-  }
-  if (L > 1) {
-    if (lr < L) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) part[threadIdx.x * 8 + k] = acc[k];
-    }
-    __syncthreads();
-    if (lr == 0 && chunk < nvec) {
-      for (int q = 1; q < L; ++q)
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] += part[(q * cw + ci) * 8 + k];
-    }
-  }
-  if (lr == 0 && chunk < nvec) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) atomicAdd(&out[chunk * 8 + k], acc[k]);
-  }
 }
 
 // ---------------- fused vocabulary cross entropy ----------------
@@ -615,29 +632,21 @@ extern "C" int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamm
                                  void* stream) {
   DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
   if (rows == 0) return 0;
-  const int grid = (int)std::min<long long>((rows + 7) / 8, 148 * 2);
-  DPN_REQUIRE(workspace != nullptr && workspace_floats >= (long long)grid * 2 * cols,
-              "workspace must hold min(ceil(rows/8), 296) * 2 * cols floats");
-  static bool smem_set = false;
-  if (!smem_set) {
-    const int mx = 8 * 2 * 2048 * (int)sizeof(float);
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    smem_set = true;
-  }
-  LN_DISPATCH(ln_bwd_kernel, grid, 8 * 2 * cols * sizeof(float), (const __nv_bfloat16*)dy,
+  (void)workspace;
+  (void)workspace_floats;
+  LN_DISPATCH(ln_dx_kernel, grid_for(rows, 8), 0, (const __nv_bfloat16*)dy,
               (const __nv_bfloat16*)x, (const __nv_bfloat16*)gamma, mean, rstd, (__nv_bfloat16*)dx,
-              (const __nv_bfloat16*)dx_add, workspace, rows, (int)cols);
+              (const __nv_bfloat16*)dx_add, rows, (int)cols);
   DPN_LAUNCH_CHECK();
-  DPN_CHECK_CUDA(launch_pdl(reduce_rows_kernel, (unsigned)((2 * cols + 31) / 32), 1024, 0, (cudaStream_t)stream, 
-      workspace, grid, (int)(2 * cols), dgamma, dbeta, (int)cols));
-  DPN_LAUNCH_CHECK();
+  if (dgamma || dbeta) {
+    DPN_REQUIRE(dgamma && dbeta, "dgamma and dbeta go together");
+    long long per;
+    const dim3 g = colred_grid(rows, cols, &per);
+    DPN_CHECK_CUDA(launch_pdl(colred_kernel<1>, g, kColThreads, 0, (cudaStream_t)stream,
+                              (const __nv_bfloat16*)dy, (long long)cols, (const __nv_bfloat16*)x,
+                              mean, rstd, rows, (int)cols, per, dgamma, dbeta));
+    DPN_LAUNCH_CHECK();
+  }
   return 0;
 }
 
@@ -714,16 +723,12 @@ extern "C" int dpn_colsum(const void* x, int64_t rows, int64_t cols, int64_t ld,
   if (rows == 0) return 0;
   (void)workspace;
   (void)workspace_floats;
-  // single pass: <= 64 row bands per column group, one atomic per column per
-  // CTA (<= 64-way: cheaper than a second launch)
-  const long long nvec = cols / 8;
-  const int cw = (int)std::min<long long>(nvec, 256);
-  const int gy = (int)((nvec + cw - 1) / cw);
-  const long long bands = std::max<long long>(1, std::min<long long>(64, (rows + 31) / 32));
-  const long long per = (rows + bands - 1) / bands;
-  dim3 grid((unsigned)((rows + per - 1) / per), (unsigned)gy);
-  DPN_CHECK_CUDA(launch_pdl(colsum_kernel, grid, 256, 0, (cudaStream_t)stream, (const __nv_bfloat16*)x, rows, (int)cols, ld,
-                                                        per, out));
+  long long per;
+  const dim3 g = colred_grid(rows, cols, &per);
+  DPN_CHECK_CUDA(launch_pdl(colred_kernel<0>, g, kColThreads, 0, (cudaStream_t)stream,
+                            (const __nv_bfloat16*)x, (long long)ld, (const __nv_bfloat16*)nullptr,
+                            (const float*)nullptr, (const float*)nullptr, rows, (int)cols, per,
+                            out, (float*)nullptr));
   DPN_LAUNCH_CHECK();
   return 0;
 }

@@ -172,11 +172,10 @@ def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
 def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stream=None):
     rows, cols = x.shape
     INSTR.launches += 2
-    ws = _workspace(x.device, 296 * 2 * cols, stream)
     check(lib().dpn_layernorm_bwd(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(), mean.data_ptr(),
                                   rstd.data_ptr(), dx.data_ptr(), _p(dx_add), dgamma.data_ptr(),
-                                  dbeta.data_ptr(), rows, cols, ws.data_ptr(), ws.numel(),
-                                  _s(stream)), "dpn_layernorm_bwd")
+                                  dbeta.data_ptr(), rows, cols, None, 0, _s(stream)),
+          "dpn_layernorm_bwd")
 
 
 def softmax_fwd(s, p, q_len, alpha, causal, stream=None):
@@ -220,9 +219,8 @@ def cast_f32_bf16(x, y, stream=None):
 def colsum(x, out, stream=None):
     rows, cols = x.shape
     INSTR.launches += 1
-    ws = _workspace(x.device, 296 * cols, stream)
-    check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), ws.data_ptr(),
-                           ws.numel(), _s(stream)), "dpn_colsum")
+    check(lib().dpn_colsum(x.data_ptr(), rows, cols, x.stride(0), out.data_ptr(), None, 0,
+                           _s(stream)), "dpn_colsum")
 
 
 def xent(logits, labels, vocab, grad_scale, loss_sum, dlogits, loss_scale=1.0, stream=None):
