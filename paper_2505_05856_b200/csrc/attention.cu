@@ -5,16 +5,21 @@
 // touches HBM (the unfused `score` node writes b*heads*s^2 bf16 and reads it
 // back three times).
 //
-// Forward, one CTA per (batch, head, 128-query tile), 256 threads:
+// Forward, one CTA per (batch, head, 128-query tile), 384 threads:
 //   warp 0   TMA: Q once, then K_j / V_j tiles into a 3-deep ring
 //   warp 1   MMA issuer: S_j = Q K_j^T (M=128,N=128,K=64) into TMEM S[j%2];
 //            O_j = P_j V_j (M=128,N=64,K=128) into TMEM O[j%2]
 //   warp 2   TMEM allocator
-//   warps 4-7 softmax: thread t owns query row t; reads S_j (tcgen05.ld),
-//            masks (causal, key < seq), updates running max / sum, writes
-//            P_j = exp(S_j - m) as bf16 into smem, accumulates
-//            O = O * exp(m_old - m_new) + O_j in registers; finally writes
-//            O / l (bf16) and the log-sum-exp (fp32, for the backward).
+//   warps 4-11 softmax, two warps per query row: warp w reads TMEM lanes
+//            32*(w%4).. (its 32 rows) and column half (w-4)/4 -- 64 keys of S_j,
+//            32 columns of O_j.  The two halves exchange their row maxima
+//            through shared memory (one named barrier per warp pair), keep
+//            partial row sums, write their own 64-key swizzle atom of P_j =
+//            exp2(S_j*scale*log2e - m) (bf16), and accumulate their 32 output
+//            columns O = O * alpha + O_j in registers.  The running max is only
+//            raised when it grows by more than 2^8 (conditional rescaling), so
+//            alpha is 1 on most tiles.  Finally O / l (bf16) and the natural-log
+//            LSE (fp32, for the backward).
 // head_dim is 64 (one 128-byte swizzle row).
 #include "common.cuh"
 #include "../../include/dawnpiper.h"
@@ -29,7 +34,8 @@ constexpr int kD = 64;
 constexpr int kKVStages = 3;
 constexpr int kTileBytes = kTile * kD * 2;  // 16 KB (128 rows x 128 B)
 constexpr int kPBytes = kTile * kTile * 2;  // 32 KB (two 64-key swizzle atoms)
-constexpr int kFwdThreads = 256;
+constexpr int kFwdThreads = 384;
+constexpr float kRescaleLog2 = 8.f;  // raise the running max only past 2^8
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct AttnParams {
@@ -48,6 +54,17 @@ __device__ __forceinline__ uint32_t sw128(int row, int chunk) {
 
 __device__ __forceinline__ void fence_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// named barrier over the two warps (64 threads) that share a row quarter
+__device__ __forceinline__ void pair_sync(int quarter) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
 }
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
@@ -96,11 +113,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);  // one arrival per softmax warp
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_empty[i], 8);  // one arrival per softmax warp
+      mbar_init(&p_full[i], 8);
       mbar_init(&p_empty[i], 1);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_empty[i], 4);
+      mbar_init(&o_empty[i], 8);
     }
     fence_mbar_init();
   }
@@ -171,52 +188,69 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     issue_o(n_kv - 1);
   } else if (warp >= 4) {
     // ---------------- softmax / correction ----------------
-    const int r = (warp - 4) * 32 + lane;  // query row within the tile (== TMEM lane)
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int r = quarter * 32 + lane;  // query row within the tile (== TMEM lane)
     const int q = q0 + r;
-    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
-    float m = -INFINITY, l = 0.f;
-    float o[kD];
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float* xmax = reinterpret_cast<float*>(tmem_slot + 4);  // [2][128][2] row-max exchange
+    const float sl = p.scale_log2;
+    float ms = -INFINITY;  // running max, scaled log2 units
+    float l = 0.f;         // partial row sum over this half's keys
+    float o[kD / 2];
 #pragma unroll
-    for (int c = 0; c < kD; ++c) o[c] = 0.f;
-    float alpha_prev = 0.f;
+    for (int c = 0; c < kD / 2; ++c) o[c] = 0.f;
+    float alpha_prev = 1.f;
     for (int j = 0; j <= n_kv; ++j) {
       if (j < n_kv) {
         const int i = j & 1;
+        const int k0 = j * kTile + half * 64;
+        const bool mask = (j + 1) * kTile > p.seq || (p.causal && j == qt);
         mbar_wait(&s_full[i], (j >> 1) & 1);
         tc_fence_after();
-        float s[kTile];
-#pragma unroll
-        for (int c = 0; c < kTile / 32; ++c) {
+        float s[64];
+        {
           uint32_t u[32];
-          tmem_ld_32x32b_x32(tmem + i * 128 + c * 32 + lane_off, u);
+          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + lane_off, u);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) s[c * 32 + e] = __uint_as_float(u[e]);
+          for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(u[e]);
+          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, u);
+          tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) s[32 + e] = __uint_as_float(u[e]);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[i]);
-        const int k0 = j * kTile;
-        float mx = m;
+        if (mask) {
 #pragma unroll
-        for (int c = 0; c < kTile; ++c) {
-          const int key = k0 + c;
-          const bool ok = key < p.seq && (!p.causal || key <= q);
-          s[c] = ok ? s[c] * p.scale_log2 : -INFINITY;
-          mx = fmaxf(mx, s[c]);
+          for (int c = 0; c < 64; ++c) {
+            const int key = k0 + c;
+            if (!(key < p.seq && (!p.causal || key <= q))) s[c] = -INFINITY;
+          }
         }
-        const float alpha = (m == -INFINITY) ? 0.f : exp2f(m - mx);
-        const float base = (mx == -INFINITY) ? 0.f : mx;
-        float sum = 0.f;
-        // P_j into shared memory: 128-byte swizzled, two 64-key atoms
-        mbar_wait(&p_empty[i], ((j >> 1) & 1) ^ 1);
-        uint8_t* pt = sP + i * kPBytes;
+        float mx = s[0];
 #pragma unroll
-        for (int c = 0; c < kTile / 8; ++c) {
+        for (int c = 1; c < 64; ++c) mx = fmaxf(mx, s[c]);
+        float* xm = xmax + (j & 1) * 256 + r * 2;
+        xm[half] = mx;
+        pair_sync(quarter);
+        mx = fmaxf(xm[0], xm[1]) * sl;  // row max over all 128 keys (scaled)
+        float alpha = 1.f;
+        if (mx > ms + kRescaleLog2 || ms == -INFINITY) {
+          alpha = (ms == -INFINITY) ? 0.f : ex2(ms - mx);
+          ms = mx;
+        }
+        const float base = (ms == -INFINITY) ? 0.f : ms;
+        float sum = 0.f;
+        mbar_wait(&p_empty[i], ((j >> 1) & 1) ^ 1);
+        uint8_t* pt = sP + i * kPBytes + half * (kPBytes / 2);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
           float e8[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            e8[e] = exp2f(s[c * 8 + e] - base);
+            e8[e] = ex2(fmaf(s[c * 8 + e], sl, -base));
             sum += e8[e];
           }
           uint4 w;
@@ -224,10 +258,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.y = pack_bf16(e8[2], e8[3]);
           w.z = pack_bf16(e8[4], e8[5]);
           w.w = pack_bf16(e8[6], e8[7]);
-          *reinterpret_cast<uint4*>(pt + (c >> 3) * (kPBytes / 2) + sw128(r, c & 7)) = w;
+          *reinterpret_cast<uint4*>(pt + sw128(r, c)) = w;
         }
         l = l * alpha + sum;
-        m = mx;
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[i]);
@@ -236,39 +269,38 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           const int pi = (j - 1) & 1;
           mbar_wait(&o_full[pi], ((j - 1) >> 1) & 1);
           tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < kD / 32; ++c) {
-            uint32_t u[32];
-            tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + c * 32 + lane_off, u);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha_prev + __uint_as_float(u[e]);
-          }
+          uint32_t u[32];
+          tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + half * 32 + lane_off, u);
+          tmem_ld_wait();
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&o_empty[pi]);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(u[e]));
         }
         alpha_prev = alpha;
       } else {
         const int pi = (j - 1) & 1;
         mbar_wait(&o_full[pi], ((j - 1) >> 1) & 1);
         tc_fence_after();
+        uint32_t u[32];
+        tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + half * 32 + lane_off, u);
+        tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < kD / 32; ++c) {
-          uint32_t u[32];
-          tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + c * 32 + lane_off, u);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[c * 32 + e] = o[c * 32 + e] * alpha_prev + __uint_as_float(u[e]);
-        }
+        for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(u[e]));
         tc_fence_before();
       }
     }
+    // combine the two halves' row sums
+    float* xs = xmax + 512 + r * 2;
+    xs[half] = l;
+    pair_sync(quarter);
+    l = xs[0] + xs[1];
     if (q < p.seq) {
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD;
+      __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + half * 32;
 #pragma unroll
-      for (int c = 0; c < kD / 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint4 w;
         w.x = pack_bf16(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
         w.y = pack_bf16(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
@@ -277,7 +309,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         reinterpret_cast<uint4*>(op)[c] = w;
       }
       // natural-log LSE of scale * S:  (m + log2 l) / log2(e)
-      p.lse[((long long)bb * p.heads + h) * p.seq + q] = (m + log2f(l)) / kLog2e;
+      if (half == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (ms + log2f(l)) / kLog2e;
     }
   }
   tc_fence_before();
@@ -322,7 +354,7 @@ int map_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols) {
   return 0;
 }
 
-constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256;
+constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256 + 768 * 4;
 
 }  // namespace
 
@@ -338,7 +370,7 @@ constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes +
 // D_i = rowsum(dO_i * O_i) comes from attn_bwd_prep.
 namespace {
 
-constexpr int kBwdThreads = 256;
+constexpr int kBwdThreads = 384;
 
 struct AttnBwdParams {
   int seq, heads, H;
@@ -399,11 +431,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&q_empty[s], 1);
     }
     mbar_init(sp_full, 1);
-    mbar_init(sp_empty, 4);
-    mbar_init(ds_full, 4);
+    mbar_init(sp_empty, 8);
+    mbar_init(ds_full, 8);
     mbar_init(ds_empty, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 4);
+    mbar_init(dq_empty, 8);
     mbar_init(dkv_full, 1);
     fence_mbar_init();
   }
@@ -477,36 +509,44 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     if (lane == 0) umma_commit(dkv_full);
     __syncwarp();
   } else if (warp >= 4) {
-    const int r = (warp - 4) * 32 + lane;  // query row (S, dP, dQ) / key row (dV, dK)
-    const uint32_t lane_off = (uint32_t)((warp - 4) * 32) << 16;
+    // two warps per TMEM lane quarter: warp w owns rows 32*(w%4).. and column
+    // half (w-4)/4 (64 keys of S / dP, 32 columns of dQ / dV / dK)
+    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int r = quarter * 32 + lane;  // query row (S, dP, dQ) / key row (dV, dK)
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float lse_scale = 1.4426950408889634f;
+    const float sl = p.scale_log2, sc = p.scale;
     for (int i = i0, it = 0; i < n_q; ++i, ++it) {
       const int q = i * kTile + r;
       const bool qok = q < p.seq;
       const long long sidx = ((long long)bb * p.heads + h) * p.seq + (qok ? q : 0);
       const float lse2 = qok ? p.lse[sidx] * lse_scale : 0.f;
-      const float Dq = qok ? p.D[sidx] : 0.f;
+      const float Dq = qok ? p.D[sidx] * sc : 0.f;
+      const bool mask = !qok || k0 + kTile > p.seq || (p.causal && i == kt);
       mbar_wait(sp_full, it & 1);
       mbar_wait(ds_empty, (it & 1) ^ 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int c = 0; c < kTile / 32; ++c) {
+      for (int c = 0; c < 2; ++c) {
+        const int col = half * 64 + c * 32;  // key offset within the tile
         uint32_t us[32], ud[32];
-        tmem_ld_32x32b_x32(tmem + c * 32 + lane_off, us);
-        tmem_ld_32x32b_x32(tmem + 128 + c * 32 + lane_off, ud);
+        tmem_ld_32x32b_x32(tmem + col + lane_off, us);
+        tmem_ld_32x32b_x32(tmem + 128 + col + lane_off, ud);
         tmem_ld_wait();
         float pv[32], dsv[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const int key = k0 + c * 32 + e;
-          const bool ok = qok && key < p.seq && (!p.causal || key <= q);
-          const float pr = ok ? exp2f(__uint_as_float(us[e]) * p.scale_log2 - lse2) : 0.f;
+          float pr = ex2(fmaf(__uint_as_float(us[e]), sl, -lse2));
+          if (mask) {
+            const int key = k0 + col + e;
+            if (!(qok && key < p.seq && (!p.causal || key <= q))) pr = 0.f;
+          }
           pv[e] = pr;
-          dsv[e] = pr * (__uint_as_float(ud[e]) - Dq) * p.scale;
+          dsv[e] = pr * fmaf(__uint_as_float(ud[e]), sc, -Dq);
         }
 #pragma unroll
         for (int w = 0; w < 4; ++w) {
-          const int cc = c * 4 + w;  // 16-byte chunk index over the 128 keys
+          const int cc = c * 4 + w;  // 16-byte chunk within this half's 64-key atom
           uint4 a, b2;
           a.x = pack_bf16(pv[w * 8 + 0], pv[w * 8 + 1]);
           a.y = pack_bf16(pv[w * 8 + 2], pv[w * 8 + 3]);
@@ -516,7 +556,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           b2.y = pack_bf16(dsv[w * 8 + 2], dsv[w * 8 + 3]);
           b2.z = pack_bf16(dsv[w * 8 + 4], dsv[w * 8 + 5]);
           b2.w = pack_bf16(dsv[w * 8 + 6], dsv[w * 8 + 7]);
-          const uint32_t off = (cc >> 3) * (kPBytes / 2) + sw128(r, cc & 7);
+          const uint32_t off = half * (kPBytes / 2) + sw128(r, cc);
           *reinterpret_cast<uint4*>(sP + off) = a;
           *reinterpret_cast<uint4*>(sdS + off) = b2;
         }
@@ -531,22 +571,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // dQ_i (this KV tile's contribution) -> f32 accumulator
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
-#pragma unroll
-      for (int c = 0; c < kD / 32; ++c) {
+      {
         uint32_t u[32];
-        tmem_ld_32x32b_x32(tmem + 384 + c * 32 + lane_off, u);
+        tmem_ld_32x32b_x32(tmem + 384 + half * 32 + lane_off, u);
         tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dq_empty);
         if (qok) {
-          float* dst = p.dq + (long long)(row0 + q) * p.H + h * kD + c * 32;
+          float* dst = p.dq + (long long)(row0 + q) * p.H + h * kD + half * 32;
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
             red_add_v4f(dst + e, __uint_as_float(u[e]), __uint_as_float(u[e + 1]),
                         __uint_as_float(u[e + 2]), __uint_as_float(u[e + 3]));
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(dq_empty);
     }
     // dV, dK of this key tile (TMEM lane = key row)
     mbar_wait(dkv_full, 0);
@@ -554,30 +593,27 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int key = k0 + r;
     const bool any = i0 < n_q;
     if (key < p.seq) {
-      __nv_bfloat16* dk = p.dqkv + (long long)(row0 + key) * 3 * p.H + p.H + h * kD;
-      __nv_bfloat16* dv = p.dqkv + (long long)(row0 + key) * 3 * p.H + 2 * p.H + h * kD;
+      __nv_bfloat16* dk = p.dqkv + (long long)(row0 + key) * 3 * p.H + p.H + h * kD + half * 32;
+      __nv_bfloat16* dv = p.dqkv + (long long)(row0 + key) * 3 * p.H + 2 * p.H + h * kD + half * 32;
+      uint32_t uv[32], uk[32];
+      tmem_ld_32x32b_x32(tmem + 256 + half * 32 + lane_off, uv);
+      tmem_ld_32x32b_x32(tmem + 320 + half * 32 + lane_off, uk);
+      tmem_ld_wait();
 #pragma unroll
-      for (int c = 0; c < kD / 32; ++c) {
-        uint32_t uv[32], uk[32];
-        tmem_ld_32x32b_x32(tmem + 256 + c * 32 + lane_off, uv);
-        tmem_ld_32x32b_x32(tmem + 320 + c * 32 + lane_off, uk);
-        tmem_ld_wait();
+      for (int w = 0; w < 4; ++w) {
+        uint4 a, b2;
+        float fv[8], fk[8];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          uint4 a, b2;
-          float fv[8], fk[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            fv[e] = any ? __uint_as_float(uv[w * 8 + e]) : 0.f;
-            fk[e] = any ? __uint_as_float(uk[w * 8 + e]) : 0.f;
-          }
-          a.x = pack_bf16(fv[0], fv[1]); a.y = pack_bf16(fv[2], fv[3]);
-          a.z = pack_bf16(fv[4], fv[5]); a.w = pack_bf16(fv[6], fv[7]);
-          b2.x = pack_bf16(fk[0], fk[1]); b2.y = pack_bf16(fk[2], fk[3]);
-          b2.z = pack_bf16(fk[4], fk[5]); b2.w = pack_bf16(fk[6], fk[7]);
-          reinterpret_cast<uint4*>(dv + c * 32)[w] = a;
-          reinterpret_cast<uint4*>(dk + c * 32)[w] = b2;
+        for (int e = 0; e < 8; ++e) {
+          fv[e] = any ? __uint_as_float(uv[w * 8 + e]) : 0.f;
+          fk[e] = any ? __uint_as_float(uk[w * 8 + e]) : 0.f;
         }
+        a.x = pack_bf16(fv[0], fv[1]); a.y = pack_bf16(fv[2], fv[3]);
+        a.z = pack_bf16(fv[4], fv[5]); a.w = pack_bf16(fv[6], fv[7]);
+        b2.x = pack_bf16(fk[0], fk[1]); b2.y = pack_bf16(fk[2], fk[3]);
+        b2.z = pack_bf16(fk[4], fk[5]); b2.w = pack_bf16(fk[6], fk[7]);
+        reinterpret_cast<uint4*>(dv)[w] = a;
+        reinterpret_cast<uint4*>(dk)[w] = b2;
       }
     }
   }
