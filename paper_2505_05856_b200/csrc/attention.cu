@@ -25,6 +25,7 @@
 #include "../../include/dawnpiper.h"
 
 #include <mutex>
+#include <type_traits>
 
 namespace dpn {
 namespace {
@@ -354,6 +355,23 @@ int map_2d(CUtensorMap* map, const void* ptr, long long rows, long long cols) {
   return 0;
 }
 
+// 2-D map over the f32 dQ accumulator [rows, cols], box 32 columns x 128 rows
+// (128 bytes wide), SW128 -- the TMA reduce-add target of the backward.
+int map_2d_f32(CUtensorMap* map, const void* ptr, long long rows, long long cols) {
+  EncodeFn enc = encode2();
+  DPN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  DPN_REQUIRE((reinterpret_cast<uintptr_t>(ptr) & 15) == 0 && cols % 4 == 0, "16-byte alignment");
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(cols * 4)};
+  cuuint32_t box[2] = {32, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DPN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed");
+  return 0;
+}
+
 constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256 + 768 * 4;
 
 }  // namespace
@@ -363,14 +381,25 @@ constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes +
 // while the CTA walks the query tiles i (causal: i >= j):
 //   S = Q_i K_j^T, dP = dO_i V_j^T                  (TMEM, M = queries)
 //   P = exp(scale*S - lse), dS = scale * P * (dP - D_i)   (softmax warps ->
-//       bf16 in 128-byte swizzled smem, one thread per query row)
+//       bf16 in 128-byte swizzled smem, double-buffered)
 //   dV += P^T dO_i, dK += dS^T Q_i                   (TMEM accumulators, M = keys;
 //       P^T / dS^T are the same smem tiles read MN-major)
-//   dQ_i = dS K_j                                    (TMEM -> red.global.add.v4.f32)
+//   dQ_i = dS K_j                                    (TMEM -> swizzled f32 smem ->
+//       TMA reduce-add into the f32 dQ accumulator)
 // D_i = rowsum(dO_i * O_i) comes from attn_bwd_prep.
+//
+// 512 threads, four warpgroups with re-balanced registers (setmaxnreg):
+//   WG0  warp 0 TMA (K/V once, Q/dO double-buffered), warp 1 MMA issuer,
+//        warp 2 TMEM allocator                                    (56 regs)
+//   WG1-2 softmax: warp w owns rows 32*(w%4).. and key half (w-4)/4   (184 regs)
+//   WG3  dQ drain: TMEM dQ -> smem staging -> cp.reduce.async.bulk.tensor
+//        (.add), off the softmax critical path                    (88 regs)
+// MMA issue order per query tile: S/dP(i+1) as soon as the softmax holds
+// S/dP(i) in registers, then dV(i), dQ(i), dK(i).  dS is double-buffered in
+// smem, P single-buffered (stored last, after dV(i-1) released it).
 namespace {
 
-constexpr int kBwdThreads = 384;
+constexpr int kBwdThreads = 512;
 
 struct AttnBwdParams {
   int seq, heads, H;
@@ -380,17 +409,31 @@ struct AttnBwdParams {
   const float* D;    // [b, heads, s]
   float* dq;         // [b*s, H] f32 accumulator (zeroed)
   __nv_bfloat16* dqkv;  // [b*s, 3H]
+  long long* trace;     // debug: per-CTA clock64 stamps (nullptr = off)
 };
 
-__device__ __forceinline__ void red_add_v4f(float* addr, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
-               "f"(d)
-               : "memory");
+// debug timeline of one CTA role (dpn_attn_debug_trace): slot k of CTA c
+#define ATTN_STAMP(slot)                                                              \
+  do {                                                                                \
+    if (p.trace && lane == 0) {                                                       \
+      const long long c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
+      p.trace[c_ * 64 + (slot)] = clock64();                                          \
+    }                                                                                 \
+  } while (0)
+
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
-                    const __grid_constant__ CUtensorMap tm_do, const AttnBwdParams p) {
+                    const __grid_constant__ CUtensorMap tm_do,
+                    const __grid_constant__ CUtensorMap tm_dq, const AttnBwdParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -399,18 +442,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sQ = sV + kTileBytes;          // [2]
   uint8_t* sdO = sQ + 2 * kTileBytes;     // [2]
   uint8_t* sP = sdO + 2 * kTileBytes;     // 32 KB
-  uint8_t* sdS = sP + kPBytes;            // 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdS + kPBytes);
+  uint8_t* sdS = sP + kPBytes;            // [2] 32 KB
+  uint8_t* sdQ = sdS + 2 * kPBytes;       // 32 KB f32 staging: two [128][32] SW128 boxes
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdQ + kPBytes);
   uint64_t* kv_full = bars;
   uint64_t* q_full = bars + 1;    // [2]
   uint64_t* q_empty = q_full + 2; // [2]
   uint64_t* sp_full = q_empty + 2;
-  uint64_t* sp_empty = sp_full + 1;
-  uint64_t* ds_full = sp_empty + 1;
-  uint64_t* ds_empty = ds_full + 1;
-  uint64_t* dq_full = ds_empty + 1;
-  uint64_t* dq_empty = dq_full + 1;
-  uint64_t* dkv_full = dq_empty + 1;
+  uint64_t* sp_loaded = sp_full + 1;
+  uint64_t* p_empty = sp_loaded + 1;
+  uint64_t* ds_full = p_empty + 1;  // [2]
+  uint64_t* ds_empty = ds_full + 2; // [2]
+  uint64_t* dq_full = ds_empty + 2;  // [2] (dQ is double-buffered in TMEM)
+  uint64_t* dq_empty = dq_full + 2;  // [2]
+  uint64_t* dkv_full = dq_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,24 +463,29 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const int k0 = kt * kTile;
   const int n_q = (p.seq + kTile - 1) / kTile;
   const int i0 = p.causal ? kt : 0;
+  const int n_it = n_q - i0;
   const int row0 = bb * p.seq;
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_qkv);
     prefetch_tmap(&tm_do);
+    prefetch_tmap(&tm_dq);
   }
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
+    mbar_init(sp_loaded, 8);
+    mbar_init(p_empty, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
+      mbar_init(&ds_full[s], 8);
+      mbar_init(&ds_empty[s], 1);
     }
     mbar_init(sp_full, 1);
-    mbar_init(sp_empty, 8);
-    mbar_init(ds_full, 8);
-    mbar_init(ds_empty, 1);
-    mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 8);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&dq_full[s], 1);
+      mbar_init(&dq_empty[s], 4);
+    }
     mbar_init(dkv_full, 1);
     fence_mbar_init();
   }
@@ -445,153 +495,198 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
-  // TMEM columns: S 0..127, dP 128..255, dV 256..319, dK 320..383, dQ 384..447
+  if (p.trace && threadIdx.x == 0) {
+    const long long c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    uint64_t gt;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[c_ * 64 + 60] = (long long)gt;
+    p.trace[c_ * 64 + 62] = smid;
+    p.trace[c_ * 64 + 63] = clock64();
+  }
+  // TMEM columns: S 0..127, dP 128..255, dV 256..319, dK 320..383, dQ[2] 384..511
 
-  if (warp == 0) {
-    if (lane == 0) {
+  if (warp < 4) {
+    regs_dec<56>();
+    if (warp == 0 && lane == 0) {
       mbar_expect_tx(kv_full, 2 * kTileBytes);
       tma_load_2d(sK, &tm_qkv, kv_full, p.H + h * kD, row0 + k0);
       tma_load_2d(sV, &tm_qkv, kv_full, 2 * p.H + h * kD, row0 + k0);
-      for (int i = i0, it = 0; i < n_q; ++i, ++it) {
-        const int st = it & 1;
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, i = i0 + it;
         mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
         mbar_expect_tx(&q_full[st], 2 * kTileBytes);
         tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], h * kD, row0 + i * kTile);
         tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], h * kD, row0 + i * kTile);
       }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // S, dP
-    constexpr uint32_t id_kv = idesc_bf16(128, 64, 1, 1);   // dV, dK: A^T and B MN-major
-    constexpr uint32_t id_q = idesc_bf16(128, 64, 0, 1);    // dQ: dS K-major, K_j MN-major
-    mbar_wait(kv_full, 0);
-    for (int i = i0, it = 0; i < n_q; ++i, ++it) {
-      const int st = it & 1;
-      mbar_wait(&q_full[st], (it >> 1) & 1);
-      mbar_wait(sp_empty, (it & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
-      if (lane == 0) {
-        const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+    } else if (warp == 1) {
+      constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // S, dP
+      constexpr uint32_t id_kv = idesc_bf16(128, 64, 1, 1);   // dV, dK: A^T and B MN-major
+      constexpr uint32_t id_q = idesc_bf16(128, 64, 0, 1);    // dQ: dS K-major, K_j MN-major
+      auto issue_sdp = [&](int it) {
+        const int st = it & 1;
+        mbar_wait(&q_full[st], (it >> 1) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
+          const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          umma_bf16(tmem, smem_desc_sw128(qa + k * 32, 16, 1024), smem_desc_sw128(kb + k * 32, 16, 1024),
-                    id_s, k > 0 ? 1u : 0u);
-          umma_bf16(tmem + 128, smem_desc_sw128(doa + k * 32, 16, 1024),
-                    smem_desc_sw128(vb + k * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
-        }
-        umma_commit(sp_full);
-      }
-      __syncwarp();
-      mbar_wait(ds_full, it & 1);
-      mbar_wait(dq_empty, (it & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS), kb = smem_u32(sK);
+          for (int k = 0; k < kD / 16; ++k)
+            umma_bf16(tmem, smem_desc_sw128(qa + k * 32, 16, 1024),
+                      smem_desc_sw128(kb + k * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
 #pragma unroll
-        for (int k = 0; k < kTile / 16; ++k) {
-          // K = queries: MN-major A (keys contiguous, two 64-key atoms 16 KB apart)
-          const uint64_t a_p = smem_desc_sw128(pa + k * 2048, kPBytes / 2, 1024);
-          const uint64_t a_ds = smem_desc_sw128(dsa + k * 2048, kPBytes / 2, 1024);
-          const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
-          umma_bf16(tmem + 256, a_p, smem_desc_sw128(doa + k * 2048, kD * 128, 1024), id_kv, acc);
-          umma_bf16(tmem + 320, a_ds, smem_desc_sw128(qa + k * 2048, kD * 128, 1024), id_kv, acc);
-          // dQ: K = keys: dS K-major (two atoms), K_j MN-major
-          umma_bf16(tmem + 384, smem_desc_sw128(dsa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024),
-                    smem_desc_sw128(kb + k * 2048, kD * 128, 1024), id_q, k > 0 ? 1u : 0u);
+          for (int k = 0; k < kD / 16; ++k)
+            umma_bf16(tmem + 128, smem_desc_sw128(doa + k * 32, 16, 1024),
+                      smem_desc_sw128(vb + k * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
+          umma_commit(sp_full);
         }
-        umma_commit(dq_full);
-        umma_commit(ds_empty);
-        umma_commit(&q_empty[st]);
+        __syncwarp();
+      };
+      ATTN_STAMP(0);
+      mbar_wait(kv_full, 0);
+      ATTN_STAMP(1);
+      if (n_it > 0) issue_sdp(0);
+      for (int it = 0; it < n_it; ++it) {
+        const int st = it & 1, b = it & 1;
+        mbar_wait(sp_loaded, it & 1);  // softmax holds S/dP(it) in registers
+        if (it + 1 < n_it) issue_sdp(it + 1);
+        mbar_wait(&ds_full[b], (it >> 1) & 1);
+        ATTN_STAMP(44 + it * 4);
+        tc_fence_after();
+        const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS + b * kPBytes);
+        const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
+        const uint32_t kb = smem_u32(sK);
+        if (lane == 0) {
+          // dV += P^T dO (K = queries: P read MN-major, two 64-key atoms 16 KB apart)
+#pragma unroll
+          for (int k = 0; k < kTile / 16; ++k)
+            umma_bf16(tmem + 256, smem_desc_sw128(pa + k * 2048, kPBytes / 2, 1024),
+                      smem_desc_sw128(doa + k * 2048, kD * 128, 1024), id_kv,
+                      (it > 0 || k > 0) ? 1u : 0u);
+          umma_commit(p_empty);
+        }
+        __syncwarp();
+        mbar_wait(&dq_empty[b], ((it >> 1) & 1) ^ 1);
+        ATTN_STAMP(45 + it * 4);
+        tc_fence_after();
+        if (lane == 0) {
+          // dQ = dS K_j (K = keys: dS K-major, K_j MN-major)
+#pragma unroll
+          for (int k = 0; k < kTile / 16; ++k)
+            umma_bf16(tmem + 384 + b * 64,
+                      smem_desc_sw128(dsa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024),
+                      smem_desc_sw128(kb + k * 2048, kD * 128, 1024), id_q, k > 0 ? 1u : 0u);
+          umma_commit(&dq_full[b]);
+          // dK += dS^T Q
+#pragma unroll
+          for (int k = 0; k < kTile / 16; ++k)
+            umma_bf16(tmem + 320, smem_desc_sw128(dsa + k * 2048, kPBytes / 2, 1024),
+                      smem_desc_sw128(qa + k * 2048, kD * 128, 1024), id_kv,
+                      (it > 0 || k > 0) ? 1u : 0u);
+          umma_commit(&ds_empty[b]);
+          umma_commit(&q_empty[st]);
+        }
+        __syncwarp();
       }
+      if (lane == 0) umma_commit(dkv_full);
       __syncwarp();
     }
-    if (lane == 0) umma_commit(dkv_full);
-    __syncwarp();
-  } else if (warp >= 4) {
-    // two warps per TMEM lane quarter: warp w owns rows 32*(w%4).. and column
-    // half (w-4)/4 (64 keys of S / dP, 32 columns of dQ / dV / dK)
+  } else if (warp < 12) {
+    regs_inc<184>();
+    // two warps per TMEM lane quarter: warp w owns rows 32*(w%4).. and key
+    // half (w-4)/4 (64 keys of S / dP; 32 columns of dV / dK at the end)
     const int quarter = warp & 3, half = (warp - 4) >> 2;
-    const int r = quarter * 32 + lane;  // query row (S, dP, dQ) / key row (dV, dK)
+    const int r = quarter * 32 + lane;  // query row (S, dP) / key row (dV, dK)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float lse_scale = 1.4426950408889634f;
     const float sl = p.scale_log2, sc = p.scale;
-    for (int i = i0, it = 0; i < n_q; ++i, ++it) {
+    // per-row lse / D, loaded one query tile ahead (their latency is not hidden otherwise)
+    const float* lse_row = p.lse + ((long long)bb * p.heads + h) * p.seq;
+    const float* d_row = p.D + ((long long)bb * p.heads + h) * p.seq;
+    auto row_stats = [&](int it, float& l2, float& dq) {
+      const int qq = (i0 + it) * kTile + r;
+      const bool ok = it < n_it && qq < p.seq;
+      l2 = ok ? lse_row[qq] : 0.f;
+      dq = ok ? d_row[qq] : 0.f;
+    };
+    float lse_next, d_next;
+    row_stats(0, lse_next, d_next);
+    for (int it = 0; it < n_it; ++it) {
+      const int i = i0 + it;
       const int q = i * kTile + r;
       const bool qok = q < p.seq;
-      const long long sidx = ((long long)bb * p.heads + h) * p.seq + (qok ? q : 0);
-      const float lse2 = qok ? p.lse[sidx] * lse_scale : 0.f;
-      const float Dq = qok ? p.D[sidx] * sc : 0.f;
+      const float lse2 = lse_next * lse_scale;
+      const float Dq = d_next * sc;
+      row_stats(it + 1, lse_next, d_next);
       const bool mask = !qok || k0 + kTile > p.seq || (p.causal && i == kt);
+      const int pb = it & 1;
+      uint8_t* tdS = sdS + pb * kPBytes;
+      if (warp == 4) ATTN_STAMP(2 + it * 8);
       mbar_wait(sp_full, it & 1);
-      mbar_wait(ds_empty, (it & 1) ^ 1);
+      if (warp == 4) ATTN_STAMP(3 + it * 8);
       tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        const int col = half * 64 + c * 32;  // key offset within the tile
-        uint32_t us[32], ud[32];
-        tmem_ld_32x32b_x32(tmem + col + lane_off, us);
-        tmem_ld_32x32b_x32(tmem + 128 + col + lane_off, ud);
-        tmem_ld_wait();
-        float pv[32], dsv[32];
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          float pr = ex2(fmaf(__uint_as_float(us[e]), sl, -lse2));
-          if (mask) {
-            const int key = k0 + col + e;
-            if (!(qok && key < p.seq && (!p.causal || key <= q))) pr = 0.f;
-          }
-          pv[e] = pr;
-          dsv[e] = pr * fmaf(__uint_as_float(ud[e]), sc, -Dq);
-        }
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          const int cc = c * 4 + w;  // 16-byte chunk within this half's 64-key atom
-          uint4 a, b2;
-          a.x = pack_bf16(pv[w * 8 + 0], pv[w * 8 + 1]);
-          a.y = pack_bf16(pv[w * 8 + 2], pv[w * 8 + 3]);
-          a.z = pack_bf16(pv[w * 8 + 4], pv[w * 8 + 5]);
-          a.w = pack_bf16(pv[w * 8 + 6], pv[w * 8 + 7]);
-          b2.x = pack_bf16(dsv[w * 8 + 0], dsv[w * 8 + 1]);
-          b2.y = pack_bf16(dsv[w * 8 + 2], dsv[w * 8 + 3]);
-          b2.z = pack_bf16(dsv[w * 8 + 4], dsv[w * 8 + 5]);
-          b2.w = pack_bf16(dsv[w * 8 + 6], dsv[w * 8 + 7]);
-          const uint32_t off = half * (kPBytes / 2) + sw128(r, cc);
-          *reinterpret_cast<uint4*>(sP + off) = a;
-          *reinterpret_cast<uint4*>(sdS + off) = b2;
-        }
-      }
+      uint32_t us[64], ud[64];
+      tmem_ld_32x32b_x32(tmem + half * 64 + lane_off, us);
+      tmem_ld_32x32b_x32(tmem + half * 64 + 32 + lane_off, us + 32);
+      tmem_ld_32x32b_x32(tmem + 128 + half * 64 + lane_off, ud);
+      tmem_ld_32x32b_x32(tmem + 128 + half * 64 + 32 + lane_off, ud + 32);
+      tmem_ld_wait();
+      if (warp == 4) ATTN_STAMP(4 + it * 8);
       tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(sp_loaded);  // the MMA may overwrite S/dP now
+      mbar_wait(&ds_empty[pb], ((it >> 1) & 1) ^ 1);
+      if (warp == 4) ATTN_STAMP(5 + it * 8);
+      uint4 pk[8];  // P row chunk, packed bf16 (stored once dV(it-1) released sP)
+      // the key mask only exists on boundary tiles: two straight-line copies
+      auto tile = [&](auto masked) {
+        constexpr bool kMask = decltype(masked)::value;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this half's 64-key atom
+          float pv[8], dsv[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float pr = ex2(fmaf(__uint_as_float(us[c * 8 + e]), sl, -lse2));
+            if constexpr (kMask) {
+              const int key = k0 + half * 64 + c * 8 + e;
+              pr = (qok && key < p.seq && (!p.causal || key <= q)) ? pr : 0.f;
+            }
+            pv[e] = pr;
+            dsv[e] = pr * fmaf(__uint_as_float(ud[c * 8 + e]), sc, -Dq);
+          }
+          pk[c].x = pack_bf16(pv[0], pv[1]);
+          pk[c].y = pack_bf16(pv[2], pv[3]);
+          pk[c].z = pack_bf16(pv[4], pv[5]);
+          pk[c].w = pack_bf16(pv[6], pv[7]);
+          uint4 b2;
+          b2.x = pack_bf16(dsv[0], dsv[1]);
+          b2.y = pack_bf16(dsv[2], dsv[3]);
+          b2.z = pack_bf16(dsv[4], dsv[5]);
+          b2.w = pack_bf16(dsv[6], dsv[7]);
+          *reinterpret_cast<uint4*>(tdS + half * (kPBytes / 2) + sw128(r, c)) = b2;
+        }
+      };
+      if (mask) tile(std::true_type{});
+      else tile(std::false_type{});
+      if (warp == 4) ATTN_STAMP(6 + it * 8);
+      mbar_wait(p_empty, (it & 1) ^ 1);
+      if (warp == 4) ATTN_STAMP(7 + it * 8);
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<uint4*>(sP + half * (kPBytes / 2) + sw128(r, c)) = pk[c];
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(sp_empty);
-        mbar_arrive(ds_full);
-      }
-      // dQ_i (this KV tile's contribution) -> f32 accumulator
-      mbar_wait(dq_full, it & 1);
-      tc_fence_after();
-      {
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(tmem + 384 + half * 32 + lane_off, u);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(dq_empty);
-        if (qok) {
-          float* dst = p.dq + (long long)(row0 + q) * p.H + h * kD + half * 32;
-#pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            red_add_v4f(dst + e, __uint_as_float(u[e]), __uint_as_float(u[e + 1]),
-                        __uint_as_float(u[e + 2]), __uint_as_float(u[e + 3]));
-        }
-      }
+      if (warp == 4) ATTN_STAMP(8 + it * 8);
+      if (lane == 0) mbar_arrive(&ds_full[pb]);
     }
+    if (warp == 4) ATTN_STAMP(36);
     // dV, dK of this key tile (TMEM lane = key row)
     mbar_wait(dkv_full, 0);
+    if (warp == 4) ATTN_STAMP(37);
     tc_fence_after();
     const int key = k0 + r;
-    const bool any = i0 < n_q;
+    const bool any = n_it > 0;
     if (key < p.seq) {
       __nv_bfloat16* dk = p.dqkv + (long long)(row0 + key) * 3 * p.H + p.H + h * kD + half * 32;
       __nv_bfloat16* dv = p.dqkv + (long long)(row0 + key) * 3 * p.H + 2 * p.H + h * kD + half * 32;
@@ -616,9 +711,60 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         reinterpret_cast<uint4*>(dk)[w] = b2;
       }
     }
+  } else {
+    regs_dec<88>();
+    // dQ drain: warp w reads TMEM lanes 32*(w%4).. (its 32 query rows), all 64 columns
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const bool issuer = warp == 12 && lane == 0;
+    for (int it = 0; it < n_it; ++it) {
+      const int b = it & 1;
+      mbar_wait(&dq_full[b], (it >> 1) & 1);
+      tc_fence_after();
+      uint32_t u[64];
+      tmem_ld_32x32b_x32(tmem + 384 + b * 64 + lane_off, u);
+      tmem_ld_32x32b_x32(tmem + 384 + b * 64 + 32 + lane_off, u + 32);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dq_empty[b]);
+      // the previous reduce must have finished reading the staging tile
+      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync 6, 128;" ::: "memory");
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(sdQ + hh * (kPBytes / 2) + sw128(r, c)) =
+              make_uint4(u[hh * 32 + c * 4], u[hh * 32 + c * 4 + 1], u[hh * 32 + c * 4 + 2],
+                         u[hh * 32 + c * 4 + 3]);
+      fence_async_smem();
+      asm volatile("bar.sync 6, 128;" ::: "memory");
+      if (issuer) {
+        // rows past seq carry zero (P = dS = 0 there), rows past the tensor are clipped
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
+              " [%0, {%2, %3}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&tm_dq)),
+              "r"(smem_u32(sdQ + hh * (kPBytes / 2))), "r"(h * kD + hh * 32),
+              "r"(row0 + (i0 + it) * kTile)
+              : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
+  if (p.trace && threadIdx.x == 0) {
+    const long long c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+    uint64_t gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    p.trace[c_ * 64 + 61] = (long long)gt;
+    p.trace[c_ * 64 + 59] = clock64();
+  }
   if (warp == 2) {
     tc_fence_after();
     tmem_free<512>(tmem);
@@ -678,7 +824,7 @@ __global__ void attn_dq_store_kernel(const float* __restrict__ dq, __nv_bfloat16
   }
 }
 
-constexpr int kBwdSmem = 1024 + kTileBytes * 6 + 2 * kPBytes + 256;
+constexpr int kBwdSmem = 1024 + kTileBytes * 6 + 4 * kPBytes + 256;  // K V Q[2] dO[2] | P dS[2] dQ-staging
 
 }  // namespace
 }  // namespace dpn
@@ -717,6 +863,11 @@ extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batc
   return 0;
 }
 
+static long long* g_attn_trace = nullptr;
+// debug hook (not in the public header): per-CTA clock64 timeline of the
+// backward kernel into buf[cta * 64 + slot]; nullptr turns it off.
+extern "C" void dpn_attn_debug_trace(void* buf) { g_attn_trace = static_cast<long long*>(buf); }
+
 extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                             void* dqkv, float* workspace, int64_t workspace_floats, int64_t batch,
                             int64_t seq, int64_t heads, int64_t head_dim, float scale, int causal,
@@ -741,6 +892,9 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
   if (rc) return rc;
   rc = map_2d(&td, dout, rows, H);
   if (rc) return rc;
+  CUtensorMap tdq;
+  rc = map_2d_f32(&tdq, dq, rows, H);
+  if (rc) return rc;
   AttnBwdParams p{};
   p.seq = (int)seq;
   p.heads = (int)heads;
@@ -752,6 +906,7 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
   p.D = D;
   p.dq = dq;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  p.trace = g_attn_trace;
   static bool set = false;
   if (!set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -759,7 +914,7 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
     set = true;
   }
   dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
-  DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, td, p));
+  DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, td, tdq, p));
   DPN_LAUNCH_CHECK();
   DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel, (unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0, st, 
       dq, (__nv_bfloat16*)dqkv, rows, (int)H));
