@@ -19,6 +19,9 @@ numerics to; this restatement fixes the semantics instead:
   * weight stashing (PipeDream): a forward uses the stage's newest weights and
     its backward differentiates through that same version; every backward is
     followed by an AdamW step on the fp32 master weights;
+  * sync schedule (GPipe, simulate.py:169-208): all forwards, then backwards in
+    reverse micro-batch order with one weight version; gradients accumulate
+    and one AdamW step on their mean ends the iteration;
   * AdamW: torch.optim.AdamW semantics (decoupled weight decay, bias
     correction), applied to every parameter.
 
@@ -77,7 +80,8 @@ def _inputs(nid: str, layers: int, fused: bool = True) -> Tuple[str, ...]:
 
 
 class RefStage:
-    def __init__(self, dims: dict, init: Dict[str, torch.Tensor], nodes: Sequence[str], opt: dict):
+    def __init__(self, dims: dict, init: Dict[str, torch.Tensor], nodes: Sequence[str], opt: dict,
+                 sync_m: int = 0):
         self.d = dims
         self.nodes = list(nodes)
         self.params = {k: v.detach().clone().float() for k, v in init.items()
@@ -87,6 +91,8 @@ class RefStage:
         self.step = 0
         self.opt = opt
         self.inflight: Dict[int, tuple] = {}
+        self.sync_m = sync_m  # > 0: GPipe, accumulate over sync_m micro-batches
+        self.gacc = {k: torch.zeros_like(v) for k, v in self.params.items()}
 
     def _node(self, nid: str, env: Dict[str, torch.Tensor], W: Dict[str, torch.Tensor],
               ids, labels) -> torch.Tensor:
@@ -158,9 +164,20 @@ class RefStage:
             roots.append(env[k])
             grads.append(gk)
         torch.autograd.backward(roots, grads)
-        self._adamw({k: (v.grad if v.grad is not None else torch.zeros_like(v))
-                     for k, v in version.items()})
+        g = {k: (v.grad if v.grad is not None else torch.zeros_like(v)) for k, v in version.items()}
+        if self.sync_m:
+            for k, gk in g.items():
+                self.gacc[k] += gk
+        else:
+            self._adamw(g)
         return {k: leaves[k].grad.detach() for k in leaves if leaves[k].grad is not None}
+
+    def flush(self) -> None:
+        """GPipe: one AdamW step on the mean of the accumulated gradients."""
+        if self.sync_m:
+            self._adamw({k: v / self.sync_m for k, v in self.gacc.items()})
+            for v in self.gacc.values():
+                v.zero_()
 
     def _adamw(self, g: Dict[str, torch.Tensor]) -> None:
         o = self.opt
@@ -185,17 +202,22 @@ def boundary(stage_nodes: List[List[str]], x: int, layers: int, fused: bool = Tr
 
 def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor,
                     labels: torch.Tensor, stage_nodes: List[List[str]], opt: dict,
-                    steps: int = 1):
+                    steps: int = 1, schedule: str = "async_1f1b"):
     """Run `steps` iterations of m micro-batches (ids/labels: int [m, b*s]).
     Returns (losses [steps][m], final fp32 parameters)."""
     l, m = len(stage_nodes), ids.shape[0]
-    stages = [RefStage(dims, init, nodes, opt) for nodes in stage_nodes]
+    sync = schedule == "sync"
+    stages = [RefStage(dims, init, nodes, opt, sync_m=m if sync else 0) for nodes in stage_nodes]
     sends = [boundary(stage_nodes, x, dims["layers"], dims.get("fused_attention", True))
              for x in range(l)]
     all_losses = []
     for _ in range(steps):
         losses = [0.0] * m
-        ops = [one_f_one_b(l, m, x + 1) for x in range(l)]
+        if sync:
+            ops = [[("fwd", j) for j in range(1, m + 1)] + [("bwd", j) for j in range(m, 0, -1)]
+                   for _ in range(l)]
+        else:
+            ops = [one_f_one_b(l, m, x + 1) for x in range(l)]
         ptr = [0] * l
         acts: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
         grads: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
@@ -227,6 +249,8 @@ def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor
                     moved = True
             if not moved:
                 raise RuntimeError("oracle schedule deadlock")
+        for st in stages:
+            st.flush()
         all_losses.append(losses)
     final = {}
     for s in stages:

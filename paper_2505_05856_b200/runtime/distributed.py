@@ -29,7 +29,8 @@ from typing import Dict, List, Optional, Tuple
 import torch
 import torch.distributed as dist
 
-from ..planner.schedule import async_ops
+from ..planner.balance import SCHEDULE_ASYNC, SCHEDULE_SYNC
+from ..planner.schedule import async_ops, sync_ops
 
 
 class BoundaryChannels:
@@ -64,8 +65,11 @@ def _recv(ts: List[torch.Tensor], src: int, group) -> None:
 
 def run_stage_step(stage, chans: BoundaryChannels, rank: int, world: int, m: int,
                    ids: Optional[torch.Tensor] = None, labels: Optional[torch.Tensor] = None,
-                   loss: Optional[torch.Tensor] = None, on_op=None) -> None:
-    """Run stage rank+1's op list for one iteration of m micro-batches.
+                   loss: Optional[torch.Tensor] = None, on_op=None,
+                   schedule: str = SCHEDULE_ASYNC) -> None:
+    """Run stage rank+1's op list for one iteration of m micro-batches:
+    `async_ops` (1F1B) or, for the sync schedule, `sync_ops` (GPipe: all
+    forwards, backwards in reverse order, one `optimizer_step` at the end).
 
     `stage` provides recv_ids/send_ids, recv_buffer/send_buffer(tid, j),
     forward(j, ids, labels, loss_out), backward(j) -> {tid: grad},
@@ -75,7 +79,8 @@ def run_stage_step(stage, chans: BoundaryChannels, rank: int, world: int, m: int
     stream = getattr(stage, "stream", None)
     ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
     with ctx:
-        for kind, j, _ in async_ops(world, m, x):
+        ops = sync_ops(world, m, x) if schedule == SCHEDULE_SYNC else async_ops(world, m, x)
+        for kind, j, _ in ops:
             if on_op is not None:
                 on_op("start", kind, j)
             if kind == "fwd":
@@ -100,6 +105,8 @@ def run_stage_step(stage, chans: BoundaryChannels, rank: int, world: int, m: int
                 stage.finish_backward(j)
             if on_op is not None:
                 on_op("end", kind, j)
+        if schedule == SCHEDULE_SYNC:
+            stage.optimizer_step()
         for w, _ in pending:
             w.wait()
 

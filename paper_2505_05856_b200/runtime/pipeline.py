@@ -32,7 +32,7 @@ import torch
 
 from .. import kernels as K
 from .._lib import init_device
-from ..planner.balance import SCHEDULE_ASYNC
+from ..planner.balance import SCHEDULE_ASYNC, SCHEDULE_SYNC
 from ..planner.profile import ComputationGraph
 from ..planner.schedule import SimEvent, async_iteration, async_ops, inflight_depth
 from ..planner.search import PartitionPlan, stage_bounds
@@ -89,6 +89,15 @@ class RunReport:
         }
 
 
+def sync_order(stages: int, m: int) -> List[Tuple[int, str, int]]:
+    """GPipe issue order of simulate.py:169-208: every forward (micro-batch j
+    through stages 1..l), then every backward in reverse micro-batch order
+    (j = m..1 through stages l..1).  Per stage this is `sync_ops`."""
+    out = [(x, "fwd", j) for j in range(1, m + 1) for x in range(1, stages + 1)]
+    out += [(x, "bwd", j) for j in range(m, 0, -1) for x in range(stages, 0, -1)]
+    return out
+
+
 def colocated_order(stages: int, m: int) -> List[Tuple[int, str, int]]:
     """Interleave the stages' 1F1B op lists by dependency readiness, scanning
     stages in order exactly like simulate.py:244-282 (without durations).
@@ -125,8 +134,9 @@ class Pipeline:
 
     def __init__(self, model: TransformerConfig, g: ComputationGraph, plan: PartitionPlan,
                  cfg: RunConfig):
-        if plan.schedule != SCHEDULE_ASYNC:
-            raise ValueError("the B200 run implements the async 1F1B schedule")
+        if plan.schedule not in (SCHEDULE_ASYNC, SCHEDULE_SYNC):
+            raise ValueError(f"unknown schedule {plan.schedule!r}")
+        self.sync = plan.schedule == SCHEDULE_SYNC
         bounds = stage_bounds(plan.cuts, len(g))
         if len(g) != len(build_nodes(model)):
             raise ValueError("graph does not describe this model (node count mismatch)")
@@ -156,8 +166,9 @@ class Pipeline:
                 self.stages.append(StageExecutor(
                     cfg=model, g=g, nodes=nodes, lo=lo, hi=hi, stage=x, stages=self.l,
                     micro_batch=cfg.micro_batch_size, memopt=plan.memopt[x - 1], init=init,
-                    device=torch.device("cuda", d), stream=self.streams[d], opt=cfg.opt))
-        self.order = colocated_order(self.l, self.m)
+                    device=torch.device("cuda", d), stream=self.streams[d], opt=cfg.opt,
+                    schedule=plan.schedule, micro_batches=self.m))
+        self.order = sync_order(self.l, self.m) if self.sync else colocated_order(self.l, self.m)
         first_dev = self.stage_dev[0]
         self.loss = torch.zeros(self.m, dtype=torch.float32, device=torch.device("cuda", self.stage_dev[-1]))
         self.static_bytes = [self._stage_bytes(s) for s in self.stages]
@@ -258,6 +269,10 @@ class Pipeline:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(st)
                 events.append((x, j, kind, e0, e1))
+        if self.sync:  # GPipe: one update per stage after the last backward
+            for x, s in enumerate(self.stages):
+                with torch.cuda.stream(self.streams[self.stage_dev[x]]):
+                    s.optimizer_step()
         return self.loss
 
     def report(self, events: list, t_origin: torch.cuda.Event, losses: torch.Tensor,
@@ -273,7 +288,9 @@ class Pipeline:
             if kind == "bwd" and x == 1:
                 done[j] = b
         makespan = max(e.end for e in ev) if ev else 0
-        iteration = async_iteration(done, self.l, self.m, makespan)
+        # sync reports the whole iteration (simulate.py:143), async the
+        # steady-state time per micro-batch (simulate.py:326-336)
+        iteration = float(makespan) if self.sync else async_iteration(done, self.l, self.m, makespan)
         busy = [sum(e.end - e.start for e in ev if e.stage == x + 1) for x in range(self.l)]
         bubble = 1.0 - sum(busy) / (self.l * makespan) if makespan > 0 else 0.0
         peaks = list(self.static_bytes)
@@ -287,7 +304,7 @@ class Pipeline:
             waste_ratio=waste, trace=tuple(sorted(ev, key=lambda e: (e.start, e.end, e.stage, e.mb, e.kind))),
             makespan=makespan, capacity_exceeded=exceeded,
             losses=tuple(float(v) for v in losses.tolist()),
-            samples_per_s=(b * 1e6 / iteration) if iteration > 0 else 0.0,
+            samples_per_s=((b * (self.m if self.sync else 1)) * 1e6 / iteration) if iteration > 0 else 0.0,
             step_time_us=wall_us,
             device_peak_bytes=max(torch.cuda.max_memory_allocated(d) for d in set(self.stage_dev)))
 

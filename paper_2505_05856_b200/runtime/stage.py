@@ -36,6 +36,7 @@ from typing import Dict, List, Optional, Sequence, Set, Tuple
 import torch
 
 from .. import kernels as K
+from ..planner.balance import SCHEDULE_ASYNC, SCHEDULE_SYNC
 from ..planner.memplan import MemOptPlan, producer_chain
 from ..planner.profile import ComputationGraph
 from .graph import out_tid, stats_tid
@@ -150,7 +151,8 @@ class StageExecutor:
     def __init__(self, *, cfg: TransformerConfig, g: ComputationGraph, nodes: Sequence[NodeDef],
                  lo: int, hi: int, stage: int, stages: int, micro_batch: int, memopt: MemOptPlan,
                  init: Dict[str, torch.Tensor], device: torch.device, stream: torch.cuda.Stream,
-                 opt: AdamWConfig = AdamWConfig(), slots: Optional[int] = None):
+                 opt: AdamWConfig = AdamWConfig(), slots: Optional[int] = None,
+                 schedule: str = SCHEDULE_ASYNC, micro_batches: Optional[int] = None):
         self.cfg, self.g = cfg, g
         self.all_nodes = list(nodes)
         self.nodes = self.all_nodes[lo:hi + 1]
@@ -162,12 +164,29 @@ class StageExecutor:
         self.stream = stream
         self.copy_stream = torch.cuda.Stream(device=device)
         self.opt = opt
-        self.w = slots if slots is not None else stages - stage + 1
+        if schedule not in (SCHEDULE_ASYNC, SCHEDULE_SYNC):
+            raise ValueError(f"unknown schedule {schedule!r}")
+        # GPipe (sync, simulate.py:169-208): every micro-batch of the iteration is
+        # in flight before the first backward (schedule_weight = m,
+        # balance.py:65-77), one weight version, gradients accumulated over the
+        # m micro-batches and one AdamW step at the end of the iteration
+        self.sync = schedule == SCHEDULE_SYNC
+        if self.sync and micro_batches is None and slots is None:
+            raise ValueError("the sync schedule needs micro_batches")
+        self.m_sync = micro_batches if self.sync else 1
+        if slots is not None:
+            self.w = slots
+        else:
+            self.w = micro_batches if self.sync else stages - stage + 1
+        # dense weight gradients are written by the first backward of an
+        # iteration and accumulated by the rest (sync only)
+        self._wgrad_acc = False
+        self.grad_scale = 1.0 / (self.M * self.m_sync)  # mean over the iteration's tokens
         self.is_first = lo == 0
         self.is_last = hi == len(self.all_nodes) - 1
         self.node_by_id = {n.id: n for n in self.all_nodes}
         self.index = {n.id: i for i, n in enumerate(self.all_nodes)}
-        self.params = FlatParams(self.nodes, init, self.w, device)
+        self.params = FlatParams(self.nodes, init, 1 if self.sync else self.w, device)
 
         # ---- tensor bookkeeping -------------------------------------------------
         self.readers = backward_readers(self.all_nodes)
@@ -479,7 +498,8 @@ class StageExecutor:
             K.linear_fwd(inp[0], W("weight"), out, stream=st)
             # fused loss + dlogits; on a recompute replay the loss is discarded
             loss = (loss_out if loss_out is not None else self.loss) if phase == "fwd" else self._scratch_loss()
-            K.xent(out, self.labels[slot], cfg.vocab, 1.0 / M, loss, out, loss_scale=1.0 / M, stream=st)
+            K.xent(out, self.labels[slot], cfg.vocab, self.grad_scale, loss, out, loss_scale=1.0 / M,
+                   stream=st)
         else:
             raise ValueError(k)
 
@@ -539,7 +559,8 @@ class StageExecutor:
         ver = self.params.pinned(mb)
         with torch.cuda.stream(st):
             self._drop_leftovers()
-            self.params.zero_accum_grads(stream=st)
+            if not self._wgrad_acc:
+                self.params.zero_accum_grads(stream=st)
             # swap-ins in first-use order (backward runs right to left), kept
             # `swap_lookahead` tensors ahead of the node that needs them
             queue = sorted(self.swap_ids, key=lambda t: (-self.bwd_first.get(t, -1), t))
@@ -592,13 +613,30 @@ class StageExecutor:
 
     def finish_backward(self, mb: int) -> None:
         """Optimizer step after micro-batch mb's backward (PipeDream per-micro-batch
-        update); writes the next weight version into the retiring slot."""
-        dst = self.params.retire(mb)
-        with torch.cuda.stream(self.stream):
-            self.params.adamw(dst, self.opt, stream=self.stream)
+        update); writes the next weight version into the retiring slot.  Under the
+        sync schedule the gradients only accumulate; `optimizer_step` applies them."""
+        if self.sync:
+            self.params.version_of.pop(mb, None)
+            self.params.users[0].discard(mb)
+            self._wgrad_acc = True
+        else:
+            dst = self.params.retire(mb)
+            with torch.cuda.stream(self.stream):
+                self.params.adamw(dst, self.opt, stream=self.stream)
         self.grads = {}
         self.grad_init = set()
         self._skip_bwd = set()
+
+    def optimizer_step(self) -> None:
+        """Sync schedule: one AdamW step over the gradients accumulated by the
+        iteration's m backwards (already averaged by the loss-gradient scale)."""
+        if not self.sync:
+            return
+        if self.params.version_of:
+            raise RuntimeError("optimizer step with micro-batches still in flight")
+        with torch.cuda.stream(self.stream):
+            self.params.adamw(0, self.opt, stream=self.stream)
+        self._wgrad_acc = False
 
     def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
         # outputs of a replayed node land in a live buffer if evicted, else in
@@ -624,7 +662,7 @@ class StageExecutor:
             K.linear_dgrad(dlog, W("weight"), dx, accumulate_into=dx if dx_t in self.grad_init else None,
                            stream=st)
             self.grad_init.add(dx_t)
-            K.linear_wgrad(dlog, x, G("weight"), stream=st)
+            K.linear_wgrad(dlog, x, G("weight"), accumulate=self._wgrad_acc, stream=st)
             return
         if tid not in self.grad_init:
             return  # nothing flows into this node (cannot happen for a connected graph)
@@ -663,7 +701,7 @@ class StageExecutor:
                 dx = self.grad_buffer(x_t)
                 K.linear_dgrad(dy, W("weight"), dx, stream=st)
                 self.grad_init.add(x_t)
-            K.linear_wgrad(dy, x, G("weight"), stream=st)
+            K.linear_wgrad(dy, x, G("weight"), accumulate=self._wgrad_acc, stream=st)
             K.colsum(dy, G("bias"), stream=st)
             if k == "linear_res":
                 self._contribute_identity(out_tid(n.inputs[1]), dy)

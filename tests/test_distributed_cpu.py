@@ -58,6 +58,9 @@ class FakeStage:
     def finish_backward(self, j):
         self.grads = {}
 
+    def optimizer_step(self):
+        self.log.append(("opt", 0))
+
 
 def _free_port():
     s = socket.socket()
@@ -67,12 +70,12 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, m, q):
+def _worker(rank, world, port, m, q, schedule="async_1f1b"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2505_05856_b200.runtime.distributed import BoundaryChannels, run_stage_step
-    from paper_2505_05856_b200.planner.schedule import async_ops
+    from paper_2505_05856_b200.planner.schedule import async_ops, sync_ops
     chans = BoundaryChannels(world)
     st = FakeStage(rank, world)
     ids = torch.arange(m * 4, dtype=torch.int32).reshape(m, 4) if rank == 0 else None
@@ -83,20 +86,24 @@ def _worker(rank, world, port, m, q):
         grads_seen[len(grads_seen) + 1] = t.clone()
         _o(tid, t)
     st.set_recv_grad = spy
-    run_stage_step(st, chans, rank, world, m, ids=ids)
-    expect = [(k, j) for k, j, _ in async_ops(world, m, rank + 1)]
+    run_stage_step(st, chans, rank, world, m, ids=ids, schedule=schedule)
+    if schedule == "sync":
+        expect = [(k, j) for k, j, _ in sync_ops(world, m, rank + 1)] + [("opt", 0)]
+    else:
+        expect = [(k, j) for k, j, _ in async_ops(world, m, rank + 1)]
     q.put((rank, st.log == expect, {j: v.tolist() for j, v in st.results.items()},
            {k: v.tolist() for k, v in grads_seen.items()}))
     dist.barrier()
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m", [(2, 5), (3, 7)])
-def test_gloo_pipeline_order_and_matching(world, m):
+@pytest.mark.parametrize("world,m,schedule", [(2, 5, "async_1f1b"), (3, 7, "async_1f1b"),
+                                               (2, 4, "sync"), (3, 5, "sync")])
+def test_gloo_pipeline_order_and_matching(world, m, schedule):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, m, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, q, schedule)) for r in range(world)]
     for p in procs:
         p.start()
     out = {}
@@ -107,16 +114,17 @@ def test_gloo_pipeline_order_and_matching(world, m):
         p.join(timeout=60)
         assert p.exitcode == 0
     for r in range(world):
-        assert out[r][0], f"rank {r} did not run async_ops order"
+        assert out[r][0], f"rank {r} did not run the {schedule} op order"
     # last stage output of micro-batch j: ids[j] + 10 * (1 + 2 + ... + world)
     res = out[world - 1][1]
     shift = 10 * sum(range(1, world + 1))
     for j in range(1, m + 1):
         assert res[j] == [float((j - 1) * 4 + i + shift) for i in range(4)]
-    # gradients received by stage x (x < l), in backward order j = 1..m:
-    # seed j at the last stage, + x' added by every stage x' > x
+    # gradients received by stage x (x < l), in backward order (1F1B: j = 1..m,
+    # GPipe: j = m..1): seed j at the last stage, + x' added by every stage x' > x
     for r in range(world - 1):
         add = sum(range(r + 2, world + 1))
         grads = out[r][2]
-        for j in range(1, m + 1):
-            assert grads[j] == [float(j + add)] * 4
+        for k in range(1, m + 1):
+            j = m + 1 - k if schedule == "sync" else k
+            assert grads[k] == [float(j + add)] * 4

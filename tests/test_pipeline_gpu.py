@@ -16,15 +16,15 @@ pytestmark = pytest.mark.gpu
 REL = 2e-2
 
 
-def _setup(name, stages, cap_frac, bandwidth, b=2, m=6):
+def _setup(name, stages, cap_frac, bandwidth, b=2, m=6, schedule="async_1f1b"):
     from paper_2505_05856_b200 import planner as P
     from paper_2505_05856_b200.runtime.graph import profile_graph
     from paper_2505_05856_b200.runtime.model import PRESETS
     cfg = PRESETS[name]
     g = profile_graph(cfg, b)
     cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)
-    top = max(s.sched_peak for s in P.stage_profiles(g, cb, stages, P.SCHEDULE_ASYNC))
-    pc = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=int(cap_frac * top),
+    top = max(s.sched_peak for s in P.stage_profiles(g, cb, stages, schedule))
+    pc = P.PlanConfig(stages=stages, schedule=schedule, capacity=int(cap_frac * top),
                       bandwidth=bandwidth)
     return cfg, g, P.plan(g, pc)
 
@@ -56,7 +56,7 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
     ref_losses, ref_params = reference_train(
         dims, init, ids, labels, stage_nodes,
         dict(lr=opt.lr, beta1=opt.beta1, beta2=opt.beta2, eps=opt.eps, weight_decay=opt.weight_decay),
-        steps=steps)
+        steps=steps, schedule=plan.schedule)
     for gl, rl in zip(gpu_losses, ref_losses):
         for a, r in zip(gl, rl):
             assert abs(a - r) <= REL * abs(r), (gl, rl)
@@ -121,4 +121,19 @@ def test_pipeline_executes_memopt_actions(frac, bw):
     cfg, g, plan = _setup("tiny", 2, frac, bw)
     kinds = {a.kind for m in plan.memopt for a in m.actions}
     assert kinds, "expected memopt actions at this capacity"
+    _compare(cfg, g, plan)
+
+
+@pytest.mark.parametrize("name,stages", [("tiny", 1), ("tiny", 2), ("tiny-causal", 3)])
+def test_pipeline_sync_gpipe_matches_oracle(name, stages):
+    """GPipe (sync) schedule: all forwards, reverse-order backwards, gradients
+    accumulated over the m micro-batches and one AdamW step per iteration."""
+    cfg, g, plan = _setup(name, stages, 4.0, 16 << 30, schedule="sync")
+    assert plan.schedule == "sync"
+    _compare(cfg, g, plan)
+
+
+def test_pipeline_sync_with_memopt():
+    cfg, g, plan = _setup("tiny", 2, 0.6, 16 << 30, schedule="sync")
+    assert any(m.actions for m in plan.memopt)
     _compare(cfg, g, plan)
