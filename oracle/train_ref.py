@@ -14,6 +14,12 @@ numerics to; this restatement fixes the semantics instead:
         g = gelu_tanh(f); z = g W2^T + b2; out = z + y
     embed = tok[ids] + pos[t]; head = LN_f then logits = h Wh[:V]^T,
     loss = mean-over-tokens cross entropy per micro-batch;
+  * encoder-decoder (T5-large config): encoder blocks as above (non-causal) ->
+    E = enc_ln(x); decoder input dembed(tgt ids); decoder block = causal
+    self-attention sub-block, then c = lnx(y); q = c Wq^T + bq;
+    kv = E Wkv^T + bkv; ctx = softmax(q k^T / sqrt(d)) v; y2 = ctx Wo^T + bo + y;
+    then the FFN sub-block; lnf / head over the target tokens.  ids per
+    micro-batch are the b*s source ids followed by the b*t target ids;
   * schedule: per stage x of l, the 1F1B op list of simulate.py:211-222
     (restated below as `one_f_one_b`);
   * weight stashing (PipeDream): a forward uses the stage's newest weights and
@@ -60,23 +66,46 @@ def node_ids(layers: int, fused: bool = True) -> List[str]:
     return ids + ["lnf", "head"]
 
 
-def _inputs(nid: str, layers: int, fused: bool = True) -> Tuple[str, ...]:
-    if nid == "embed":
+def _inputs(nid: str, d: dict) -> Tuple[str, ...]:
+    layers, dec = d["layers"], d.get("dec_layers", 0)
+    fused = d.get("fused_attention", True)
+    if nid in ("embed", "dembed"):
         return ()
-    if nid == "lnf":
+    if nid == "enc_ln":
         return (f"b{layers - 1}.add",)
+    if nid == "lnf":
+        return (f"d{dec - 1}.add",) if dec else (f"b{layers - 1}.add",)
     if nid == "head":
         return ("lnf",)
     b, k = nid.split(".")
     blk = int(b[1:])
-    x = "embed" if blk == 0 else f"b{blk - 1}.add"
-    p = f"b{blk}."
+    if b[0] == "d":
+        x = "dembed" if blk == 0 else f"d{blk - 1}.add"
+    else:
+        x = "embed" if blk == 0 else f"b{blk - 1}.add"
+    p = f"{b[0]}{blk}."
+    y = p + "xproj" if b[0] == "d" else p + "proj"
     return {
         "ln1": (x,), "qkv": (p + "ln1",), "score": (p + "qkv",),
         "attn": (p + "qkv",) if fused else (p + "score", p + "qkv"),
-        "proj": (p + "attn", x), "ln2": (p + "proj",), "fc1": (p + "ln2",), "gelu": (p + "fc1",),
-        "fc2": (p + "gelu",), "add": (p + "fc2", p + "proj"),
+        "proj": (p + "attn", x), "lnx": (p + "proj",), "xattn": (p + "lnx", "enc_ln"),
+        "xproj": (p + "xattn", p + "proj"), "ln2": (y,), "fc1": (p + "ln2",),
+        "gelu": (p + "fc1",), "fc2": (p + "gelu",), "add": (p + "fc2", y),
     }[k]
+
+
+def _mha(q, k, v, b: int, A: int, causal: bool) -> torch.Tensor:
+    """Multi-head attention over [b*t, H] q and [b*s, H] k, v -> [b*t, H]."""
+    H = q.shape[1]
+    hd = H // A
+    t, s = q.shape[0] // b, k.shape[0] // b
+    qh = q.reshape(b, t, A, hd).transpose(1, 2)
+    kh = k.reshape(b, s, A, hd).transpose(1, 2)
+    vh = v.reshape(b, s, A, hd).transpose(1, 2)
+    sc = (qh @ kh.transpose(-1, -2)) / math.sqrt(hd)
+    if causal:
+        sc = sc.masked_fill(torch.ones(t, s, dtype=torch.bool).triu(1), float("-inf"))
+    return (torch.softmax(sc, -1) @ vh).transpose(1, 2).reshape(b * t, H)
 
 
 class RefStage:
@@ -99,19 +128,30 @@ class RefStage:
         d = self.d
         H, A, s = d["hidden"], d["heads"], d["seq"]
         hd = H // A
-        kind = nid.split(".")[-1] if nid not in ("embed", "lnf", "head") else nid
+        kind = nid.split(".")[-1] if "." in nid else nid
         fused = d.get("fused_attention", True)
-        ins = [env[u] for u in _inputs(nid, d["layers"], fused)]
+        ins = [env[u] for u in _inputs(nid, d)]
         w = lambda pn: W[f"{nid}.{pn}"]
-        if kind == "embed":
-            M = ids.numel()
-            return w("tok")[ids.long()] + w("pos")[torch.arange(M) % s]
-        if kind in ("ln1", "ln2", "lnf"):
+        dec = nid.startswith("d") and nid != "dembed"  # decoder block node
+        T = d.get("tgt_seq", 0)
+        if T and (dec or nid in ("dembed",)):
+            s = T
+        causal = True if dec else (d["causal"] and not T)
+        b = ids.numel() // (d["seq"] + T)
+        if kind in ("embed", "dembed"):
+            src = ids[:b * d["seq"]] if kind == "embed" else ids[b * d["seq"]:]
+            M = src.numel()
+            return w("tok")[src.long()] + w("pos")[torch.arange(M) % s]
+        if kind in ("ln1", "ln2", "lnf", "enc_ln", "lnx"):
             return F.layer_norm(ins[0], (H,), w("gamma"), w("beta"), d["ln_eps"])
         if kind in ("qkv", "fc1", "fc2"):
             return ins[0] @ w("weight").t() + w("bias")
-        if kind == "proj":
+        if kind in ("proj", "xproj"):
             return ins[0] @ w("weight").t() + w("bias") + ins[1]
+        if kind == "xattn":
+            q = ins[0] @ w("q_weight").t() + w("q_bias")
+            kv = ins[1] @ w("kv_weight").t() + w("kv_bias")
+            return _mha(q, kv[:, :H], kv[:, H:], b, A, False)
         if kind == "gelu":
             return F.gelu(ins[0], approximate="tanh")
         if kind == "add":
@@ -122,19 +162,12 @@ class RefStage:
             q = qkv[:, :H].reshape(b, s, A, hd).transpose(1, 2)
             k = qkv[:, H:2 * H].reshape(b, s, A, hd).transpose(1, 2)
             sc = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
-            if d["causal"]:
+            if causal:
                 sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), float("-inf"))
             return torch.softmax(sc, -1)
         if kind == "attn" and fused:
             qkv = ins[0]
-            b = qkv.shape[0] // s
-            q = qkv[:, :H].reshape(b, s, A, hd).transpose(1, 2)
-            k = qkv[:, H:2 * H].reshape(b, s, A, hd).transpose(1, 2)
-            v = qkv[:, 2 * H:].reshape(b, s, A, hd).transpose(1, 2)
-            sc = (q @ k.transpose(-1, -2)) / math.sqrt(hd)
-            if d["causal"]:
-                sc = sc.masked_fill(torch.ones(s, s, dtype=torch.bool).triu(1), float("-inf"))
-            return (torch.softmax(sc, -1) @ v).transpose(1, 2).reshape(b * s, H)
+            return _mha(qkv[:, :H], qkv[:, H:2 * H], qkv[:, 2 * H:], b, A, causal)
         if kind == "attn":
             P, qkv = ins
             b = qkv.shape[0] // s
@@ -193,11 +226,11 @@ class RefStage:
             p.addcdiv_(self.exp_avg[k] / bc1, denom, value=-o["lr"])
 
 
-def boundary(stage_nodes: List[List[str]], x: int, layers: int, fused: bool = True) -> List[str]:
+def boundary(stage_nodes: List[List[str]], x: int, dims: dict) -> List[str]:
     """Outputs produced at or before stage x that a later stage reads."""
     before = [n for st in stage_nodes[:x + 1] for n in st]
     after = {n for st in stage_nodes[x + 1:] for n in st}
-    return [u for u in before if any(u in _inputs(v, layers, fused) for v in after)]
+    return [u for u in before if any(u in _inputs(v, dims) for v in after)]
 
 
 def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor,
@@ -208,8 +241,7 @@ def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor
     l, m = len(stage_nodes), ids.shape[0]
     sync = schedule == "sync"
     stages = [RefStage(dims, init, nodes, opt, sync_m=m if sync else 0) for nodes in stage_nodes]
-    sends = [boundary(stage_nodes, x, dims["layers"], dims.get("fused_attention", True))
-             for x in range(l)]
+    sends = [boundary(stage_nodes, x, dims) for x in range(l)]
     all_losses = []
     for _ in range(steps):
         losses = [0.0] * m

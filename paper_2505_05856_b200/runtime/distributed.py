@@ -154,7 +154,7 @@ def run_bench_distributed(args) -> None:
                           stages=stages, micro_batch=b, memopt=plan.memopt[rank],
                           init=init_params(cfg, 0), device=dev, stream=stream)
     ids, labels = synthetic_batch(cfg, m, b, seed=0)
-    ids_d = ids.to(dev) if stage.is_first else None
+    ids_d = ids.to(dev) if stage.needs_ids else None
     lab_d = labels.to(dev) if stage.is_last else None
     loss = torch.zeros(m, device=dev) if stage.is_last else None
     torch.cuda.synchronize()

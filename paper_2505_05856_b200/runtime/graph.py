@@ -19,7 +19,7 @@ from typing import Dict, List, Optional, Tuple
 
 from ..planner.profile import ComputationGraph, ProfiledNode, TensorRef
 from .model import (NodeDef, TransformerConfig, backward_readers, build_nodes, has_stats,
-                    output_spec, saved_for_backward, stats_bytes)
+                    internal_specs, node_rows, output_spec, saved_for_backward, stats_bytes)
 
 
 def tensor_bytes(shape, dtype) -> int:
@@ -37,6 +37,10 @@ def stats_tid(node_id: str) -> str:
     return f"{node_id}.stats"
 
 
+def internal_tid(node_id: str, name: str) -> str:
+    return f"{node_id}.{name}"
+
+
 def node_param_bytes(node: NodeDef) -> int:
     total = 0
     for _, shp in node.params:
@@ -52,8 +56,9 @@ def analytic_times(cfg: TransformerConfig, b: int, tflops: float = 900.0,
     """Roofline estimate (us) per node: max(flops / tflops, bytes / gbs), bwd = 2x
     contraction work.  Only a placeholder until profiler times exist."""
     out = {}
-    M, H, F, s = b * cfg.seq, cfg.hidden, cfg.ffn, cfg.seq
+    H = cfg.hidden
     for n in build_nodes(cfg):
+        M, s = node_rows(cfg, n, b), n.seq or cfg.seq
         shape, dt = output_spec(cfg, n, b)
         byt = tensor_bytes(shape, dt)
         fl = 0
@@ -66,6 +71,8 @@ def analytic_times(cfg: TransformerConfig, b: int, tflops: float = 900.0,
             fl = 2 * b * cfg.heads * s * s * cfg.head_dim
         elif n.kind == "attn_fused":
             fl = 4 * b * cfg.heads * s * s * cfg.head_dim
+        elif n.kind == "xattn":  # q and kv projections + the two attention products
+            fl = 2 * M * H * H + 2 * b * cfg.seq * 2 * H * H + 4 * b * cfg.heads * s * cfg.seq * cfg.head_dim
         tf = max(1, int(round(max(fl / (tflops * 1e6), 2 * byt / (gbs * 1e3)))))
         tb = max(1, int(round(max(2 * fl / (tflops * 1e6), 3 * byt / (gbs * 1e3)))))
         out[n.id] = (tf, tb)
@@ -101,7 +108,9 @@ def profile_graph(cfg: TransformerConfig, b: int,
     clock = 0
     for i, n in enumerate(nodes):
         shape, dt = output_spec(cfg, n, b)
-        m_a = tensor_bytes(shape, dt) + stats_bytes(cfg, n, b)
+        internal = internal_specs(cfg, n, b)
+        m_a = (tensor_bytes(shape, dt) + stats_bytes(cfg, n, b)
+               + sum(tensor_bytes(shp, t) for shp, t in internal.values()))
         saved = []
         if saved_for_backward(n):
             rd = [index[r] for r in readers[n.id]]
@@ -109,6 +118,8 @@ def profile_graph(cfg: TransformerConfig, b: int,
                 saved.append(TensorRef(out_tid(n.id), tensor_bytes(shape, dt), n.id, min(rd)))
         if has_stats(n):
             saved.append(TensorRef(stats_tid(n.id), stats_bytes(cfg, n, b), n.id, i))
+        for nm, (shp, t) in internal.items():
+            saved.append(TensorRef(internal_tid(n.id, nm), tensor_bytes(shp, t), n.id, i))
         t_f, t_b = times[n.id]
         out.append(ProfiledNode(
             id=n.id, depth=depth[n.id], fwd_start=clock, t_f=int(t_f), t_b=int(t_b), m_a=m_a,

@@ -90,9 +90,10 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
                            device=dev, stream=stream)
         w = l - x + 1
         m = micro_batches or (w + 1)
-        M = b * model.seq
         gen = torch.Generator(device=dev).manual_seed(x)
-        ids = torch.randint(0, model.vocab, (m, M), device=dev, dtype=torch.int32, generator=gen)
+        ids = torch.randint(0, model.vocab, (m, b * model.in_tokens), device=dev, dtype=torch.int32,
+                            generator=gen)
+        labels = ids[:, :b * model.out_tokens]
         loss = torch.zeros(m, device=dev)
         with torch.cuda.stream(stream):
             for kind, j, _ in async_ops(l, m, x):
@@ -100,8 +101,8 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
                     for tid in ex.recv_ids:
                         buf = ex.recv_buffer(tid, j)
                         buf.normal_(0, 1, generator=gen) if buf.is_floating_point() else None
-                    ex.forward(j, ids=ids[j - 1] if ex.is_first else None,
-                               labels=ids[j - 1] if ex.is_last else None,
+                    ex.forward(j, ids=ids[j - 1] if ex.needs_ids else None,
+                               labels=labels[j - 1] if ex.is_last else None,
                                loss_out=loss[j - 1:j] if ex.is_last else None)
                 else:
                     for tid in ex.send_ids:

@@ -253,7 +253,7 @@ class Pipeline:
             if kind == "fwd":
                 if x > 1:
                     self._deliver_fwd(x, j, mailbox.pop((x, j)))
-                s.forward(j, ids=ids[j - 1] if s.is_first else None,
+                s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
                           labels=labels[j - 1] if s.is_last else None,
                           loss_out=self.loss[j - 1:j] if s.is_last else None)
                 if x < self.l:

@@ -39,8 +39,9 @@ from .. import kernels as K
 from ..planner.balance import SCHEDULE_ASYNC, SCHEDULE_SYNC
 from ..planner.memplan import MemOptPlan, producer_chain
 from ..planner.profile import ComputationGraph
-from .graph import out_tid, stats_tid
+from .graph import internal_tid, out_tid, stats_tid
 from .model import (AdamWConfig, NodeDef, TransformerConfig, backward_readers, has_stats,
+                    internal_specs, node_rows,
                     output_spec, saved_for_backward)
 
 BF16 = torch.bfloat16
@@ -69,7 +70,8 @@ class FlatParams:
         for n in nodes:
             for pn, shp in n.params:
                 name = f"{n.id}.{pn}"
-                is_dense = n.kind in ("linear", "linear_res", "head") and pn == "weight"
+                is_dense = ((n.kind in ("linear", "linear_res", "head") and pn == "weight")
+                            or (n.kind == "xattn" and pn in ("q_weight", "kv_weight")))
                 (dense if is_dense else accum).append((name, tuple(shp)))
         self.slots: Dict[str, ParamSlot] = {}
         off = 0
@@ -160,6 +162,10 @@ class StageExecutor:
         self.stage, self.stages = stage, stages
         self.b = micro_batch
         self.M = micro_batch * cfg.seq
+        # token rows of the id input (encoder-decoder: src then tgt) and of the head
+        self.in_rows = micro_batch * cfg.in_tokens
+        self.out_rows = micro_batch * cfg.out_tokens
+        self.id_offset = {"embed": 0, "dembed": self.M}
         self.device = device
         self.stream = stream
         self.copy_stream = torch.cuda.Stream(device=device)
@@ -181,8 +187,11 @@ class StageExecutor:
         # dense weight gradients are written by the first backward of an
         # iteration and accumulated by the rest (sync only)
         self._wgrad_acc = False
-        self.grad_scale = 1.0 / (self.M * self.m_sync)  # mean over the iteration's tokens
+        self.grad_scale = 1.0 / (self.out_rows * self.m_sync)  # mean over the iteration's tokens
         self.is_first = lo == 0
+        # stages holding an embedding node take the micro-batch's token ids
+        # (encoder-decoder: `dembed` may sit behind a cut at position 0)
+        self.needs_ids = any(n.kind == "embed" for n in self.nodes)
         self.is_last = hi == len(self.all_nodes) - 1
         self.node_by_id = {n.id: n for n in self.all_nodes}
         self.index = {n.id: i for i, n in enumerate(self.all_nodes)}
@@ -197,8 +206,7 @@ class StageExecutor:
         # tensors some backward in this stage reads
         needed: Set[str] = set()
         for n in self.nodes:
-            if has_stats(n):
-                needed.add(stats_tid(n.id))
+            needed.update(self.self_tids(n))
         for src, rd in self.readers.items():
             if any(r in in_stage for r in rd) and saved_for_backward(self.node_by_id[src]):
                 needed.add(out_tid(src))
@@ -224,7 +232,7 @@ class StageExecutor:
         self.host: Dict[str, List[torch.Tensor]] = {}
         self.live: Dict[str, torch.Tensor] = {}
         ids_needed = {out_tid(n) for n in self._produced_or_received()}
-        ids_needed |= {stats_tid(n.id) for n in self.nodes if has_stats(n)}
+        ids_needed |= {t for n in self.nodes for t in self.self_tids(n)}
         for tid in sorted(ids_needed):
             shape, dt = self._spec(tid)
             if tid in needed and tid not in self.evicted:
@@ -236,10 +244,12 @@ class StageExecutor:
                                       for _ in range(self.w)]
             else:
                 self.work[tid] = torch.empty(shape, dtype=dt, device=device)
-        if self.is_first:
-            self.ids = [torch.empty(self.M, dtype=torch.int32, device=device) for _ in range(self.w)]
+        if self.needs_ids:
+            self.ids = [torch.empty(self.in_rows, dtype=torch.int32, device=device)
+                        for _ in range(self.w)]
         if self.is_last:
-            self.labels = [torch.empty(self.M, dtype=torch.int32, device=device) for _ in range(self.w)]
+            self.labels = [torch.empty(self.out_rows, dtype=torch.int32, device=device)
+                           for _ in range(self.w)]
             self.loss = torch.zeros(1, dtype=F32, device=device)
         self.swap_in_done: Dict[str, torch.cuda.Event] = {}
         # D2H back-pressure: memory of a swapped tensor is recycled only once its
@@ -289,14 +299,13 @@ class StageExecutor:
         self.fwd_last: Dict[str, float] = {}
         for tid in self.evicted:
             src, kind = tid.rsplit(".", 1)
-            users = [src] if kind == "stats" else [n.id for n in self.nodes if src in n.inputs]
+            users = [src] if kind != "out" else [n.id for n in self.nodes if src in n.inputs]
             last = max((pos[u] for u in users), default=-1)
             self.fwd_last[tid] = math.inf if tid in self.send_ids else last
         self.bwd_reads: Dict[str, List[str]] = {}
         for n in self.nodes:
             reads = [out_tid(src) for src, rd in self.readers.items() if n.id in rd]
-            if has_stats(n):
-                reads.append(stats_tid(n.id))
+            reads += self.self_tids(n)
             if n.id in self.bwd_gelu_of:  # fused GELU backward reads the pre-activation
                 reads.append(out_tid(self.node_by_id[self.bwd_gelu_of[n.id]].inputs[0]))
             self.bwd_reads[n.id] = [t for t in reads if t in self.evicted]
@@ -313,6 +322,13 @@ class StageExecutor:
 
     # ---- helpers -------------------------------------------------------------------
 
+    def self_tids(self, n: NodeDef) -> List[str]:
+        """Tensors n produces besides its output that only its own backward reads:
+        statistics (LayerNorm mean/rstd, attention LSE) and internal tensors
+        (cross-attention q / kv / P)."""
+        out = [stats_tid(n.id)] if has_stats(n) else []
+        return out + [internal_tid(n.id, k) for k in internal_specs(self.cfg, n, self.b)]
+
     def _boundary(self, pos: int) -> List[str]:
         """Output tids crossing the cut after canonical index pos (simulate.py:93-100)."""
         last = self.g.last_consumer
@@ -328,8 +344,10 @@ class StageExecutor:
         node = self.node_by_id[nid]
         if kind == "stats":
             if node.kind == "attn_fused":
-                return (self.b, self.cfg.heads, self.cfg.seq), F32
-            return (2, self.M), F32
+                return (self.b, self.cfg.heads, node.seq or self.cfg.seq), F32
+            return (2, node_rows(self.cfg, node, self.b)), F32
+        if kind != "out":
+            return internal_specs(self.cfg, node, self.b)[kind]
         return output_spec(self.cfg, node, self.b)
 
     def buf(self, tid: str, slot: int, phase: str) -> torch.Tensor:
@@ -371,7 +389,7 @@ class StageExecutor:
         self.slot_mb[slot] = mb
         ver = self.params.pin_latest(mb)
         with torch.cuda.stream(st):
-            if self.is_first:
+            if self.needs_ids:
                 self.ids[slot].copy_(ids, non_blocking=True)
             if self.is_last:
                 self.labels[slot].copy_(labels, non_blocking=True)
@@ -412,7 +430,7 @@ class StageExecutor:
         return self.buf(tid, self.slot_of(mb), "fwd")
 
     def _outputs(self, n: NodeDef) -> List[str]:
-        outs = [out_tid(n.id)] + ([stats_tid(n.id)] if has_stats(n) else [])
+        outs = [out_tid(n.id)] + self.self_tids(n)
         if n.id in self.fwd_gelu_of:
             outs.append(out_tid(self.fwd_gelu_of[n.id]))
         if n.id in self.fwd_add_of:
@@ -460,7 +478,9 @@ class StageExecutor:
         inp = [self.buf(out_tid(u), slot, phase) for u in n.inputs]
         k = n.kind
         if k == "embed":
-            K.embed_fwd(self.ids[slot], W("tok"), W("pos"), out, cfg.seq, stream=st)
+            off, rows = self.id_offset[n.id], node_rows(cfg, n, self.b)
+            K.embed_fwd(self.ids[slot][off:off + rows], W("tok"), W("pos"), out, n.seq or cfg.seq,
+                        stream=st)
         elif k == "ln":
             stats = self.buf(stats_tid(n.id), slot, phase)
             K.layernorm_fwd(inp[0], W("gamma"), W("beta"), out, stats[0], stats[1], cfg.ln_eps,
@@ -487,19 +507,22 @@ class StageExecutor:
             if not (phase == "fwd" and n.inputs[0] in self.fwd_add_of):
                 K.add(inp[0], inp[1], out, stream=st)
         elif k == "score":
-            self._scores(inp[0], out)
-            K.softmax_fwd(out, out, cfg.seq, 1.0 / math.sqrt(cfg.head_dim), cfg.causal, stream=st)
+            self._scores(inp[0], out, n.seq or cfg.seq)
+            K.softmax_fwd(out, out, n.seq or cfg.seq, 1.0 / math.sqrt(cfg.head_dim), n.causal,
+                          stream=st)
         elif k == "attn":
-            self._pv(inp[0], inp[1], out)
+            self._pv(inp[0], inp[1], out, n.seq or cfg.seq)
         elif k == "attn_fused":
             lse = self.buf(stats_tid(n.id), slot, phase)
-            K.attn_fwd(inp[0], out, lse, self.b, cfg.seq, cfg.heads, cfg.causal, stream=st)
+            K.attn_fwd(inp[0], out, lse, self.b, n.seq or cfg.seq, cfg.heads, n.causal, stream=st)
+        elif k == "xattn":
+            self._xattn_fwd(n, inp[0], inp[1], out, slot, phase, W)
         elif k == "head":
             K.linear_fwd(inp[0], W("weight"), out, stream=st)
             # fused loss + dlogits; on a recompute replay the loss is discarded
             loss = (loss_out if loss_out is not None else self.loss) if phase == "fwd" else self._scratch_loss()
-            K.xent(out, self.labels[slot], cfg.vocab, self.grad_scale, loss, out, loss_scale=1.0 / M,
-                   stream=st)
+            K.xent(out, self.labels[slot], cfg.vocab, self.grad_scale, loss, out,
+                   loss_scale=1.0 / self.out_rows, stream=st)
         else:
             raise ValueError(k)
 
@@ -508,17 +531,73 @@ class StageExecutor:
             self._sl = torch.zeros(1, dtype=F32, device=self.device)
         return self._sl
 
+    # cross-attention (decoder): q from the decoder stream, k/v from E
+    def _xattn_fwd(self, n: NodeDef, c, E, out, slot: int, phase: str, W) -> None:
+        cfg, st = self.cfg, self.stream
+        t, s, d, A, H, b = n.seq, cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        q = self.buf(internal_tid(n.id, "q"), slot, phase)
+        kv = self.buf(internal_tid(n.id, "kv"), slot, phase)
+        P = self.buf(internal_tid(n.id, "p"), slot, phase)
+        K.linear_fwd(c, W("q_weight"), q, bias=W("q_bias"), stream=st)
+        K.linear_fwd(E, W("kv_weight"), kv, bias=W("kv_bias"), stream=st)
+        # S = q K^T per (batch, head): [t, s]
+        K.gemm_raw(M=t, N=s, K=d, A=q, lda=H, a_s=(d, t * H), B=kv, ldb=2 * H, b_s=(d, s * 2 * H),
+                   batch1=A, batch2=b, Cout=P, ldc=s, c_s=(t * s, A * t * s), stream=st)
+        K.softmax_fwd(P, P, t, 1.0 / math.sqrt(d), False, stream=st)
+        # O = P V: V rows are s-contiguous per head (MN-major over d)
+        K.gemm_raw(M=t, N=d, K=s, A=P, lda=s, a_s=(t * s, A * t * s), B=kv[:, H:], ldb=2 * H,
+                   b_mn=True, b_s=(d, s * 2 * H), batch1=A, batch2=b, Cout=out, ldc=H,
+                   c_s=(d, t * H), stream=st)
+
+    def _xattn_bwd(self, n: NodeDef, dy, slot: int, W, G) -> None:
+        cfg, st = self.cfg, self.stream
+        t, s, d, A, H, b = n.seq, cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        c_t, e_t = out_tid(n.inputs[0]), out_tid(n.inputs[1])
+        c, E = self.buf(c_t, slot, "bwd"), self.buf(e_t, slot, "bwd")
+        q = self.buf(internal_tid(n.id, "q"), slot, "bwd")
+        kv = self.buf(internal_tid(n.id, "kv"), slot, "bwd")
+        P = self.buf(internal_tid(n.id, "p"), slot, "bwd")
+        dS = torch.empty_like(P)
+        dq = torch.empty_like(q)
+        dkv = torch.empty_like(kv)
+        # dP = dO V^T
+        K.gemm_raw(M=t, N=s, K=d, A=dy, lda=H, a_s=(d, t * H), B=kv[:, H:], ldb=2 * H,
+                   b_s=(d, s * 2 * H), batch1=A, batch2=b, Cout=dS, ldc=s, c_s=(t * s, A * t * s),
+                   stream=st)
+        # dV = P^T dO
+        K.gemm_raw(M=s, N=d, K=t, A=P, lda=s, a_mn=True, a_s=(t * s, A * t * s), B=dy, ldb=H,
+                   b_mn=True, b_s=(d, t * H), batch1=A, batch2=b, Cout=dkv[:, H:], ldc=2 * H,
+                   c_s=(d, s * 2 * H), stream=st)
+        K.softmax_bwd(P, dS, dS, 1.0 / math.sqrt(d), stream=st)  # dS (scale folded)
+        # dq = dS K ; dK = dS^T q
+        K.gemm_raw(M=t, N=d, K=s, A=dS, lda=s, a_s=(t * s, A * t * s), B=kv, ldb=2 * H, b_mn=True,
+                   b_s=(d, s * 2 * H), batch1=A, batch2=b, Cout=dq, ldc=H, c_s=(d, t * H), stream=st)
+        K.gemm_raw(M=s, N=d, K=t, A=dS, lda=s, a_mn=True, a_s=(t * s, A * t * s), B=q, ldb=H,
+                   b_mn=True, b_s=(d, t * H), batch1=A, batch2=b, Cout=dkv, ldc=2 * H,
+                   c_s=(d, s * 2 * H), stream=st)
+        # projections: dc (+)= dq Wq, dE (+)= dkv Wkv, weight / bias gradients
+        for g_in, w, x_t, x, wn, bn in ((dq, W("q_weight"), c_t, c, "q_weight", "q_bias"),
+                                         (dkv, W("kv_weight"), e_t, E, "kv_weight", "kv_bias")):
+            if x_t in self.grad_init:
+                dx = self.grads[x_t]
+                K.linear_dgrad(g_in, w, dx, accumulate_into=dx, stream=st)
+            else:
+                K.linear_dgrad(g_in, w, self.grad_buffer(x_t), stream=st)
+                self.grad_init.add(x_t)
+            K.linear_wgrad(g_in, x, G(wn), accumulate=self._wgrad_acc, stream=st)
+            K.colsum(g_in, G(bn), stream=st)
+
     # attention products straight out of the fused [M, 3H] qkv buffer
-    def _scores(self, qkv, S):
+    def _scores(self, qkv, S, s):
         cfg = self.cfg
-        s, d, A, H, b = cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        d, A, H, b = cfg.head_dim, cfg.heads, cfg.hidden, self.b
         K.gemm_raw(M=s, N=s, K=d, A=qkv, lda=3 * H, a_s=(d, s * 3 * H), B=qkv[:, H:], ldb=3 * H,
                    b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=S, ldc=s,
                    c_s=(s * s, A * s * s), stream=self.stream)
 
-    def _pv(self, P, qkv, O):
+    def _pv(self, P, qkv, O, s):
         cfg = self.cfg
-        s, d, A, H, b = cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        d, A, H, b = cfg.head_dim, cfg.heads, cfg.hidden, self.b
         K.gemm_raw(M=s, N=d, K=s, A=P, lda=s, a_s=(s * s, A * s * s), B=qkv[:, 2 * H:], ldb=3 * H,
                    b_mn=True, b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=O, ldc=H,
                    c_s=(d, s * H), stream=self.stream)
@@ -641,7 +720,7 @@ class StageExecutor:
     def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
         # outputs of a replayed node land in a live buffer if evicted, else in
         # their normal home (slot buffer or workspace)
-        for t in [out_tid(n.id)] + ([stats_tid(n.id)] if has_stats(n) else []):
+        for t in [out_tid(n.id)] + self.self_tids(n):
             if t in self.evicted and t not in self.live:
                 self._alloc_live(t)
         self._node_fwd(n, slot, ver, "bwd")
@@ -668,7 +747,9 @@ class StageExecutor:
             return  # nothing flows into this node (cannot happen for a connected graph)
         dy = self.grads[tid]
         if k == "embed":
-            K.embed_bwd(self.ids[slot], dy, G("tok"), G("pos"), cfg.seq, stream=st)
+            off, rows = self.id_offset[n.id], node_rows(cfg, n, self.b)
+            K.embed_bwd(self.ids[slot][off:off + rows], dy, G("tok"), G("pos"), n.seq or cfg.seq,
+                        stream=st)
         elif k == "ln":
             x_t = out_tid(n.inputs[0])
             x = self.buf(x_t, slot, "bwd")
@@ -723,7 +804,7 @@ class StageExecutor:
             qkv = self.buf(qkv_t, slot, "bwd")
             dP = self.grad_buffer(P_t)
             dqkv = self.grad_buffer(qkv_t)
-            s, d, A, b = cfg.seq, cfg.head_dim, cfg.heads, self.b
+            s, d, A, b = n.seq or cfg.seq, cfg.head_dim, cfg.heads, self.b
             # dP = dO V^T : A = dO (K-major over d), B = V (K-major over d)
             K.gemm_raw(M=s, N=s, K=d, A=dy, lda=H, a_s=(d, s * H), B=qkv[:, 2 * H:], ldb=3 * H,
                        b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=dP, ldc=s,
@@ -738,15 +819,17 @@ class StageExecutor:
             assert qkv_t not in self.grad_init
             dqkv = self.grad_buffer(qkv_t)
             K.attn_bwd(self.buf(qkv_t, slot, "bwd"), self.buf(tid, slot, "bwd"), dy,
-                       self.buf(stats_tid(n.id), slot, "bwd"), dqkv, self.b, cfg.seq, cfg.heads,
-                       cfg.causal, stream=st)
+                       self.buf(stats_tid(n.id), slot, "bwd"), dqkv, self.b, n.seq or cfg.seq,
+                       cfg.heads, n.causal, stream=st)
             self.grad_init.add(qkv_t)
+        elif k == "xattn":
+            self._xattn_bwd(n, dy, slot, W, G)
         elif k == "score":
             qkv_t = out_tid(n.inputs[0])
             Pm = self.buf(tid, slot, "bwd")
             qkv = self.buf(qkv_t, slot, "bwd")
             dqkv = self.grads[qkv_t]
-            s, d, A, b = cfg.seq, cfg.head_dim, cfg.heads, self.b
+            s, d, A, b = n.seq or cfg.seq, cfg.head_dim, cfg.heads, self.b
             K.softmax_bwd(Pm, dy, dy, 1.0 / math.sqrt(d), stream=st)  # dy := dS (pre-scale folded)
             # dQ = dS K : A = dS (K-major over keys), B = K (MN-major, d contiguous)
             K.gemm_raw(M=s, N=d, K=s, A=dy, lda=s, a_s=(s * s, A * s * s), B=qkv[:, H:], ldb=3 * H,

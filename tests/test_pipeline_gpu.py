@@ -51,7 +51,8 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
     stage_nodes = [nodes[lo:hi + 1] for lo, hi in stage_bounds(plan.cuts, len(g))]
     dims = dict(layers=cfg.layers, hidden=cfg.hidden, heads=cfg.heads, seq=cfg.seq,
                 vocab=cfg.vocab, causal=cfg.causal, ln_eps=cfg.ln_eps,
-                fused_attention=cfg.fused_attention)
+                fused_attention=cfg.fused_attention, dec_layers=cfg.dec_layers,
+                tgt_seq=cfg.tgt_seq)
     init = init_params(cfg, 0)
     ref_losses, ref_params = reference_train(
         dims, init, ids, labels, stage_nodes,
@@ -73,6 +74,9 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
                 H = cfg.hidden
                 keep = torch.cat([torch.arange(0, H), torch.arange(2 * H, 3 * H)])
                 got, want, w0 = got[keep], want[keep], w0[keep]
+            elif name.endswith("xattn.kv_bias"):  # same for the cross-attention key bias
+                H = cfg.hidden
+                got, want, w0 = got[H:], want[H:], w0[H:]
             rel = float((got - want).norm() / (want.norm() + 1e-12))
             dg = (got - w0).flatten()
             dr = (want - w0).flatten()
@@ -136,4 +140,21 @@ def test_pipeline_sync_gpipe_matches_oracle(name, stages):
 def test_pipeline_sync_with_memopt():
     cfg, g, plan = _setup("tiny", 2, 0.6, 16 << 30, schedule="sync")
     assert any(m.actions for m in plan.memopt)
+    _compare(cfg, g, plan)
+
+
+@pytest.mark.parametrize("stages", [1, 2, 3, 4])
+def test_pipeline_t5_encoder_decoder(stages):
+    """T5-style encoder-decoder (BASELINE configs[3] at tiny size): relayed
+    boundary tensors (decoder layer-0 sub-block outputs through the encoder
+    stages, E through the decoder stages), cross-attention, two sequence lengths."""
+    cfg, g, plan = _setup("tiny-t5", stages, 4.0, 16 << 30)
+    _compare(cfg, g, plan)
+
+
+def test_pipeline_t5_memopt_and_sync():
+    cfg, g, plan = _setup("tiny-t5", 3, 0.6, 16 << 30)
+    assert any(m.actions for m in plan.memopt)
+    _compare(cfg, g, plan)
+    cfg, g, plan = _setup("tiny-t5", 2, 4.0, 16 << 30, schedule="sync")
     _compare(cfg, g, plan)
