@@ -32,6 +32,7 @@ class GemmArgs(C.Structure):
         ("block_n", _i32),
         ("split_k", _i32),
         ("cta_group", _i32),
+        ("epilogue", _i32),
     ]
 
 

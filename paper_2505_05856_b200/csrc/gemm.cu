@@ -14,9 +14,13 @@
 //   warp 1      MMA issuer: one elected lane issues tcgen05.mma (M=128, N=BN,
 //               K=16) into a double-buffered TMEM accumulator
 //   warp 2      TMEM allocator
-//   warps 4-7   epilogue: tcgen05.ld (a 32-row x 32-column fp32 block per
-//               warp) -> shared-memory transpose -> alpha/bias/residual/GELU
-//               on row-contiguous 16-byte vectors -> coalesced global stores
+//   warps 4-11  epilogue: tcgen05.ld (each thread one accumulator row) ->
+//               alpha/bias/residual/GELU in registers -> a 128-byte-swizzled
+//               32-row staging tile in shared memory -> TMA bulk store (f32
+//               split-K / accumulate: TMA bulk reduce-add).  The residual
+//               operand is TMA-loaded into a second staging tile ahead of use,
+//               so the epilogue issues no per-thread global loads or stores.
+//               Batched (attention) GEMMs keep a direct-store epilogue.
 // Barriers: full/empty per smem stage (TMA <-> MMA), tmem_full/tmem_empty per
 // accumulator buffer (MMA <-> epilogue), so the epilogue of one work unit
 // overlaps the mainloop of the next.
@@ -40,6 +44,7 @@ constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
 struct GemmParams {
+  int tma_epi;  // 1: staged TMA-store epilogue (tmC / tmR / tmX valid)
   int M, N, K;
   int Z1, Z;
   int tiles_m, tiles_n, tile_m;
@@ -57,16 +62,62 @@ struct GemmParams {
   int gelu;
 };
 
+// per epilogue warp: a 4 KB output staging tile (32 rows x 128 B) and a 4 KB
+// side tile (the TMA-loaded residual, or the GELU pre-activation `aux` output)
+constexpr int kEpiStage = 4096;
+constexpr int kEpiBytes = kEpiWarps * 2 * kEpiStage;
+constexpr int kMaxSmem = 232448;  // 227 KB per CTA on sm_100
+
 template <int BN, int CG>
 struct Cfg {
   static constexpr int kBRows = BN / CG;  // rows of B this CTA loads (pair: half of N)
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kStages = (200 * 1024) / kStageBytes < 8 ? (200 * 1024) / kStageBytes : 8;
+  static constexpr int kFit = (kMaxSmem - kEpiBytes - 2048) / kStageBytes;
+  static constexpr int kStages = kFit < 8 ? kFit : 8;
   static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(kSmem <= kMaxSmem, "shared memory budget");
 };
+
+// byte offset of 16-byte chunk c of row r in a 128-byte-swizzled tile
+__device__ __forceinline__ uint32_t swz128(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
+
+__device__ __forceinline__ void epi_fence_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d_cta(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int c0,
+                                                  int c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 struct Unit {
   int z1, z2, m0, nb, kb0, kb1;
@@ -230,22 +281,159 @@ __device__ __forceinline__ void epilogue_chunk(const GemmParams& p, float* v, in
   }
 }
 
+// TMA-staged epilogue of one accumulator tile for one epilogue warp: rows
+// [row_base, row_base+32) (one per lane), the warp's column chunks of the tile.
+// bf16 outputs move in 64-column chunks (128-byte rows), f32 in 32-column ones.
+template <int BN>
+__device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUtensorMap* tmC,
+                                                  const CUtensorMap* tmR, const CUtensorMap* tmX,
+                                                  uint32_t taddr, int n0, int row_base, int half,
+                                                  int lane, uint8_t* s_out, uint8_t* s_side,
+                                                  uint64_t* rbar, uint32_t& rphase) {
+  if (p.c_f32) {
+    constexpr int kChunks = BN / 32;
+#pragma unroll 1
+    for (int c = half; c < kChunks; c += 2) {
+      const int col0 = n0 + c * 32;
+      if (col0 >= p.N) break;
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + c * 32, r);
+      tmem_ld_wait();
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 o = make_float4(__uint_as_float(r[4 * q]) * p.alpha, __uint_as_float(r[4 * q + 1]) * p.alpha,
+                               __uint_as_float(r[4 * q + 2]) * p.alpha, __uint_as_float(r[4 * q + 3]) * p.alpha);
+        *reinterpret_cast<float4*>(s_out + swz128(lane, q)) = o;
+      }
+      epi_fence_async();
+      __syncwarp();
+      if (lane == 0) {
+        if (p.splits > 1 || p.accumulate) tma_reduce_add_2d(tmC, s_out, col0, row_base);
+        else tma_store_2d(tmC, s_out, col0, row_base);
+        bulk_commit();
+      }
+    }
+    return;
+  }
+  constexpr int kChunks = BN / 64;
+  const bool res = p.res != nullptr;
+  const bool aux = p.gelu && p.aux != nullptr;
+#pragma unroll 1
+  for (int c = half; c < kChunks; c += 2) {
+    const int col0 = n0 + c * 64;
+    if (col0 >= p.N) break;
+    float v[64];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t r[32];
+      tmem_ld_32x32b_x32(taddr + c * 64 + h * 32, r);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[h * 32 + i] = __uint_as_float(r[i]) * p.alpha;
+    }
+    if (p.bias) {
+      const __nv_bfloat16* bp = p.bias + col0;
+      if (col0 + 64 <= p.N) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint4 u = reinterpret_cast<const uint4*>(bp)[q];
+          const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float2 f = __bfloat1622float2(hh[k]);
+            v[8 * q + 2 * k] += f.x;
+            v[8 * q + 2 * k + 1] += f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (col0 + i < p.N) v[i] += __bfloat162float(bp[i]);
+      }
+    }
+    if (res) {
+      mbar_wait(rbar, rphase);
+      rphase ^= 1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint4 u = *reinterpret_cast<const uint4*>(s_side + swz128(lane, q));
+        const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float2 f = __bfloat1622float2(hh[k]);
+          if (p.res_mode == 0) {
+            v[8 * q + 2 * k] += f.x;
+            v[8 * q + 2 * k + 1] += f.y;
+          } else {
+            v[8 * q + 2 * k] *= gelu_tanh_grad(f.x);
+            v[8 * q + 2 * k + 1] *= gelu_tanh_grad(f.y);
+          }
+        }
+      }
+      __syncwarp();  // every lane has read the residual tile: prefetch the next chunk's
+      const int cn = c + 2;
+      if (lane == 0 && cn < kChunks && n0 + cn * 64 < p.N) {
+        mbar_expect_tx(rbar, kEpiStage);
+        tma_load_2d_cta(s_side, tmR, rbar, n0 + cn * 64, row_base);
+      }
+    }
+    if (lane == 0) bulk_wait_read0();  // earlier stores have finished reading the staging tiles
+    __syncwarp();
+    if (aux) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        uint4 u;
+        u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+        u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+        u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+        u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+        *reinterpret_cast<uint4*>(s_side + swz128(lane, q)) = u;
+      }
+    }
+    if (p.gelu) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      uint4 u;
+      u.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+      u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+      u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+      u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+      *reinterpret_cast<uint4*>(s_out + swz128(lane, q)) = u;
+    }
+    epi_fence_async();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_2d(tmC, s_out, col0, row_base);
+      if (aux) tma_store_2d(tmX, s_side, col0, row_base);
+      bulk_commit();
+    }
+  }
+}
+
 template <int BN, bool A_MN, bool B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                const GemmParams p) {
+                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
+                const __grid_constant__ CUtensorMap tmX, const GemmParams p) {
   using C = Cfg<BN, CG>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::kStages * C::kABytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+  uint8_t* sEpi = smem + C::kStages * C::kStageBytes;  // 1024-aligned (stage bytes are)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sEpi + kEpiBytes);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::kStages;
   uint64_t* tfull = bars + 2 * C::kStages;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rbar = tempty + 2;  // one residual-tile barrier per epilogue warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -259,6 +447,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    if (p.tma_epi) {
+      prefetch_tmap(&tmC);
+      if (p.res) prefetch_tmap(&tmR);
+      if (p.aux) prefetch_tmap(&tmX);
+    }
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
@@ -269,6 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], CG * kEpiWarps);  // one arrival per epilogue warp of the pair
     }
+    for (int e = 0; e < kEpiWarps; ++e) mbar_init(&rbar[e], 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols, CG>(tmem_slot);
@@ -376,9 +570,35 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int half = ew >> 2;           // which column chunks (even / odd) it owns
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint8_t* s_out = sEpi + ew * 2 * kEpiStage;
+    uint8_t* s_side = s_out + kEpiStage;
+    uint32_t rphase = 0;
     for (long long u = cluster_id; u < p.units; u += n_clusters) {
       const Unit w = decode(p, u, nk);
       const int n0 = w.nb * BN;
+      if (p.tma_epi) {
+        const int row_base = w.m0 + BM * (int)rank + lanes;
+        // the first residual tile loads while the accumulator is still being built
+        if (p.res && lane == 0 && n0 + half * 64 < p.N) {
+          mbar_expect_tx(&rbar[ew], kEpiStage);
+          tma_load_2d_cta(s_side, &tmR, &rbar[ew], n0 + half * 64, row_base);
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        epilogue_tile_tma<BN>(p, &tmC, &tmR, &tmX, tmem_base + acc * BN + ((uint32_t)lanes << 16), n0,
+                              row_base, half, lane, s_out, s_side, &rbar[ew], rphase);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
+          else mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+        continue;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = w.m0 + BM * (int)rank + lanes + lane;
@@ -406,6 +626,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
+    if (p.tma_epi && lane == 0) bulk_wait0();  // stores complete before the CTA retires
   }
 
   tc_fence_before();
@@ -484,6 +705,52 @@ int make_map(CUtensorMap* map, const void* ptr, long long inner, long long outer
   return rc;
 }
 
+// 2-D epilogue map over an output / residual / aux matrix [rows, cols] with
+// leading dimension ld: box 32 rows x 128 bytes, 128-byte swizzle (the staging
+// tile layout of epilogue_tile_tma).
+struct EpiKey {
+  const void* ptr;
+  long long rows, cols, ld;
+  int f32;
+  bool operator==(const EpiKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && f32 == o.f32;
+  }
+};
+struct EpiKeyHash {
+  size_t operator()(const EpiKey& k) const {
+    size_t h = std::hash<const void*>()(k.ptr);
+    for (long long v : {k.rows, k.cols, k.ld, (long long)k.f32}) h = h * 1000003u ^ std::hash<long long>()(v);
+    return h;
+  }
+};
+std::unordered_map<EpiKey, CUtensorMap, EpiKeyHash> g_epi_maps;
+
+int make_epi_map(CUtensorMap* map, const void* ptr, long long rows, long long cols, long long ld,
+                 bool f32) {
+  const EpiKey key{ptr, rows, cols, ld, f32 ? 1 : 0};
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  auto it = g_epi_maps.find(key);
+  if (it != g_epi_maps.end()) {
+    *map = it->second;
+    return 0;
+  }
+  EncodeFn enc = encode_fn();
+  DPN_REQUIRE(enc != nullptr, "cuTensorMapEncodeTiled unavailable");
+  const int es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / es), 32};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  DPN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (epilogue) failed (code " + std::to_string((int)r) + ")");
+  if (g_epi_maps.size() > 65536) g_epi_maps.clear();
+  g_epi_maps.emplace(key, *map);
+  return 0;
+}
+
 // 4-D map over a bf16 operand: (inner, z1, outer, z2); box (64, 1, box_outer, 1).
 int encode_map(CUtensorMap* map, const void* ptr, long long inner, long long outer, long long ld,
                int Z1, long long s1, int Z2, long long s2, int box_outer) {
@@ -535,6 +802,16 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
   if (rc) return rc;
 
   GemmParams p = p0;
+  CUtensorMap tc{}, tr{}, tx{};
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  p.tma_epi = g->batch1 * g->batch2 == 1 && (!p.res || (al16(p.res) && p.ldr % 8 == 0)) &&
+              (!p.aux || al16(p.aux)) && g->epilogue != 1;
+  if (p.tma_epi) {
+    rc = make_epi_map(&tc, g->C, g->M, g->N, g->ldc, p.c_f32 != 0);
+    if (!rc && p.res) rc = make_epi_map(&tr, p.res, g->M, g->N, p.ldr, false);
+    if (!rc && p.aux) rc = make_epi_map(&tx, p.aux, g->M, g->N, g->ldc, false);
+    if (rc) return rc;
+  }
   p.tile_m = BM * CG;
   p.tiles_m = (p.M + p.tile_m - 1) / p.tile_m;
   p.tiles_n = (p.N + BN - 1) / BN;
@@ -591,7 +868,7 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  DPN_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, p));
+  DPN_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, tr, tx, p));
   return 0;
 }
 

@@ -77,7 +77,7 @@ def _s(stream) -> Optional[int]:
 def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batch1=1, batch2=1,
              a_s=(0, 0), b_s=(0, 0), c_s=(0, 0), bias=None, residual=None, ldr=None, r_s=None,
              aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, split_k=0,
-             cta_group=0, residual_mode=0, stream=None) -> None:
+             cta_group=0, residual_mode=0, epilogue=0, stream=None) -> None:
     """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules."""
     rs = (r_s if r_s is not None else c_s) if residual is not None else (0, 0)
     g = GemmArgs(M, N, K, batch1, batch2,
@@ -88,7 +88,7 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
                  None if residual is None else residual.data_ptr(),
                  (ldr if ldr is not None else ldc) if residual is not None else 0, rs[0], rs[1],
                  residual_mode, None if aux is None else aux.data_ptr(), alpha, gelu, block_n,
-                 split_k, cta_group)
+                 split_k, cta_group, epilogue)
     INSTR.launches += 1
     ev = INSTR.gemm_events
     if ev is not None:

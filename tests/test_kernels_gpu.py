@@ -44,7 +44,8 @@ def rnd(*shape, dtype=torch.bfloat16, scale=1.0):
                                            (77, 136, 40, 0, 0), (512, 768, 1024, 256, 2),
                                            (384, 1024, 512, 128, 2), (700, 520, 200, 256, 2),
                                            (200, 384, 64, 128, 2)])
-def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn, cg):
+@pytest.mark.parametrize("epi", [0, 1])
+def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn, cg, epi):
     k = K()
     A = rnd(M, K_)
     B = rnd(N, K_)
@@ -56,10 +57,52 @@ def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn, cg):
         pytest.skip("TMA needs 16-byte strides")
     C = torch.empty(M, (N + 7) // 8 * 8, device="cuda", dtype=torch.float32)
     k.gemm_raw(M=M, N=N, K=K_, A=As, lda=lda, a_mn=a_mn, B=Bs, ldb=ldb, b_mn=b_mn, Cout=C,
-               ldc=C.stride(0), block_n=bn, cta_group=cg)
+               ldc=C.stride(0), block_n=bn, cta_group=cg, epilogue=epi)
     torch.cuda.synchronize()
     ref = A.float() @ B.float().t()
     close(C[:, :N], ref, rel=5e-3)
+
+
+@pytest.mark.parametrize("mode", ["plain", "bias", "bias_res", "gelu_aux", "gelu_grad"])
+@pytest.mark.parametrize("M,N,K_,bn,cg", [(512, 384, 256, 0, 0), (300, 200, 96, 0, 0),
+                                           (77, 136, 40, 0, 0), (1024, 1024, 1024, 256, 2),
+                                           (384, 512, 128, 128, 1), (640, 320, 192, 128, 2)])
+@pytest.mark.parametrize("epi", [0, 1])
+def test_gemm_bf16_epilogues(mode, M, N, K_, bn, cg, epi):
+    """bf16 outputs through the TMA-staged epilogue (epi 0) and the direct-store
+    one (epi 1), with tails in M and N, every epilogue combination the executor uses."""
+    k = K()
+    A, B = rnd(M, K_), rnd(N, K_, scale=0.05)
+    ldc = (N + 7) // 8 * 8
+    bias, res = rnd(N), rnd(M, ldc)
+    out = torch.zeros(M, ldc, device="cuda", dtype=torch.bfloat16)
+    aux = torch.zeros_like(out)
+    kw = {}
+    pre = A.float() @ B.float().t()
+    if mode in ("bias", "bias_res", "gelu_aux"):
+        kw["bias"] = bias
+        pre = pre + bias.float()
+    if mode == "bias_res":
+        kw["residual"] = res
+        pre = pre + res[:, :N].float()
+    if mode == "gelu_aux":
+        kw.update(gelu=True, aux=aux)
+    if mode == "gelu_grad":
+        kw.update(residual=res, residual_mode=1)
+    k.gemm_raw(M=M, N=N, K=K_, A=A, lda=K_, B=B, ldb=K_, Cout=out, ldc=ldc, block_n=bn, cta_group=cg,
+               epilogue=epi, **kw)
+    torch.cuda.synchronize()
+    if mode == "gelu_aux":
+        close(aux[:, :N], pre)
+        close(out[:, :N], torch.nn.functional.gelu(pre, approximate="tanh"))
+    elif mode == "gelu_grad":
+        fr = res[:, :N].float().requires_grad_()
+        torch.nn.functional.gelu(fr, approximate="tanh").backward(pre)
+        close(out[:, :N], fr.grad)
+    else:
+        close(out[:, :N], pre)
+    if ldc > N:  # pad columns untouched
+        assert torch.all(out[:, N:] == 0)
 
 
 def test_gemm_epilogue_bias_residual_gelu_aux():
@@ -268,7 +311,8 @@ def test_adamw():
 
 @pytest.mark.parametrize("split", [2, 3, 0])
 @pytest.mark.parametrize("accumulate", [False, True])
-def test_gemm_split_k_wgrad(split, accumulate):
+@pytest.mark.parametrize("epi", [0, 1])
+def test_gemm_split_k_wgrad(split, accumulate, epi):
     """Split-K partials reduced with red.add.f32 (wgrad shapes with few tiles)."""
     k = K()
     M, N, Kd = 256, 384, 1000
@@ -276,7 +320,7 @@ def test_gemm_split_k_wgrad(split, accumulate):
     dw = torch.randn(M, N, device="cuda")
     base = dw.clone()
     k.gemm_raw(M=M, N=N, K=Kd, A=dy, lda=M, a_mn=True, B=x, ldb=N, b_mn=True, Cout=dw, ldc=N,
-               accumulate=accumulate, split_k=split)
+               accumulate=accumulate, split_k=split, epilogue=epi)
     torch.cuda.synchronize()
     ref = dy.float().t() @ x.float() + (base if accumulate else 0)
     close(dw, ref, rel=5e-3)
