@@ -129,6 +129,40 @@ int dpn_embed_bwd(const int32_t* ids, const void* dout, float* dtok, float* dpos
 int dpn_adamw(float* w, float* m, float* v, const float* g, void* out_bf16, int64_t n, float lr,
               float beta1, float beta2, float eps, float weight_decay, int64_t step, void* stream);
 
+/* ---- CNN nodes (AmoebaNet-D; synth.py:123-135 conv / act / pool vocabulary) ----
+ * Activations are NHWC bf16 viewed as [pixels, C], C % 8 == 0.  3x3 windows
+ * use pad 1; output size (H-1)/stride+1.  Dense 1x1 convolutions are dpn_gemm. */
+int dpn_relu_fwd(const void* x, void* y, int64_t n, void* stream);
+int dpn_relu_bwd(const void* dy, const void* y, void* dx, int64_t n, void* stream);
+/* depthwise 3x3, w: [C, 9] bf16; backward: dx (if non-NULL) and dw += (f32, if non-NULL) */
+int dpn_dwconv3_fwd(const void* x, const void* w, void* y, int64_t b, int64_t H, int64_t W,
+                    int64_t C, int64_t stride, void* stream);
+int dpn_dwconv3_bwd(const void* x, const void* w, const void* dy, void* dx, float* dw, int64_t b,
+                    int64_t H, int64_t W, int64_t C, int64_t stride, void* stream);
+/* training-mode batch norm over P pixels; stats: [2, C] f32 (sum, sum of squares),
+ * written by the forward and read by the backward.  Backward: dx, dgamma/dbeta +=
+ * (f32); workspace >= 2*C floats. */
+int dpn_bn_fwd(const void* x, const void* gamma, const void* beta, void* y, float* stats,
+               int64_t P, int64_t C, float eps, void* stream);
+int dpn_bn_bwd(const void* dy, const void* x, const float* stats, const void* gamma, void* dx,
+               float* dgamma, float* dbeta, float* workspace, int64_t P, int64_t C, float eps,
+               void* stream);
+/* 3x3 pooling, mode 0 max (argmax: uint8 tap per output element), 1 average
+ * (padding excluded from the count). */
+int dpn_pool3_fwd(const void* x, void* y, void* argmax, int64_t b, int64_t H, int64_t W, int64_t C,
+                  int64_t stride, int mode, void* stream);
+int dpn_pool3_bwd(const void* dy, const void* argmax, void* dx, int64_t b, int64_t H, int64_t W,
+                  int64_t C, int64_t stride, int mode, void* stream);
+/* dst[r, :cols] (+)= src[r, :cols] with row strides lds / ldd (channel concat) */
+int dpn_copy_cols(const void* src, int64_t lds, void* dst, int64_t ldd, int64_t rows, int64_t cols,
+                  int accumulate, void* stream);
+/* stem: cols[p, (r*3+s)*C + c] = x[n, ho*stride-1+r, wo*stride-1+s, c] (zero outside) */
+int dpn_im2col3(const void* x, void* cols, int64_t b, int64_t H, int64_t W, int64_t C,
+                int64_t stride, void* stream);
+/* head: y[n, c] = mean over the HW pixels of sample n; backward spreads dy / HW */
+int dpn_gap_fwd(const void* x, void* y, int64_t b, int64_t HW, int64_t C, void* stream);
+int dpn_gap_bwd(const void* dy, void* dx, int64_t b, int64_t HW, int64_t C, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,18 @@ SIGNATURES = {
     "dpn_embed_fwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_embed_bwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_adamw": [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _f32, _i64, _vp],
+    "dpn_relu_fwd": [_vp, _vp, _i64, _vp],
+    "dpn_relu_bwd": [_vp, _vp, _vp, _i64, _vp],
+    "dpn_dwconv3_fwd": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
+    "dpn_dwconv3_bwd": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
+    "dpn_bn_fwd": [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp],
+    "dpn_bn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp],
+    "dpn_pool3_fwd": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp],
+    "dpn_pool3_bwd": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, C.c_int, _vp],
+    "dpn_copy_cols": [_vp, _i64, _vp, _i64, _i64, _i64, C.c_int, _vp],
+    "dpn_im2col3": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp],
+    "dpn_gap_fwd": [_vp, _vp, _i64, _i64, _i64, _vp],
+    "dpn_gap_bwd": [_vp, _vp, _i64, _i64, _i64, _vp],
 }
 
 _lock = threading.Lock()

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 SO = PKG / "_dawnpiper.so"
-SOURCES = ["runtime.cu", "gemm.cu", "kernels.cu", "attention.cu"]
+SOURCES = ["runtime.cu", "gemm.cu", "kernels.cu", "attention.cu", "cnn.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

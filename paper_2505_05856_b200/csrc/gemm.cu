@@ -804,8 +804,9 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
   GemmParams p = p0;
   CUtensorMap tc{}, tr{}, tx{};
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  // the side staging tile holds either the residual or the aux output, not both
   p.tma_epi = g->batch1 * g->batch2 == 1 && (!p.res || (al16(p.res) && p.ldr % 8 == 0)) &&
-              (!p.aux || al16(p.aux)) && g->epilogue != 1;
+              (!p.aux || al16(p.aux)) && !(p.res && p.aux && p.gelu) && g->epilogue != 1;
   if (p.tma_epi) {
     rc = make_epi_map(&tc, g->C, g->M, g->N, g->ldc, p.c_f32 != 0);
     if (!rc && p.res) rc = make_epi_map(&tr, p.res, g->M, g->N, p.ldr, false);

@@ -260,3 +260,78 @@ def copy_d2d(dst, src, nbytes=None, dst_dev=0, src_dev=0, stream=None):
     n = nbytes if nbytes is not None else src.numel() * src.element_size()
     check(lib().dpn_p2p_copy(dst.data_ptr(), dst_dev, src.data_ptr(), src_dev, n, _s(stream)),
           "dpn_p2p_copy")
+
+
+# ---- CNN nodes (AmoebaNet-D) --------------------------------------------------------
+
+
+def relu_fwd(x, y, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_relu_fwd(x.data_ptr(), y.data_ptr(), x.numel(), _s(stream)), "dpn_relu_fwd")
+
+
+def relu_bwd(dy, y, dx, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_relu_bwd(dy.data_ptr(), y.data_ptr(), dx.data_ptr(), dy.numel(), _s(stream)),
+          "dpn_relu_bwd")
+
+
+def dwconv3_fwd(x, w, y, b, H, W, C, stride, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_dwconv3_fwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), b, H, W, C, stride,
+                                _s(stream)), "dpn_dwconv3_fwd")
+
+
+def dwconv3_bwd(x, w, dy, dx, dw, b, H, W, C, stride, stream=None):
+    INSTR.launches += (dx is not None) + (dw is not None)
+    check(lib().dpn_dwconv3_bwd(x.data_ptr(), w.data_ptr(), dy.data_ptr(), _p(dx), _p(dw), b, H, W, C,
+                                stride, _s(stream)), "dpn_dwconv3_bwd")
+
+
+def bn_fwd(x, gamma, beta, y, stats, eps=1e-5, stream=None):
+    P, C_ = x.shape
+    INSTR.launches += 2
+    check(lib().dpn_bn_fwd(x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(),
+                           stats.data_ptr(), P, C_, eps, _s(stream)), "dpn_bn_fwd")
+
+
+def bn_bwd(dy, x, stats, gamma, dx, dgamma, dbeta, workspace, eps=1e-5, stream=None):
+    P, C_ = x.shape
+    INSTR.launches += 2
+    check(lib().dpn_bn_bwd(dy.data_ptr(), x.data_ptr(), stats.data_ptr(), gamma.data_ptr(),
+                           dx.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(), workspace.data_ptr(),
+                           P, C_, eps, _s(stream)), "dpn_bn_bwd")
+
+
+def pool3_fwd(x, y, argmax, b, H, W, C, stride, mode, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_pool3_fwd(x.data_ptr(), y.data_ptr(), _p(argmax), b, H, W, C, stride, mode,
+                              _s(stream)), "dpn_pool3_fwd")
+
+
+def pool3_bwd(dy, argmax, dx, b, H, W, C, stride, mode, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_pool3_bwd(dy.data_ptr(), _p(argmax), dx.data_ptr(), b, H, W, C, stride, mode,
+                              _s(stream)), "dpn_pool3_bwd")
+
+
+def copy_cols(src, lds, dst, ldd, rows, cols, accumulate=False, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_copy_cols(src.data_ptr(), lds, dst.data_ptr(), ldd, rows, cols, int(accumulate),
+                              _s(stream)), "dpn_copy_cols")
+
+
+def im2col3(x, cols, b, H, W, C, stride, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_im2col3(x.data_ptr(), cols.data_ptr(), b, H, W, C, stride, _s(stream)),
+          "dpn_im2col3")
+
+
+def gap_fwd(x, y, b, HW, C, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_gap_fwd(x.data_ptr(), y.data_ptr(), b, HW, C, _s(stream)), "dpn_gap_fwd")
+
+
+def gap_bwd(dy, dx, b, HW, C, stream=None):
+    INSTR.launches += 1
+    check(lib().dpn_gap_bwd(dy.data_ptr(), dx.data_ptr(), b, HW, C, _s(stream)), "dpn_gap_bwd")
