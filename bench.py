@@ -129,10 +129,8 @@ def cpu_port_sample(model_name: str, stages: int, samples: int = 1):
     nodes = [n.id for n in build_nodes(cfg)]
     per = (len(nodes) + stages - 1) // stages
     stage_nodes = [nodes[i:i + per] for i in range(0, len(nodes), per)]
-    dims = dict(layers=cfg.layers, hidden=cfg.hidden, heads=cfg.heads, seq=cfg.seq,
-                vocab=cfg.vocab, causal=cfg.causal, ln_eps=cfg.ln_eps,
-                fused_attention=cfg.fused_attention, dec_layers=cfg.dec_layers,
-                tgt_seq=cfg.tgt_seq)
+    from oracle.train_ref import dims_from
+    dims = dims_from(cfg, build_nodes(cfg))
     init = init_params(cfg, 0)
     ids, labels = synthetic_batch(cfg, 1, samples, seed=0)
     opt = dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)

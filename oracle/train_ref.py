@@ -20,6 +20,12 @@ numerics to; this restatement fixes the semantics instead:
     kv = E Wkv^T + bkv; ctx = softmax(q k^T / sqrt(d)) v; y2 = ctx Wo^T + bo + y;
     then the FFN sub-block; lnf / head over the target tokens.  ids per
     micro-batch are the b*s source ids followed by the b*t target ids;
+  * CNN (AmoebaNet-D config): the node structure (kind, inputs, geometry) is
+    given as data in dims["graph"]; each kind's math is restated here with
+    torch.nn.functional on NCHW fp32 tensors -- stem 3x3 convolution,
+    training-mode batch norm (biased variance), ReLU, 1x1 convolution,
+    depthwise 3x3 convolution, 3x3 max / average pooling (average excludes
+    padding), add, channel concat, global average pool, FC + cross entropy;
   * schedule: per stage x of l, the 1F1B op list of simulate.py:211-222
     (restated below as `one_f_one_b`);
   * weight stashing (PipeDream): a forward uses the stage's newest weights and
@@ -67,6 +73,8 @@ def node_ids(layers: int, fused: bool = True) -> List[str]:
 
 
 def _inputs(nid: str, d: dict) -> Tuple[str, ...]:
+    if "graph" in d:
+        return tuple(d["graph"][nid][1])
     layers, dec = d["layers"], d.get("dec_layers", 0)
     fused = d.get("fused_attention", True)
     if nid in ("embed", "dembed"):
@@ -123,9 +131,55 @@ class RefStage:
         self.sync_m = sync_m  # > 0: GPipe, accumulate over sync_m micro-batches
         self.gacc = {k: torch.zeros_like(v) for k, v in self.params.items()}
 
+    def _cnn_node(self, nid: str, env, W, images, labels) -> torch.Tensor:
+        d = self.d
+        kind, inputs, a = d["graph"][nid]
+        ins = [env[u] for u in inputs]
+        w = lambda pn: W[f"{nid}.{pn}"]
+        b = labels.numel()
+
+        def nchw(t, H, Wd):
+            return t.reshape(b, H, Wd, -1).permute(0, 3, 1, 2)
+
+        def flat(t):
+            return t.permute(0, 2, 3, 1).reshape(-1, t.shape[1])
+
+        if kind == "stem":
+            x = nchw(images.float(), a["H"], a["W"])
+            wt = w("weight").reshape(a["C"], 3, 3, a["Cin"]).permute(0, 3, 1, 2)
+            return flat(F.conv2d(x, wt, stride=a["stride"], padding=1))
+        if kind == "bn":
+            return F.batch_norm(ins[0], None, None, w("gamma"), w("beta"), training=True,
+                                eps=d["ln_eps"])
+        if kind == "relu":
+            return torch.relu(ins[0])
+        if kind == "pw":
+            return ins[0] @ w("weight").t()
+        if kind == "dw":
+            x = nchw(ins[0], a["H"], a["W"])
+            return flat(F.conv2d(x, w("weight").reshape(a["C"], 1, 3, 3), stride=a["stride"],
+                                 padding=1, groups=a["C"]))
+        if kind == "pool":
+            x = nchw(ins[0], a["H"], a["W"])
+            if a["mode"] == 0:
+                return flat(F.max_pool2d(x, 3, a["stride"], 1))
+            return flat(F.avg_pool2d(x, 3, a["stride"], 1, count_include_pad=False))
+        if kind == "add":
+            return ins[0] + ins[1]
+        if kind == "concat":
+            return torch.cat(ins, 1)
+        if kind == "gap":
+            return ins[0].reshape(b, a["H"] * a["W"], -1).mean(1)
+        if kind == "head":
+            logits = ins[0] @ w("weight")[:d["vocab"]].t()
+            return F.cross_entropy(logits, labels.long())
+        raise ValueError(kind)
+
     def _node(self, nid: str, env: Dict[str, torch.Tensor], W: Dict[str, torch.Tensor],
               ids, labels) -> torch.Tensor:
         d = self.d
+        if "graph" in d:
+            return self._cnn_node(nid, env, W, ids, labels)
         H, A, s = d["hidden"], d["heads"], d["seq"]
         hd = H // A
         kind = nid.split(".")[-1] if "." in nid else nid
@@ -288,3 +342,14 @@ def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor
     for s in stages:
         final.update({k: v.detach().clone() for k, v in s.params.items()})
     return all_losses, final
+
+
+def dims_from(cfg, nodes=None) -> dict:
+    """The oracle's model description from a config object (attributes only) and,
+    for CNN configs, the node structure (kind, inputs, geometry) as plain data."""
+    d = dict(layers=cfg.layers, hidden=cfg.hidden, heads=cfg.heads, seq=cfg.seq, vocab=cfg.vocab,
+             causal=cfg.causal, ln_eps=cfg.ln_eps, fused_attention=cfg.fused_attention,
+             dec_layers=cfg.dec_layers, tgt_seq=cfg.tgt_seq)
+    if getattr(cfg, "family", "transformer") == "cnn":
+        d["graph"] = {n.id: (n.kind, tuple(n.inputs), dict(n.attrs)) for n in nodes}
+    return d

@@ -17,6 +17,8 @@ from __future__ import annotations
 
 from typing import Dict, List, Optional, Tuple
 
+import torch
+
 from ..planner.profile import ComputationGraph, ProfiledNode, TensorRef
 from .model import (NodeDef, TransformerConfig, backward_readers, build_nodes, has_stats,
                     internal_specs, node_rows, output_spec, saved_for_backward, stats_bytes)
@@ -26,7 +28,7 @@ def tensor_bytes(shape, dtype) -> int:
     n = 1
     for s in shape:
         n *= s
-    return n * (2 if str(dtype).endswith("bfloat16") else 4)
+    return n * torch.empty((), dtype=dtype).element_size()
 
 
 def out_tid(node_id: str) -> str:
@@ -62,11 +64,11 @@ def analytic_times(cfg: TransformerConfig, b: int, tflops: float = 900.0,
         shape, dt = output_spec(cfg, n, b)
         byt = tensor_bytes(shape, dt)
         fl = 0
-        if n.kind in ("linear", "linear_res"):
+        if n.kind in ("linear", "linear_res", "head", "pw", "stem"):
             w = dict(n.params)["weight"]
             fl = 2 * M * w[0] * w[1]
-        elif n.kind == "head":
-            fl = 2 * M * cfg.vocab_padded * H
+        elif n.kind == "dw":
+            fl = 2 * M * shape[1] * 9
         elif n.kind in ("score", "attn"):
             fl = 2 * b * cfg.heads * s * s * cfg.head_dim
         elif n.kind == "attn_fused":

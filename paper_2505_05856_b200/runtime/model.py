@@ -72,6 +72,12 @@ class TransformerConfig:
     def head_dim(self) -> int:
         return self.hidden // self.heads
 
+    family = "transformer"
+
+    def input_spec(self, b: int):
+        """Per-micro-batch input buffer: token ids int32 [b * in_tokens]."""
+        return (b * self.in_tokens,), torch.int32
+
     @property
     def vocab_padded(self) -> int:
         # logits/head rows padded to a multiple of 64: 16-byte TMA strides and
@@ -130,6 +136,7 @@ class NodeDef:
     layer: int = -1
     seq: int = 0          # token rows per sample of this node's output
     causal: bool = False  # attention nodes: causal mask
+    attrs: Tuple[Tuple[str, int], ...] = ()  # CNN nodes: spatial geometry (runtime/cnn.py)
 
 
 def _ln(nid: str, x: str, H: int, layer: int, seq: int) -> NodeDef:
@@ -182,7 +189,14 @@ def canonical_order(nodes: List[NodeDef]) -> List[NodeDef]:
     return sorted(nodes, key=lambda n: depth[n.id])
 
 
+def _cnn(cfg) -> bool:
+    return getattr(cfg, "family", "transformer") == "cnn"
+
+
 def build_nodes(cfg: TransformerConfig) -> List[NodeDef]:
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.build_nodes(cfg)
     H, Vp, S = cfg.hidden, cfg.vocab_padded, cfg.seq
     nodes = [NodeDef("embed", "embed", (), (("tok", (cfg.vocab, H)), ("pos", (S, H))), -1, S)]
     x = "embed"
@@ -204,11 +218,17 @@ def build_nodes(cfg: TransformerConfig) -> List[NodeDef]:
 
 
 def node_rows(cfg: TransformerConfig, node: NodeDef, b: int) -> int:
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.node_rows(cfg, node, b)
     return b * (node.seq or cfg.seq)
 
 
 def output_spec(cfg: TransformerConfig, node: NodeDef, b: int) -> Tuple[Tuple[int, ...], torch.dtype]:
     """Shape/dtype of a node's forward output for micro-batch size b."""
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.output_spec(cfg, node, b)
     M, H = node_rows(cfg, node, b), cfg.hidden
     k = node.kind
     if k in ("embed", "ln", "attn", "attn_fused", "linear_res", "add", "xattn"):
@@ -227,7 +247,11 @@ def output_spec(cfg: TransformerConfig, node: NodeDef, b: int) -> Tuple[Tuple[in
 
 def internal_specs(cfg: TransformerConfig, node: NodeDef, b: int):
     """Tensors a node saves for its own backward besides its output and
-    statistics: the cross-attention's q [b*t, H], kv [b*s, 2H] and P [b, A, t, s]."""
+    statistics: the cross-attention's q [b*t, H], kv [b*s, 2H] and P [b, A, t, s];
+    max pooling's argmax taps."""
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.internal_specs(cfg, node, b)
     if node.kind != "xattn":
         return {}
     t, s, H = node.seq, cfg.seq, cfg.hidden
@@ -237,7 +261,11 @@ def internal_specs(cfg: TransformerConfig, node: NodeDef, b: int):
 
 def stats_bytes(cfg: TransformerConfig, node: NodeDef, b: int) -> int:
     """Side statistics saved next to the output: LayerNorm (mean, rstd) per row,
-    fused attention's log-sum-exp per (batch, head, query); fp32."""
+    fused attention's log-sum-exp per (batch, head, query); batch-norm column
+    sums (sum, sum of squares); fp32."""
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.stats_bytes(cfg, node, b)
     if node.kind == "ln":
         return 8 * node_rows(cfg, node, b)
     if node.kind == "attn_fused":
@@ -246,7 +274,7 @@ def stats_bytes(cfg: TransformerConfig, node: NodeDef, b: int) -> int:
 
 
 def has_stats(node: NodeDef) -> bool:
-    return node.kind in ("ln", "attn_fused")
+    return node.kind in ("ln", "attn_fused", "bn")
 
 
 def saved_for_backward(node: NodeDef) -> bool:
@@ -278,11 +306,20 @@ def backward_readers(nodes: List[NodeDef]) -> Dict[str, List[str]]:
             readers[n.inputs[0]].append(n.id)         # c for the q-projection wgrad
             readers[n.inputs[1]].append(n.id)         # E for the kv-projection wgrad
             # (q, kv and P are internal tensors of the node itself)
+        elif n.kind in ("bn", "pw", "dw"):
+            readers[n.inputs[0]].append(n.id)         # x for BN's xhat / the weight gradients
+        elif n.kind == "relu":
+            readers[n.id].append(n.id)                # mask from the saved output
+        # stem (reads the input images), pool (max: own argmax), add, concat,
+        # gap: no saved activations
     # (LayerNorm statistics are a separate tensor, read only by their own node)
     return readers
 
 
 def param_shapes(cfg: TransformerConfig) -> List[Tuple[str, Tuple[int, ...]]]:
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.param_shapes(cfg)
     return [(f"{n.id}.{pn}", shp) for n in build_nodes(cfg) for pn, shp in n.params]
 
 
@@ -290,6 +327,9 @@ def init_params(cfg: TransformerConfig, seed: int = 0) -> Dict[str, torch.Tensor
     """Deterministic fp32 CPU initialisation shared by the B200 run and the
     CPU oracle: N(0, 0.02) matrices/embeddings, zero biases, LN (1, 0);
     head pad rows zero."""
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.init_params(cfg, seed)
     g = torch.Generator().manual_seed(seed)
     out: Dict[str, torch.Tensor] = {}
     for name, shp in param_shapes(cfg):
@@ -310,6 +350,9 @@ def synthetic_batch(cfg: TransformerConfig, micro_batches: int, b: int, seed: in
     """Token ids int32 [m, b*in_tokens] (encoder-decoder: the b*s source ids,
     then the b*t target ids) and labels int32 [m, b*out_tokens], uniform over
     the vocabulary."""
+    if _cnn(cfg):
+        from . import cnn
+        return cnn.synthetic_batch(cfg, micro_batches, b, seed)
     g = torch.Generator().manual_seed(seed + 1)
     ids = torch.randint(0, cfg.vocab, (micro_batches, b * cfg.in_tokens), generator=g,
                         dtype=torch.int64)
@@ -325,3 +368,8 @@ class AdamWConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     weight_decay: float = 0.01
+
+
+from .cnn import CNN_PRESETS, CNNConfig  # noqa: E402  (cnn.py imports NodeDef from here)
+
+PRESETS.update(CNN_PRESETS)

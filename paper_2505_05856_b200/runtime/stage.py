@@ -70,7 +70,7 @@ class FlatParams:
         for n in nodes:
             for pn, shp in n.params:
                 name = f"{n.id}.{pn}"
-                is_dense = ((n.kind in ("linear", "linear_res", "head") and pn == "weight")
+                is_dense = ((n.kind in ("linear", "linear_res", "head", "pw", "stem") and pn == "weight")
                             or (n.kind == "xattn" and pn in ("q_weight", "kv_weight")))
                 (dense if is_dense else accum).append((name, tuple(shp)))
         self.slots: Dict[str, ParamSlot] = {}
@@ -191,7 +191,11 @@ class StageExecutor:
         self.is_first = lo == 0
         # stages holding an embedding node take the micro-batch's token ids
         # (encoder-decoder: `dembed` may sit behind a cut at position 0)
-        self.needs_ids = any(n.kind == "embed" for n in self.nodes)
+        self.needs_ids = any(n.kind in ("embed", "stem") for n in self.nodes)
+        self.cnn = getattr(cfg, "family", "transformer") == "cnn"
+        # gradient buffers shared by the two inputs of an `add` (CNN graphs copy
+        # one on the first in-place accumulation into it)
+        self.shared_grads: Set[str] = set()
         self.is_last = hi == len(self.all_nodes) - 1
         self.node_by_id = {n.id: n for n in self.all_nodes}
         self.index = {n.id: i for i, n in enumerate(self.all_nodes)}
@@ -245,8 +249,8 @@ class StageExecutor:
             else:
                 self.work[tid] = torch.empty(shape, dtype=dt, device=device)
         if self.needs_ids:
-            self.ids = [torch.empty(self.in_rows, dtype=torch.int32, device=device)
-                        for _ in range(self.w)]
+            ishape, idt = cfg.input_spec(micro_batch)
+            self.ids = [torch.empty(ishape, dtype=idt, device=device) for _ in range(self.w)]
         if self.is_last:
             self.labels = [torch.empty(self.out_rows, dtype=torch.int32, device=device)
                            for _ in range(self.w)]
@@ -343,6 +347,8 @@ class StageExecutor:
         nid, kind = tid.rsplit(".", 1)
         node = self.node_by_id[nid]
         if kind == "stats":
+            if node.kind == "bn":
+                return (2, dict(node.attrs)["C"]), F32
             if node.kind == "attn_fused":
                 return (self.b, self.cfg.heads, node.seq or self.cfg.seq), F32
             return (2, node_rows(self.cfg, node, self.b)), F32
@@ -523,8 +529,118 @@ class StageExecutor:
             loss = (loss_out if loss_out is not None else self.loss) if phase == "fwd" else self._scratch_loss()
             K.xent(out, self.labels[slot], cfg.vocab, self.grad_scale, loss, out,
                    loss_scale=1.0 / self.out_rows, stream=st)
+        elif self.cnn:
+            self._cnn_fwd(n, inp, out, slot, phase, W)
         else:
             raise ValueError(k)
+
+    # ---- CNN nodes (runtime/cnn.py) -------------------------------------------------
+
+    def _stem_cols(self, n: NodeDef, slot: int) -> torch.Tensor:
+        a, b = dict(n.attrs), self.b
+        cols = torch.empty(b * a["Ho"] * a["Wo"], 9 * a["Cin"], dtype=BF16, device=self.device)
+        K.im2col3(self.ids[slot], cols, b, a["H"], a["W"], a["Cin"], a["stride"], stream=self.stream)
+        return cols
+
+    def _cnn_fwd(self, n: NodeDef, inp, out, slot: int, phase: str, W) -> None:
+        st, b, k = self.stream, self.b, n.kind
+        a = dict(n.attrs)
+        if k == "stem":
+            K.linear_fwd(self._stem_cols(n, slot), W("weight"), out, stream=st)
+        elif k == "bn":
+            K.bn_fwd(inp[0], W("gamma"), W("beta"), out, self.buf(stats_tid(n.id), slot, phase),
+                     self.cfg.bn_eps, stream=st)
+        elif k == "relu":
+            K.relu_fwd(inp[0], out, stream=st)
+        elif k == "pw":
+            K.linear_fwd(inp[0], W("weight"), out, stream=st)
+        elif k == "dw":
+            K.dwconv3_fwd(inp[0], W("weight"), out, b, a["H"], a["W"], a["C"], a["stride"], stream=st)
+        elif k == "pool":
+            arg = self.buf(internal_tid(n.id, "arg"), slot, phase) if a["mode"] == 0 else None
+            K.pool3_fwd(inp[0], out, arg, b, a["H"], a["W"], a["C"], a["stride"], a["mode"], stream=st)
+        elif k == "concat":
+            off, P = 0, out.shape[0]
+            for x in inp:
+                K.copy_cols(x, x.shape[1], out[:, off:], out.shape[1], P, x.shape[1], stream=st)
+                off += x.shape[1]
+        elif k == "gap":
+            K.gap_fwd(inp[0], out, b, a["H"] * a["W"], a["C"], stream=st)
+        else:
+            raise ValueError(k)
+
+    def _own(self, tid: str) -> torch.Tensor:
+        """grads[tid] for an in-place update: a buffer still shared with another
+        tensor's gradient is copied first."""
+        if tid in self.shared_grads:
+            self.grads[tid] = self.grads[tid].clone()
+            self.shared_grads.discard(tid)
+        return self.grads[tid]
+
+    def _dx_target(self, x_t: str):
+        """Where a node writes its contribution to x_t's gradient: the gradient
+        buffer itself on first contribution, else a temporary to be added."""
+        if x_t not in self.grad_init:
+            buf = self.grad_buffer(x_t)
+            self.grad_init.add(x_t)
+            return buf, False
+        return self.grad_like(x_t), True
+
+    def _dx_done(self, x_t: str, t: torch.Tensor, pending: bool) -> None:
+        if pending:
+            dst = self._own(x_t)
+            K.add(dst, t, dst, stream=self.stream)
+
+    def _cnn_bwd(self, n: NodeDef, dy, slot: int, W, G) -> None:
+        st, b, k = self.stream, self.b, n.kind
+        a = dict(n.attrs)
+        if k == "stem":  # the images need no gradient: weight gradient only
+            K.linear_wgrad(dy, self._stem_cols(n, slot), G("weight"), accumulate=self._wgrad_acc,
+                           stream=st)
+            return
+        if k == "concat":
+            off = 0
+            for u in n.inputs:
+                t = out_tid(u)
+                C = self._spec(t)[0][1]
+                if t not in self.grad_init:
+                    dst = self.grad_buffer(t)
+                    self.grad_init.add(t)
+                    K.copy_cols(dy[:, off:], dy.shape[1], dst, C, dy.shape[0], C, stream=st)
+                else:
+                    K.copy_cols(dy[:, off:], dy.shape[1], self._own(t), C, dy.shape[0], C,
+                                accumulate=True, stream=st)
+                off += C
+            return
+        x_t = out_tid(n.inputs[0])
+        if k == "pw":
+            x = self.buf(x_t, slot, "bwd")
+            if x_t in self.grad_init:
+                dx = self._own(x_t)
+                K.linear_dgrad(dy, W("weight"), dx, accumulate_into=dx, stream=st)
+            else:
+                K.linear_dgrad(dy, W("weight"), self.grad_buffer(x_t), stream=st)
+                self.grad_init.add(x_t)
+            K.linear_wgrad(dy, x, G("weight"), accumulate=self._wgrad_acc, stream=st)
+            return
+        dx, pending = self._dx_target(x_t)
+        if k == "bn":
+            ws = torch.empty(2 * a["C"], dtype=F32, device=self.device)
+            K.bn_bwd(dy, self.buf(x_t, slot, "bwd"), self.buf(stats_tid(n.id), slot, "bwd"),
+                     W("gamma"), dx, G("gamma"), G("beta"), ws, self.cfg.bn_eps, stream=st)
+        elif k == "relu":
+            K.relu_bwd(dy, self.buf(out_tid(n.id), slot, "bwd"), dx, stream=st)
+        elif k == "dw":
+            K.dwconv3_bwd(self.buf(x_t, slot, "bwd"), W("weight"), dy, dx, G("weight"), b, a["H"],
+                          a["W"], a["C"], a["stride"], stream=st)
+        elif k == "pool":
+            arg = self.buf(internal_tid(n.id, "arg"), slot, "bwd") if a["mode"] == 0 else None
+            K.pool3_bwd(dy, arg, dx, b, a["H"], a["W"], a["C"], a["stride"], a["mode"], stream=st)
+        elif k == "gap":
+            K.gap_bwd(dy, dx, b, a["H"] * a["W"], a["C"], stream=st)
+        else:
+            raise ValueError(k)
+        self._dx_done(x_t, dx, pending)
 
     def _scratch_loss(self):
         if not hasattr(self, "_sl"):
@@ -625,8 +741,10 @@ class StageExecutor:
         if tid not in self.grad_init:
             self.grads[tid] = src
             self.grad_init.add(tid)
+            if self.cnn:
+                self.shared_grads.add(tid)
         else:
-            dst = self.grads[tid]
+            dst = self._own(tid) if self.cnn else self.grads[tid]
             K.add(dst, src, dst, stream=self.stream)
 
     def backward(self, mb: int) -> Dict[str, torch.Tensor]:
@@ -705,6 +823,7 @@ class StageExecutor:
         self.grads = {}
         self.grad_init = set()
         self._skip_bwd = set()
+        self.shared_grads = set()
 
     def optimizer_step(self) -> None:
         """Sync schedule: one AdamW step over the gradients accumulated by the
@@ -840,5 +959,7 @@ class StageExecutor:
                        b_mn=True, b_s=(d, s * 3 * H), batch1=A, batch2=b, Cout=dqkv[:, H:],
                        ldc=3 * H, c_s=(d, s * 3 * H), stream=st)
             self.grad_init.add(qkv_t)
+        elif self.cnn:
+            self._cnn_bwd(n, dy, slot, W, G)
         else:
             raise ValueError(k)

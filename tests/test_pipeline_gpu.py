@@ -49,10 +49,8 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
 
     nodes = [n.id for n in build_nodes(cfg)]
     stage_nodes = [nodes[lo:hi + 1] for lo, hi in stage_bounds(plan.cuts, len(g))]
-    dims = dict(layers=cfg.layers, hidden=cfg.hidden, heads=cfg.heads, seq=cfg.seq,
-                vocab=cfg.vocab, causal=cfg.causal, ln_eps=cfg.ln_eps,
-                fused_attention=cfg.fused_attention, dec_layers=cfg.dec_layers,
-                tgt_seq=cfg.tgt_seq)
+    from oracle.train_ref import dims_from
+    dims = dims_from(cfg, build_nodes(cfg))
     init = init_params(cfg, 0)
     ref_losses, ref_params = reference_train(
         dims, init, ids, labels, stage_nodes,
@@ -158,3 +156,19 @@ def test_pipeline_t5_memopt_and_sync():
     _compare(cfg, g, plan)
     cfg, g, plan = _setup("tiny-t5", 2, 4.0, 16 << 30, schedule="sync")
     _compare(cfg, g, plan)
+
+
+@pytest.mark.parametrize("stages", [1, 2, 4])
+def test_pipeline_amoebanet(stages):
+    """AmoebaNet-D-style CNN (BASELINE configs[4] at tiny size): stem conv, BN,
+    depthwise-separable convolutions, pooling, concat cells with skip inputs."""
+    cfg, g, plan = _setup("tiny-amoeba", stages, 4.0, 16 << 30, b=4)
+    _compare(cfg, g, plan, b=4, m=6)
+
+
+def test_pipeline_amoebanet_memopt_and_sync():
+    cfg, g, plan = _setup("tiny-amoeba", 3, 0.6, 16 << 30, b=4)
+    assert any(m.actions for m in plan.memopt)
+    _compare(cfg, g, plan, b=4, m=6)
+    cfg, g, plan = _setup("tiny-amoeba", 2, 4.0, 16 << 30, b=4, schedule="sync")
+    _compare(cfg, g, plan, b=4, m=4)

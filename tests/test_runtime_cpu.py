@@ -124,3 +124,43 @@ def test_oracle_encdec_is_partition_invariant(schedule):
     if schedule == "sync":  # one update after all micro-batches: every loss is pre-update
         for a, b in zip(one[0], three[0]):
             assert abs(a - b) < 1e-5
+
+
+@pytest.mark.parametrize("name", ["tiny-amoeba", "amoebanet-d"])
+def test_cnn_profile_graph(name, tmp_path):
+    """AmoebaNet-D: valid schema-1 profile in canonical order, cells with skip
+    inputs, BN statistics and max-pool argmax saved by their nodes."""
+    cfg = PRESETS[name]
+    g = profile_graph(cfg, 4)
+    assert [n.id for n in g.nodes] == [n.id for n in build_nodes(cfg)]
+    P.save_profile(g, tmp_path / "p.json")
+    assert P.canonical_hash(P.load_profile(tmp_path / "p.json")) == P.canonical_hash(g)
+    kinds = {n.kind for n in build_nodes(cfg)}
+    assert {"stem", "bn", "relu", "pw", "dw", "pool", "add", "concat", "gap", "head"} <= kinds
+    ids = [n.id for n in g.nodes]
+    bn = g.nodes[ids.index("stem.bn")]
+    assert "stem.bn.stats" in {t.id for t in bn.saved}
+    if name == "amoebanet-d":
+        assert 25e6 < cfg.n_params() < 30e6          # ~28M (PAPER.md:494)
+        assert sum(t.numel() for t in init_params(cfg, 0).values()) == cfg.n_params()
+
+
+def test_oracle_cnn_is_partition_invariant():
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from oracle.train_ref import dims_from, reference_train
+    from paper_2505_05856_b200.runtime.model import synthetic_batch
+    cfg = PRESETS["tiny-amoeba"]
+    nodes = build_nodes(cfg)
+    ids = [n.id for n in nodes]
+    x, labels = synthetic_batch(cfg, 2, 2, seed=0)
+    opt = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    d = dims_from(cfg, nodes)
+    init = init_params(cfg, 0)
+    one, _ = reference_train(d, init, x, labels, [ids], opt)
+    k = len(ids) // 3
+    three, _ = reference_train(d, init, x, labels, [ids[:k], ids[k:2 * k], ids[2 * k:]], opt)
+    assert abs(one[0][0] - three[0][0]) < 1e-4
+    import math
+    assert abs(one[0][0] - math.log(cfg.classes)) < 1.0
