@@ -213,7 +213,7 @@ def run_ours(args):
         st.synchronize()
     e2e_s = time.perf_counter() - t0
     e2e = {"value": samples / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": ids.numel() * 4 + labels.numel() * 4,
+           "h2d_bytes_per_step": ids.numel() * ids.element_size() + labels.numel() * labels.element_size(),
            "d2h_bytes_per_step": m * 4}
 
     # ---- roofline of the dominant kernel: every GEMM of one step, event-timed ----

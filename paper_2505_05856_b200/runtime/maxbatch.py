@@ -60,12 +60,11 @@ def stage_overhead(model: TransformerConfig, g, lo: int, hi: int, b: int) -> int
     return 16 * params + 2 * largest + 3 * GIB // 2
 
 
-def optimizer_reserve(model: TransformerConfig, g, stages: int, cuts=None) -> int:
+def optimizer_reserve(model: TransformerConfig, g, stages: int, cuts=None, b: int = 1) -> int:
     """Max stage_overhead over the stages of `cuts` (default: compute-balanced)."""
     if cuts is None:
         cuts = P.compute_balanced(g, 0, len(g) - 1, [1] * stages).positions
     bounds = P.stage_bounds(P.Cut(tuple(cuts)), len(g))
-    b = max(1, g.nodes[0].m_a // (2 * model.seq * model.hidden))
     return max(stage_overhead(model, g, lo, hi, b) for lo, hi in bounds)
 
 
@@ -134,7 +133,7 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
               strategy: str, device: int = 0, times=None, run_gpu: bool = True,
               host_cap: int = 96 * GIB) -> dict:
     g = profile_graph(model, b, times=times)
-    reserve = optimizer_reserve(model, g, stages)
+    reserve = optimizer_reserve(model, g, stages, b=b)
     pcap = cap - reserve
     rec = {"b": b, "strategy": strategy, "planner_capacity": pcap, "reserve": reserve}
     cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=max(1, pcap),
@@ -151,7 +150,7 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
             except P.InfeasibleModelError as e:
                 rec.update(feasible=False, reason=f"planner: {e}")
                 return rec
-            need = optimizer_reserve(model, g, stages, plan.cuts.positions)
+            need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b)
             if cap - need >= cfg.capacity:
                 break
             pcap = cap - need

@@ -49,6 +49,10 @@ class RunConfig:
     opt: AdamWConfig = AdamWConfig()
     trace: bool = True
     capacity: Optional[int] = None  # per-GPU byte cap enforced on the caching allocator
+    # co-located stages on one GPU run on their own CUDA streams (cross-stage
+    # dependencies through events), so independent work of different stages
+    # -- what separate GPUs would run in parallel -- can overlap on the device
+    concurrent_stages: bool = True
 
     def __post_init__(self):
         if self.micro_batches < 1:
@@ -157,6 +161,10 @@ class Pipeline:
                 total = torch.cuda.get_device_properties(d).total_memory
                 torch.cuda.set_per_process_memory_fraction(min(1.0, cfg.capacity / total), d)
         self.streams = {d: torch.cuda.Stream(device=d) for d in set(self.stage_dev)}
+        # one stream per stage when several stages share a device (see RunConfig)
+        self.multi = cfg.concurrent_stages and len(set(self.stage_dev)) < self.l
+        self.stage_streams = [torch.cuda.Stream(device=d) if self.multi else self.streams[d]
+                              for d in self.stage_dev]
         nodes = build_nodes(model)
         init = init_params(model, cfg.seed)
         self.stages: List[StageExecutor] = []
@@ -166,7 +174,7 @@ class Pipeline:
                 self.stages.append(StageExecutor(
                     cfg=model, g=g, nodes=nodes, lo=lo, hi=hi, stage=x, stages=self.l,
                     micro_batch=cfg.micro_batch_size, memopt=plan.memopt[x - 1], init=init,
-                    device=torch.device("cuda", d), stream=self.streams[d], opt=cfg.opt,
+                    device=torch.device("cuda", d), stream=self.stage_streams[x - 1], opt=cfg.opt,
                     schedule=plan.schedule, micro_batches=self.m))
         self.order = sync_order(self.l, self.m) if self.sync else colocated_order(self.l, self.m)
         first_dev = self.stage_dev[0]
@@ -185,6 +193,38 @@ class Pipeline:
         for d in (s.work,):
             tot += sum(t.numel() * t.element_size() for t in d.values())
         return tot
+
+    def _send_fwd_streams(self, x: int, j: int):
+        """Concurrent co-located stages: the sender copies its boundary
+        activations into message buffers on its own stream; the receiver's
+        stream waits on the recorded event before delivering."""
+        src = self.stages[x - 1]
+        sst = self.stage_streams[x - 1]
+        out = {}
+        with torch.cuda.stream(sst):
+            for tid in src.send_ids:
+                a = src.send_buffer(tid, j)
+                msg = torch.empty_like(a)
+                K.copy_d2d(msg, a, stream=sst)
+                msg.record_stream(self.stage_streams[x])
+                out[tid] = msg
+            ev = torch.cuda.Event()
+            ev.record(sst)
+        return out, ev
+
+    def _send_bwd_streams(self, x: int, grads: Dict[str, torch.Tensor]):
+        """Gradients of stage x's inputs handed to stage x-1 (same device)."""
+        sst, dst = self.stage_streams[x - 1], self.stage_streams[x - 2]
+        out = {}
+        with torch.cuda.stream(sst):
+            for tid, gsrc in grads.items():
+                gdst = torch.empty_like(gsrc)
+                K.copy_d2d(gdst, gsrc, stream=sst)
+                gdst.record_stream(dst)
+                out[tid] = gdst
+            ev = torch.cuda.Event()
+            ev.record(sst)
+        return out, ev
 
     def _send_fwd(self, x: int, j: int) -> Dict[str, torch.Tensor]:
         """Stage x (1-based) sends micro-batch j's boundary activations: they are
@@ -240,6 +280,8 @@ class Pipeline:
         return self._step(ids, labels, events)
 
     def _step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
+        if self.multi:
+            return self._step_streams(ids, labels, events)
         with torch.cuda.stream(self.streams[self.stage_dev[-1]]):
             self.loss.zero_()
         pending: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
@@ -273,6 +315,60 @@ class Pipeline:
             for x, s in enumerate(self.stages):
                 with torch.cuda.stream(self.streams[self.stage_dev[x]]):
                     s.optimizer_step()
+        return self.loss
+
+    def _step_streams(self, ids, labels, events=None) -> torch.Tensor:
+        """Co-located stages on their own streams: fork from the device's main
+        stream (where the caller's inputs / timing events live), issue the same
+        op order, join back at the end."""
+        main = self.streams[self.stage_dev[0]]
+        with torch.cuda.stream(main):
+            self.loss.zero_()
+        fork = torch.cuda.Event()
+        fork.record(main)
+        for st in self.stage_streams:
+            st.wait_event(fork)
+        pending: Dict[Tuple[int, int], tuple] = {}
+        mailbox: Dict[Tuple[int, int], tuple] = {}
+        for x, kind, j in self.order:
+            s = self.stages[x - 1]
+            st = self.stage_streams[x - 1]
+            if events is not None:
+                e0 = torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+            if kind == "fwd":
+                if x > 1:
+                    msgs, ev = mailbox.pop((x, j))
+                    st.wait_event(ev)
+                    with torch.cuda.stream(st):
+                        for tid, msg in msgs.items():
+                            K.copy_d2d(s.recv_buffer(tid, j), msg, stream=st)
+                s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
+                          labels=labels[j - 1] if s.is_last else None,
+                          loss_out=self.loss[j - 1:j] if s.is_last else None)
+                if x < self.l:
+                    mailbox[(x + 1, j)] = self._send_fwd_streams(x, j)
+            else:
+                if (x, j) in pending:
+                    gts, ev = pending.pop((x, j))
+                    st.wait_event(ev)
+                    for tid, gt in gts.items():
+                        s.set_recv_grad(tid, gt)
+                grads = s.backward(j)
+                if x > 1:
+                    pending[(x - 1, j)] = self._send_bwd_streams(x, grads)
+                s.finish_backward(j)
+            if events is not None:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(st)
+                events.append((x, j, kind, e0, e1))
+        if self.sync:
+            for s in self.stages:
+                s.optimizer_step()
+        for st in self.stage_streams:
+            join = torch.cuda.Event()
+            join.record(st)
+            main.wait_event(join)
         return self.loss
 
     def report(self, events: list, t_origin: torch.cuda.Event, losses: torch.Tensor,

