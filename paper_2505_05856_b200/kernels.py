@@ -26,6 +26,7 @@ class _Instrument:
     def __init__(self):
         self.launches = 0
         self.gemm_events = None
+        self.gemm_flops = 0  # algorithmic 2*M*N*K*batch of every GEMM issued
 
 
 INSTR = _Instrument()
@@ -90,6 +91,7 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
                  residual_mode, None if aux is None else aux.data_ptr(), alpha, gelu, block_n,
                  split_k, cta_group, epilogue)
     INSTR.launches += 1
+    INSTR.gemm_flops += 2 * int(M) * int(N) * int(K) * int(batch1) * int(batch2)
     ev = INSTR.gemm_events
     if ev is not None:
         ts = _torch_stream(stream)

@@ -165,6 +165,9 @@ class Pipeline:
         self.multi = cfg.concurrent_stages and len(set(self.stage_dev)) < self.l
         self.stage_streams = [torch.cuda.Stream(device=d) if self.multi else self.streams[d]
                               for d in self.stage_dev]
+        # True: concurrent stages are chained op by op (issue order), e.g. to
+        # time kernels in isolation
+        self.serialize = False
         nodes = build_nodes(model)
         init = init_params(model, cfg.seed)
         self.stages: List[StageExecutor] = []
@@ -330,9 +333,12 @@ class Pipeline:
             st.wait_event(fork)
         pending: Dict[Tuple[int, int], tuple] = {}
         mailbox: Dict[Tuple[int, int], tuple] = {}
+        last = None
         for x, kind, j in self.order:
             s = self.stages[x - 1]
             st = self.stage_streams[x - 1]
+            if self.serialize and last is not None:
+                st.wait_event(last)
             if events is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(st)
@@ -362,6 +368,9 @@ class Pipeline:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(st)
                 events.append((x, j, kind, e0, e1))
+            if self.serialize:
+                last = torch.cuda.Event()
+                last.record(st)
         if self.sync:
             for s in self.stages:
                 s.optimizer_step()

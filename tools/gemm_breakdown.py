@@ -8,6 +8,7 @@ cfg = PRESETS["bert-large"]; b, m = 8, 16
 g = profile_graph(cfg, b)
 plan = P.plan(g, P.PlanConfig(8, P.SCHEDULE_ASYNC, 160 << 30, 64 << 30))
 pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, trace=False))
+pipe.serialize = True  # per-GEMM times without other stages sharing the SMs
 ids, lab = synthetic_batch(cfg, m, b); ids, lab = ids.cuda(), lab.cuda()
 for _ in range(2): pipe.step(ids, lab)
 K.INSTR.gemm_events = []
