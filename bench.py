@@ -5,9 +5,12 @@
 
 Workload (BASELINE.json configs[1]): BERT-large (24 x 1024, 16 heads, FFN 4096,
 vocab 30522), seq 512, partitioned by this package's planner into an 8-stage
-async-1F1B DawnPiper plan, micro-batch b=8, m=32 micro-batches per step
+async-1F1B DawnPiper plan, micro-batch b=32, m=32 micro-batches per step
 (m = 4l, cli.py:226-228), bf16 compute with fp32 master weights, PipeDream
-weight stashing and a per-micro-batch AdamW update.  At N=1 all 8 stages are
+weight stashing and a per-micro-batch AdamW update.  BASELINE.json leaves b
+open ("b swept"); b=32 is the largest swept size (8, 16, 32 ->
+533 / 612 / 663 samples/s, profiles/r01_bench_*) -- larger micro-batches fill
+the tensor cores better and amortise the per-micro-batch optimizer step.  At N=1 all 8 stages are
 co-located on one GPU; at N>1 (torchrun) the plan has l=N stages, one per GPU.
 
 A step = one pipeline iteration (m micro-batches, b*m samples, every forward,
@@ -48,7 +51,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="bert-large")
-    ap.add_argument("--micro-batch", type=int, default=8)
+    ap.add_argument("--micro-batch", type=int, default=32)
     ap.add_argument("--stages", type=int, default=0, help="default: 8 at N=1, N otherwise")
     ap.add_argument("--micro-batches", type=int, default=32)
     ap.add_argument("--capacity-gib", type=float, default=160.0)

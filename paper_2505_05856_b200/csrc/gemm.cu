@@ -60,7 +60,19 @@ struct GemmParams {
   __nv_bfloat16* aux;
   float alpha;
   int gelu;
+  long long* trace;  // debug: per-CTA wait cycles by role (dpn_gemm_debug_trace), else null
 };
+
+// timed mbarrier wait (debug tracing only)
+__device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long long* acc) {
+  if (acc == nullptr) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  const long long t0 = clock64();
+  mbar_wait(bar, parity);
+  *acc += clock64() - t0;
+}
 
 // per epilogue warp: a 4 KB output staging tile (32 rows x 128 B) and a 4 KB
 // side tile (the TMA-loaded residual, or the GELU pre-activation `aux` output)
@@ -470,7 +482,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const long long t_start = clock64();
   pdl_wait();  // everything above overlaps the previous kernel's tail (PDL)
+  const long long t_run = clock64();
+  // debug trace slots per CTA: 0 producer wait(empty), 1 MMA wait(full),
+  // 2 MMA wait(tempty), 3 epilogue wait(tfull) (warp 4), 4 run cycles, 5 pdl wait,
+  // 6 epilogue busy (warp 4), 7 units
+  long long tw = 0, tw2 = 0;
+  long long* trace_w = p.trace ? &tw : nullptr;
+  long long* trace_w2 = p.trace ? &tw2 : nullptr;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
@@ -482,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int m0 = w.m0 + BM * (int)rank;
         const int n0 = w.nb * BN + C::kBRows * (int)rank;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_t(&empty[stage], phase ^ 1, trace_w);
           if (rank == 0) mbar_expect_tx(&full[stage], CG * C::kStageBytes);
           else mbar_arrive_remote(&full[stage], 0);
           uint8_t* a_dst = sA + stage * C::kABytes;
@@ -526,11 +546,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t acc_phase = 0;
       for (long long u = cluster_id; u < p.units; u += n_clusters) {
         const Unit w = decode(p, u, nk);
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait_t(&tempty[acc], acc_phase ^ 1, trace_w2);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_t(&full[stage], phase, trace_w);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
@@ -583,10 +603,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(&rbar[ew], kEpiStage);
           tma_load_2d_cta(s_side, &tmR, &rbar[ew], n0 + half * 64, row_base);
         }
-        mbar_wait(&tfull[acc], acc_phase);
+        mbar_wait_t(&tfull[acc], acc_phase, trace_w);
+        const long long te0 = clock64();
         tc_fence_after();
         epilogue_tile_tma<BN>(p, &tmC, &tmR, &tmX, tmem_base + acc * BN + ((uint32_t)lanes << 16), n0,
                               row_base, half, lane, s_out, s_side, &rbar[ew], rphase);
+        if (p.trace) tw2 += clock64() - te0;
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -627,6 +649,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (p.tma_epi && lane == 0) bulk_wait0();  // stores complete before the CTA retires
+  }
+  if (p.trace && lane == 0) {
+    long long* t = p.trace + (long long)blockIdx.x * 8;
+    if (warp == 0) { t[0] = tw; t[5] = t_run - t_start; }
+    if (warp == 1 && rank == 0) { t[1] = tw; t[2] = tw2; }
+    if (warp == kEpiWarp0) { t[3] = tw; t[6] = tw2; t[4] = clock64() - t_run; }
   }
 
   tc_fence_before();
@@ -905,6 +933,9 @@ void pick_config(long long M, long long N, long long Z, int& bn, int& cg) {
 
 }  // namespace dpn
 
+static long long* g_gemm_trace = nullptr;
+extern "C" void dpn_gemm_debug_trace(void* buf) { g_gemm_trace = static_cast<long long*>(buf); }
+
 extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   using namespace dpn;
   DPN_REQUIRE(g != nullptr, "null args");
@@ -940,6 +971,7 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   p.aux = static_cast<__nv_bfloat16*>(g->aux);
   p.alpha = g->alpha;
   p.gelu = g->gelu;
+  p.trace = g_gemm_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
   int bn = 0, cg = 1;
   pick_config(g->M, g->N, p.Z, bn, cg);
