@@ -286,18 +286,23 @@ __device__ __forceinline__ float tanh_fast(float x) {
   return y;
 }
 
+// tanh-GELU and its derivative in FMA form (6 / 10 instructions):
+//   u = x (k0 + k0 k1 x^2),  gelu = hx (1 + tanh u) with hx = x / 2,
+//   gelu' = (1 + t) / 2 + hx (1 - t^2) (k0 + 3 k0 k1 x^2)
 __device__ __forceinline__ float gelu_tanh(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float u = k0 * (x + k1 * x * x * x);
-  return 0.5f * x * (1.f + tanh_fast(u));
+  const float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
+  const float u = x * fmaf(k01, x * x, k0);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_fast(u), hx);
 }
 
 __device__ __forceinline__ float gelu_tanh_grad(float x) {
-  const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-  const float u = k0 * (x + k1 * x * x * x);
-  const float t = tanh_fast(u);
-  const float du = k0 * (1.f + 3.f * k1 * x * x);
-  return 0.5f * (1.f + t) + 0.5f * x * (1.f - t * t) * du;
+  const float k0 = 0.7978845608028654f, k01 = 0.7978845608028654f * 0.044715f;
+  const float x2 = x * x;
+  const float t = tanh_fast(x * fmaf(k01, x2, k0));
+  const float a = fmaf(3.f * k01, x2, k0);
+  const float s = fmaf(-t, t, 1.f);
+  return fmaf(0.5f * x * s, a, fmaf(0.5f, t, 0.5f));
 }
 
 __device__ __forceinline__ float warp_sum(float v) {

@@ -343,7 +343,11 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       tmem_ld_32x32b_x32(taddr + c * 64 + h * 32, r);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[h * 32 + i] = __uint_as_float(r[i]) * p.alpha;
+      for (int i = 0; i < 32; ++i) v[h * 32 + i] = __uint_as_float(r[i]);
+    }
+    if (p.alpha != 1.f) {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] *= p.alpha;
     }
     if (p.bias) {
       const __nv_bfloat16* bp = p.bias + col0;

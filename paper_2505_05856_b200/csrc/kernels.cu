@@ -447,14 +447,27 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
   for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
     const __nv_bfloat16* src = logits + r * ld;
     float mx = -INFINITY;
-    for (int c = tid; c < nvec; c += blockDim.x) {
-      uint4 u = reinterpret_cast<const uint4*>(src)[c];
-      reinterpret_cast<uint4*>(row)[c] = u;
-      float v[8];
-      load8(reinterpret_cast<const __nv_bfloat16*>(&u), v);
+    // 8 row vectors in flight per thread (the whole 30K-50K row in one or two rounds)
+    constexpr int U = 8;
+    for (int c0 = tid; c0 < nvec; c0 += blockDim.x * U) {
+      uint4 u[U];
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (c * 8 + k < vocab) mx = fmaxf(mx, v[k]);
+      for (int i = 0; i < U; ++i) {
+        const int c = c0 + i * blockDim.x;
+        if (c < nvec) u[i] = __ldcs(reinterpret_cast<const uint4*>(src) + c);
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const int c = c0 + i * blockDim.x;
+        if (c < nvec) {
+          reinterpret_cast<uint4*>(row)[c] = u[i];
+          float v[8];
+          load8(reinterpret_cast<const __nv_bfloat16*>(&u[i]), v);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (c * 8 + k < vocab) mx = fmaxf(mx, v[k]);
+        }
+      }
     }
     mx = warp_max(mx);
     if ((tid & 31) == 0) red[tid >> 5] = mx;

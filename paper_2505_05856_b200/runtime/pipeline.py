@@ -219,12 +219,17 @@ class Pipeline:
         """Gradients of stage x's inputs handed to stage x-1 (same device)."""
         sst, dst = self.stage_streams[x - 1], self.stage_streams[x - 2]
         out = {}
+        seen = set()
         with torch.cuda.stream(sst):
-            for tid, gsrc in grads.items():
-                gdst = torch.empty_like(gsrc)
-                K.copy_d2d(gdst, gsrc, stream=sst)
-                gdst.record_stream(dst)
-                out[tid] = gdst
+            for tid, g in grads.items():
+                # the sender drops its gradient buffers after this backward, so they
+                # are handed over as they are; one buffer aliased by two tensors'
+                # gradients is copied (the receiver may update either in place)
+                if g.data_ptr() in seen:
+                    g = g.clone()
+                seen.add(g.data_ptr())
+                g.record_stream(dst)
+                out[tid] = g
             ev = torch.cuda.Event()
             ev.record(sst)
         return out, ev
@@ -348,7 +353,7 @@ class Pipeline:
                     st.wait_event(ev)
                     with torch.cuda.stream(st):
                         for tid, msg in msgs.items():
-                            K.copy_d2d(s.recv_buffer(tid, j), msg, stream=st)
+                            s.adopt_recv(tid, j, msg)
                 s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
                           labels=labels[j - 1] if s.is_last else None,
                           loss_out=self.loss[j - 1:j] if s.is_last else None)

@@ -432,6 +432,22 @@ class StageExecutor:
             return self._alloc_live(tid)
         return self.buf(tid, self.slot_of(mb), "fwd")
 
+    def adopt_recv(self, tid: str, mb: int, msg: torch.Tensor) -> None:
+        """Zero-copy receive (co-located stages): the message buffer becomes this
+        stage's buffer of tid for micro-batch mb.  The sender hands over a
+        private copy, so nothing else writes it."""
+        if tid in self.evicted:
+            self._drop_leftovers()
+            self.live[tid] = msg
+            return
+        slot = self.slot_of(mb)
+        if tid in self.slot_buf[slot]:
+            self.slot_buf[slot][tid] = msg
+        elif tid in self.work:
+            self.work[tid] = msg
+        else:
+            raise KeyError(f"stage {self.stage}: no buffer for {tid}")
+
     def send_buffer(self, tid: str, mb: int) -> torch.Tensor:
         return self.buf(tid, self.slot_of(mb), "fwd")
 

@@ -21,18 +21,32 @@ cases = [  # name, M, N, K, a_mn, b_mn, f32, epilogue kwargs
     ("fc1 wgrad", 4096, 1024, M, 1, 1, 1, ""),
     ("proj wgrad", 1024, 1024, M, 1, 1, 1, ""),
     ("big", 8192, 8192, 8192, 0, 0, 0, ""),
+    ("fc1 plain", M, 4096, 1024, 0, 0, 0, ""),
+    ("fc1 bias", M, 4096, 1024, 0, 0, 0, "bias"),
+    ("fc1 gelu", M, 4096, 1024, 0, 0, 0, "gelu"),
+    ("fc1 b32", 16384, 4096, 1024, 0, 0, 0, "gelu_aux"),
+    ("fc2dg b32", 16384, 4096, 1024, 0, 1, 0, "gelu_grad"),
+    ("fc2dg plain", 16384, 4096, 1024, 0, 1, 0, ""),
+    ("fc2dg resadd", 16384, 4096, 1024, 0, 1, 0, "res"),
+    ("fc2dg gg-ldg", 16384, 4096, 1024, 0, 1, 0, "gelu_grad_direct"),
+    ("fc1 b32 ldg", 16384, 4096, 1024, 0, 0, 0, "gelu_aux_direct"),
 ]
 for name, m, n, kk, amn, bmn, f32, epi in cases:
     A = torch.randn(kk, m, device="cuda").to(bf) if amn else torch.randn(m, kk, device="cuda").to(bf)
     B = torch.randn(kk, n, device="cuda").to(bf) if bmn else torch.randn(n, kk, device="cuda").to(bf)
     C = torch.empty(m, n, device="cuda", dtype=torch.float32 if f32 else bf)
     kw = {}
-    if "bias" in epi or epi == "gelu_aux":
+    if "bias" in epi or epi.startswith("gelu_aux"):
         kw["bias"] = torch.randn(n, device="cuda").to(bf)
-    if epi in ("bias_res", "acc"):
+    if epi.endswith("_direct"):
+        kw["epilogue"] = 1
+        epi = epi[:-len("_direct")]
+    if epi in ("bias_res", "acc", "res"):
         kw["residual"] = torch.randn(m, n, device="cuda").to(bf)
     if epi == "gelu_aux":
         kw.update(gelu=True, aux=torch.empty(m, n, device="cuda", dtype=bf))
+    if epi == "gelu":
+        kw.update(gelu=True)
     if epi == "gelu_grad":
         kw.update(residual=torch.randn(m, n, device="cuda").to(bf), residual_mode=1)
     call = lambda: k.gemm_raw(M=m, N=n, K=kk, A=A, lda=A.stride(0), a_mn=bool(amn), B=B, ldb=B.stride(0),

@@ -11,6 +11,7 @@ m = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 cfg = PRESETS[name]; g = profile_graph(cfg, b)
 plan = P.plan(g, P.PlanConfig(8, P.SCHEDULE_ASYNC, 160 << 30, 64 << 30))
 pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, trace=False))
+pipe.serialize = len(sys.argv) > 4 and sys.argv[4] == "serial"
 ids, lab = synthetic_batch(cfg, m, b); ids, lab = ids.cuda(), lab.cuda()
 for _ in range(2): pipe.step(ids, lab)
 torch.cuda.synchronize()
