@@ -168,17 +168,56 @@ def run_bench_distributed(args) -> None:
     dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = K.INSTR.launches
+    clocks = None
+    if rank == 0:
+        try:
+            import sys
+            sys.path.insert(0, os.getcwd())
+            from bench import Clocks
+            clocks = Clocks(local)
+            clocks.start()
+        except Exception:  # clock sampling is evidence, not part of the run
+            clocks = None
     e0.record(stream)
     for _ in range(args.steps):
         step()
     e1.record(stream)
     torch.cuda.synchronize()
+    clk = clocks.stop() if clocks is not None else None
     dist.barrier()
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     launches = torch.tensor([(K.INSTR.launches - l0) // args.steps], device=dev, dtype=torch.int64)
     dist.all_reduce(launches)
     value = args.steps * m * b / (ms.item() / 1e3)
+
+    # e2e: inputs copied H2D from pinned memory on the ranks that embed, the loss
+    # vector read back on the last rank, every step; wall time, max over ranks
+    ids_h = ids.pin_memory() if stage.needs_ids else None
+    lab_h = labels.pin_memory() if stage.is_last else None
+    loss_h = torch.empty(m, dtype=torch.float32).pin_memory() if stage.is_last else None
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            if ids_h is not None:
+                ids_d.copy_(ids_h, non_blocking=True)
+            if lab_h is not None:
+                lab_d.copy_(lab_h, non_blocking=True)
+        run_stage_step(stage, chans, rank, world, m, ids_d, lab_d, loss)
+        if loss_h is not None:
+            with torch.cuda.stream(stream):
+                loss_h.copy_(loss, non_blocking=True)
+        stream.synchronize()
+    wall = torch.tensor([time.perf_counter() - t0], device=dev)
+    dist.all_reduce(wall, op=dist.ReduceOp.MAX)
+    h2d = torch.tensor([(ids.numel() * ids.element_size() if stage.needs_ids else 0)
+                        + (labels.numel() * labels.element_size() if stage.is_last else 0)],
+                       device=dev, dtype=torch.int64)
+    dist.all_reduce(h2d)
+    e2e = {"value": args.steps * m * b / wall.item(), "unit": "samples/s",
+           "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": m * 4}
     if rank == 0:
         out = {"metric": "samples/sec at 1/2/4/8 stages; max trainable batch under per-GPU mem cap",
                "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
@@ -190,7 +229,8 @@ def run_bench_distributed(args) -> None:
                           "model": args.model, "global_batch": b * m, "seq_len": cfg.seq,
                           "micro_batch": b, "micro_batches": m, "stages": stages,
                           "cuts": list(plan.cuts.positions), "parallelism": f"pp{stages}"},
-               "gpu_launches": int(launches.item())}
+               "gpu_launches": int(launches.item()), "e2e": e2e, "clocks": clk,
+               "roofline": None, "model_tflops": round(value * cfg.flops_per_sample() / 1e12, 1)}
         print(json.dumps(out), flush=True)
     dist.barrier()
     dist.destroy_process_group()
