@@ -5,8 +5,14 @@
 // touches HBM (the unfused `score` node writes b*heads*s^2 bf16 and reads it
 // back three times).
 //
-// Forward, one CTA per (batch, head, 128-query tile), 384 threads:
-//   warp 0   TMA: Q once, then K_j / V_j tiles into a 3-deep ring
+// Forward: persistent, one CTA per SM walking work units (batch, head,
+// 128-query tile) -- longest causal units first -- with every barrier phase
+// and TMEM / smem buffer indexed by a CTA-global tile counter, so the next
+// unit's Q / K / V loads and S MMAs overlap the current unit's tail (the
+// per-unit prologue / epilogue of a one-CTA-per-unit grid dominated at
+// s = 512).  384 threads:
+//   warp 0   TMA: Q per unit (single buffer, released after the unit's last
+//            S MMA), K_j / V_j tiles into a 3-deep ring
 //   warp 1   MMA issuer: S_j = Q K_j^T (M=128,N=128,K=64) into TMEM S[j%2];
 //            O_j = P_j V_j (M=128,N=64,K=128) into TMEM O[j%2]
 //   warp 2   TMEM allocator
@@ -24,6 +30,7 @@
 #include "common.cuh"
 #include "../../include/dawnpiper.h"
 
+#include <algorithm>
 #include <mutex>
 #include <type_traits>
 
@@ -77,6 +84,15 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+template <uint32_t N>
+__device__ __forceinline__ void regs_dec() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void regs_inc() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -96,18 +112,27 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* p_empty = p_full + 2;           // [2]
   uint64_t* o_full = p_empty + 2;           // [2]
   uint64_t* o_empty = o_full + 2;           // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* q_empty = o_empty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int qt = blockIdx.x, h = blockIdx.y, bb = blockIdx.z;
-  const int q0 = qt * kTile;
   const int n_kv_all = (p.seq + kTile - 1) / kTile;
-  const int n_kv = p.causal ? min(n_kv_all, qt + 1) : n_kv_all;
-  const int row0 = bb * p.seq;  // first token row of this sequence in [b*s, 3H]
+  const long long bh = (long long)p.batch * p.heads;
+  const long long units = bh * n_kv_all;
+  // unit -> (query tile, head, batch); query tiles outermost, longest first
+  auto decode = [&](long long u, int& qt, int& h, int& bb) {
+    const int qi = (int)(u / bh);
+    const long long r = u - (long long)qi * bh;
+    qt = p.causal ? n_kv_all - 1 - qi : qi;
+    h = (int)(r % p.heads);
+    bb = (int)(r / p.heads);
+  };
+  auto kv_tiles = [&](int qt) { return p.causal ? min(n_kv_all, qt + 1) : n_kv_all; };
 
   if (warp == 0 && lane == 0) prefetch_tmap(&tm_qkv);
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int s = 0; s < kKVStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -132,14 +157,21 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(q_full, kTileBytes);
-      tma_load_2d(sQ, &tm_qkv, q_full, h * kD, row0 + q0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int st = j % kKVStages;
-        mbar_wait(&kv_empty[st], ((j / kKVStages) & 1) ^ 1);
-        mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-        tma_load_2d(sK + st * kTileBytes, &tm_qkv, &kv_full[st], p.H + h * kD, row0 + j * kTile);
-        tma_load_2d(sV + st * kTileBytes, &tm_qkv, &kv_full[st], 2 * p.H + h * kD, row0 + j * kTile);
+      int g = 0, uc = 0;  // CTA-global KV tile / unit counters
+      for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+        int qt, h, bb;
+        decode(u, qt, h, bb);
+        const int n_kv = kv_tiles(qt), row0 = bb * p.seq;
+        mbar_wait(q_empty, (uc & 1) ^ 1);
+        mbar_expect_tx(q_full, kTileBytes);
+        tma_load_2d(sQ, &tm_qkv, q_full, h * kD, row0 + qt * kTile);
+        for (int j = 0; j < n_kv; ++j, ++g) {
+          const int st = g % kKVStages;
+          mbar_wait(&kv_empty[st], ((g / kKVStages) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+          tma_load_2d(sK + st * kTileBytes, &tm_qkv, &kv_full[st], p.H + h * kD, row0 + j * kTile);
+          tma_load_2d(sV + st * kTileBytes, &tm_qkv, &kv_full[st], 2 * p.H + h * kD, row0 + j * kTile);
+        }
       }
     }
   } else if (warp == 1) {
@@ -167,34 +199,46 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
       __syncwarp();
     };
-    mbar_wait(q_full, 0);
-    for (int j = 0; j < n_kv; ++j) {
-      const int st = j % kKVStages, i = j & 1;
-      mbar_wait(&kv_full[st], (j / kKVStages) & 1);
-      mbar_wait(&s_empty[i], ((j >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
+    int g = 0, uc = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+      int qt, h, bb;
+      decode(u, qt, h, bb);
+      const int n_kv = kv_tiles(qt);
+      mbar_wait(q_full, uc & 1);
+      for (int j = 0; j < n_kv; ++j, ++g) {
+        const int st = g % kKVStages, i = g & 1;
+        mbar_wait(&kv_full[st], (g / kKVStages) & 1);
+        mbar_wait(&s_empty[i], ((g >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
 #pragma unroll
-        for (int k = 0; k < kD / 16; ++k) {
-          const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(kb + k * 32, 16, 1024);
-          umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
+            const uint64_t bd = smem_desc_sw128(kb + k * 32, 16, 1024);
+            umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[i]);
+          if (j == n_kv - 1) umma_commit(q_empty);  // Q is free once the unit's S MMAs ran
         }
-        umma_commit(&s_full[i]);
+        __syncwarp();
+        if (g >= 1) issue_o(g - 1);
       }
-      __syncwarp();
-      if (j >= 1) issue_o(j - 1);
     }
-    issue_o(n_kv - 1);
+    if (g >= 1) issue_o(g - 1);
   } else if (warp >= 4) {
     // ---------------- softmax / correction ----------------
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;  // query row within the tile (== TMEM lane)
-    const int q = q0 + r;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     float* xmax = reinterpret_cast<float*>(tmem_slot + 4);  // [2][128][2] row-max exchange
     const float sl = p.scale_log2;
+    int gbase = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+    int qt, h, bb;
+    decode(u, qt, h, bb);
+    const int n_kv = kv_tiles(qt), row0 = bb * p.seq;
+    const int q = qt * kTile + r;
     float ms = -INFINITY;  // running max, scaled log2 units
     float l = 0.f;         // partial row sum over this half's keys
     float o[kD / 2];
@@ -202,23 +246,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int c = 0; c < kD / 2; ++c) o[c] = 0.f;
     float alpha_prev = 1.f;
     for (int j = 0; j <= n_kv; ++j) {
+      const int gj = gbase + j;  // CTA-global tile index
       if (j < n_kv) {
-        const int i = j & 1;
+        const int i = gj & 1;
         const int k0 = j * kTile + half * 64;
         const bool mask = (j + 1) * kTile > p.seq || (p.causal && j == qt);
-        mbar_wait(&s_full[i], (j >> 1) & 1);
+        mbar_wait(&s_full[i], (gj >> 1) & 1);
         tc_fence_after();
         float s[64];
         {
-          uint32_t u[32];
+          // both 32-column loads in flight, one wait
+          uint32_t u[64];
           tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + lane_off, u);
+          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, u + 32);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; ++e) s[e] = __uint_as_float(u[e]);
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, u);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) s[32 + e] = __uint_as_float(u[e]);
+          for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(u[e]);
         }
         tc_fence_before();
         __syncwarp();
@@ -233,7 +276,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float mx = s[0];
 #pragma unroll
         for (int c = 1; c < 64; ++c) mx = fmaxf(mx, s[c]);
-        float* xm = xmax + (j & 1) * 256 + r * 2;
+        float* xm = xmax + (gj & 1) * 256 + r * 2;
         xm[half] = mx;
         pair_sync(quarter);
         mx = fmaxf(xm[0], xm[1]) * sl;  // row max over all 128 keys (scaled)
@@ -244,7 +287,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         const float base = (ms == -INFINITY) ? 0.f : ms;
         float sum = 0.f;
-        mbar_wait(&p_empty[i], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&p_empty[i], ((gj >> 1) & 1) ^ 1);
         uint8_t* pt = sP + i * kPBytes + half * (kPBytes / 2);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -267,8 +310,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[i]);
         // accumulate the previous O tile with its own correction factor
         if (j >= 1) {
-          const int pi = (j - 1) & 1;
-          mbar_wait(&o_full[pi], ((j - 1) >> 1) & 1);
+          const int pi = (gj - 1) & 1;
+          mbar_wait(&o_full[pi], ((gj - 1) >> 1) & 1);
           tc_fence_after();
           uint32_t u[32];
           tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + half * 32 + lane_off, u);
@@ -281,8 +324,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         alpha_prev = alpha;
       } else {
-        const int pi = (j - 1) & 1;
-        mbar_wait(&o_full[pi], ((j - 1) >> 1) & 1);
+        const int pi = (gj - 1) & 1;
+        mbar_wait(&o_full[pi], ((gj - 1) >> 1) & 1);
         tc_fence_after();
         uint32_t u[32];
         tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + half * 32 + lane_off, u);
@@ -290,8 +333,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(u[e]));
         tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&o_empty[pi]);  // the buffer serves the next unit
       }
     }
+    gbase += n_kv;
     // combine the two halves' row sums
     float* xs = xmax + 512 + r * 2;
     xs[half] = l;
@@ -312,6 +358,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // natural-log LSE of scale * S:  (m + log2 l) / log2(e)
       if (half == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (ms + log2f(l)) / kLog2e;
     }
+    }  // units
   }
   tc_fence_before();
   __syncthreads();
@@ -421,14 +468,6 @@ struct AttnBwdParams {
     }                                                                                 \
   } while (0)
 
-template <uint32_t N>
-__device__ __forceinline__ void regs_dec() {
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
-}
-template <uint32_t N>
-__device__ __forceinline__ void regs_inc() {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
-}
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
@@ -857,7 +896,15 @@ extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batc
                                         kFwdSmem));
     set = true;
   }
-  dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm <= 0) n_sm = 148;
+  }
+  const long long units = (long long)((seq + kTile - 1) / kTile) * heads * batch;
+  const unsigned grid = (unsigned)std::min<long long>(units, n_sm);  // persistent: one CTA per SM
   DPN_CHECK_CUDA(launch_pdl(attn_fwd_kernel, grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream, tm, p));
   DPN_LAUNCH_CHECK();
   return 0;

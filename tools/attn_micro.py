@@ -21,7 +21,7 @@ def graph_time(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e-3
 
 
-for b, h, s, causal in ((8, 16, 512, False), (4, 25, 1024, True), (16, 16, 512, False)):
+for b, h, s, causal in ((8, 16, 512, False), (4, 25, 1024, True), (16, 16, 512, False), (32, 16, 512, False)):
     H = h * 64
     qkv = (torch.randn(b * s, 3 * H, device="cuda") * 0.5).bfloat16()
     out = torch.empty(b * s, H, device="cuda", dtype=torch.bfloat16)

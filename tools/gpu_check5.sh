@@ -4,4 +4,5 @@ mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 300 python tools/profile_step.py > gpurun_out/breakdown.txt 2>&1
+timeout 600 python tools/profile_step.py bert-large 32 32 serial > gpurun_out/breakdown.txt 2>&1
+timeout 300 python tools/attn_micro.py > gpurun_out/attn_micro.txt 2>&1
