@@ -305,6 +305,53 @@ __device__ __forceinline__ float gelu_tanh_grad(float x) {
   return fmaf(0.5f * x * s, a, fmaf(0.5f, t, 0.5f));
 }
 
+// ---- packed f32x2 math (sm_100: FFMA2 / FMUL2 issue two lanes of fp32 per instruction)
+__device__ __forceinline__ uint64_t f2_pack(float2 a) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a.x), "f"(a.y));
+  return r;
+}
+__device__ __forceinline__ float2 f2_unpack(uint64_t r) {
+  float2 a;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a.x), "=f"(a.y) : "l"(r));
+  return a;
+}
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)), "l"(f2_pack(c)));
+  return f2_unpack(r);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(r);
+}
+
+// tanh-GELU / its derivative on two values with packed fp32 FMAs (the same
+// formulas as gelu_tanh / gelu_tanh_grad, two lanes per instruction)
+__device__ __forceinline__ float2 gelu_tanh2(float2 x) {
+  const float2 k0 = make_float2(0.7978845608028654f, 0.7978845608028654f);
+  const float2 k01 = make_float2(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
+  const float2 u = mul2(x, fma2(k01, mul2(x, x), k0));
+  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 hx = mul2(make_float2(0.5f, 0.5f), x);
+  return fma2(hx, t, hx);
+}
+
+__device__ __forceinline__ float2 gelu_tanh_grad2(float2 x) {
+  const float2 k0 = make_float2(0.7978845608028654f, 0.7978845608028654f);
+  const float2 k01 = make_float2(0.7978845608028654f * 0.044715f, 0.7978845608028654f * 0.044715f);
+  const float2 k013 = make_float2(3.f * k01.x, 3.f * k01.x);
+  const float2 half = make_float2(0.5f, 0.5f), one = make_float2(1.f, 1.f);
+  const float2 x2 = mul2(x, x);
+  const float2 u = mul2(x, fma2(k01, x2, k0));
+  const float2 t = make_float2(tanh_fast(u.x), tanh_fast(u.y));
+  const float2 a = fma2(k013, x2, k0);
+  const float2 s = fma2(make_float2(-t.x, -t.y), t, one);
+  const float2 hs = mul2(mul2(half, x), s);
+  return fma2(hs, a, fma2(half, t, half));
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

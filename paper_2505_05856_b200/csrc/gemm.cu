@@ -358,9 +358,10 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
           const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const float2 f = __bfloat1622float2(hh[k]);
-            v[8 * q + 2 * k] += f.x;
-            v[8 * q + 2 * k + 1] += f.y;
+            const float2 o = fma2(make_float2(1.f, 1.f), make_float2(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]),
+                                  __bfloat1622float2(hh[k]));
+            v[8 * q + 2 * k] = o.x;
+            v[8 * q + 2 * k + 1] = o.y;
           }
         }
       } else {
@@ -379,13 +380,11 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const float2 f = __bfloat1622float2(hh[k]);
-          if (p.res_mode == 0) {
-            v[8 * q + 2 * k] += f.x;
-            v[8 * q + 2 * k + 1] += f.y;
-          } else {
-            v[8 * q + 2 * k] *= gelu_tanh_grad(f.x);
-            v[8 * q + 2 * k + 1] *= gelu_tanh_grad(f.y);
-          }
+          const float2 vv = make_float2(v[8 * q + 2 * k], v[8 * q + 2 * k + 1]);
+          const float2 o = p.res_mode == 0 ? fma2(make_float2(1.f, 1.f), vv, f)
+                                           : mul2(vv, gelu_tanh_grad2(f));
+          v[8 * q + 2 * k] = o.x;
+          v[8 * q + 2 * k + 1] = o.y;
         }
       }
       __syncwarp();  // every lane has read the residual tile: prefetch the next chunk's
@@ -410,7 +409,11 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
     }
     if (p.gelu) {
 #pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
+      for (int i = 0; i < 64; i += 2) {
+        const float2 g = gelu_tanh2(make_float2(v[i], v[i + 1]));
+        v[i] = g.x;
+        v[i + 1] = g.y;
+      }
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
