@@ -286,16 +286,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           ms = mx;
         }
         const float base = (ms == -INFINITY) ? 0.f : ms;
-        float sum = 0.f;
+        float2 sum2 = make_float2(0.f, 0.f);
         mbar_wait(&p_empty[i], ((gj >> 1) & 1) ^ 1);
         uint8_t* pt = sP + i * kPBytes + half * (kPBytes / 2);
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           float e8[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            e8[e] = ex2(fmaf(s[c * 8 + e], sl, -base));
-            sum += e8[e];
+          for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
+            const float2 a = fma2(make_float2(s[c * 8 + e], s[c * 8 + e + 1]), make_float2(sl, sl),
+                                  make_float2(-base, -base));
+            const float2 ev = make_float2(ex2(a.x), ex2(a.y));
+            e8[e] = ev.x;
+            e8[e + 1] = ev.y;
+            sum2 = fma2(make_float2(1.f, 1.f), ev, sum2);
           }
           uint4 w;
           w.x = pack_bf16(e8[0], e8[1]);
@@ -304,7 +308,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.w = pack_bf16(e8[6], e8[7]);
           *reinterpret_cast<uint4*>(pt + sw128(r, c)) = w;
         }
-        l = l * alpha + sum;
+        l = l * alpha + (sum2.x + sum2.y);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&p_full[i]);
@@ -320,7 +324,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&o_empty[pi]);
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(u[e]));
+          for (int e = 0; e < 32; e += 2) {
+            const float2 t = fma2(make_float2(o[e], o[e + 1]), make_float2(alpha_prev, alpha_prev),
+                                  make_float2(__uint_as_float(u[e]), __uint_as_float(u[e + 1])));
+            o[e] = t.x;
+            o[e + 1] = t.y;
+          }
         }
         alpha_prev = alpha;
       } else {
@@ -685,14 +694,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this half's 64-key atom
           float pv[8], dsv[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            float pr = ex2(fmaf(__uint_as_float(us[c * 8 + e]), sl, -lse2));
+          for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
+            const float2 a = fma2(make_float2(__uint_as_float(us[c * 8 + e]), __uint_as_float(us[c * 8 + e + 1])),
+                                  make_float2(sl, sl), make_float2(-lse2, -lse2));
+            float2 pr = make_float2(ex2(a.x), ex2(a.y));
             if constexpr (kMask) {
               const int key = k0 + half * 64 + c * 8 + e;
-              pr = (qok && key < p.seq && (!p.causal || key <= q)) ? pr : 0.f;
+              pr.x = (qok && key < p.seq && (!p.causal || key <= q)) ? pr.x : 0.f;
+              pr.y = (qok && key + 1 < p.seq && (!p.causal || key + 1 <= q)) ? pr.y : 0.f;
             }
-            pv[e] = pr;
-            dsv[e] = pr * fmaf(__uint_as_float(ud[c * 8 + e]), sc, -Dq);
+            pv[e] = pr.x;
+            pv[e + 1] = pr.y;
+            const float2 ds = mul2(pr, fma2(make_float2(__uint_as_float(ud[c * 8 + e]), __uint_as_float(ud[c * 8 + e + 1])),
+                                            make_float2(sc, sc), make_float2(-Dq, -Dq)));
+            dsv[e] = ds.x;
+            dsv[e + 1] = ds.y;
           }
           pk[c].x = pack_bf16(pv[0], pv[1]);
           pk[c].y = pack_bf16(pv[2], pv[3]);

@@ -90,9 +90,14 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
         w = l - x + 1
         m = micro_batches or (w + 1)
         gen = torch.Generator(device=dev).manual_seed(x)
-        ids = torch.randint(0, model.vocab, (m, b * model.in_tokens), device=dev, dtype=torch.int32,
-                            generator=gen)
-        labels = ids[:, :b * model.out_tokens]
+        ishape, idt = model.input_spec(b)
+        if idt == torch.int32:
+            ids = torch.randint(0, model.vocab, (m,) + tuple(ishape), device=dev, dtype=idt,
+                                generator=gen)
+        else:  # CNN images
+            ids = torch.randn((m,) + tuple(ishape), device=dev, generator=gen).to(idt)
+        labels = torch.randint(0, model.vocab, (m, b * model.out_tokens), device=dev,
+                               dtype=torch.int32, generator=gen)
         loss = torch.zeros(m, device=dev)
         with torch.cuda.stream(stream):
             for kind, j, _ in async_ops(l, m, x):
