@@ -58,32 +58,20 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
-  const long long stride = (long long)gridDim.x * warps;
-  long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5);
-  // the next row's raw vectors are loaded while the current one is normalised
-  // (two rows in flight per warp; the grid holds only resident CTAs)
-  uint4 nx[NV];
-  auto fetch = [&](long long rr) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int c = lane + 32 * j;
-      if (rr < rows && c < nvec) nx[j] = *reinterpret_cast<const uint4*>(x + rr * cols + c * 8);
-    }
-  };
-  fetch(r);
-  for (; r < rows; r += stride) {
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const __nv_bfloat16* xr = x + r * cols;
     float v[NV][8];
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int c = lane + 32 * j;
       if (c < nvec) {
-        load8(reinterpret_cast<const __nv_bfloat16*>(&nx[j]), v[j]);
+        load8(xr + c * 8, v[j]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) s += v[j][i];
       }
     }
-    fetch(r + stride);
     const float mu = warp_sum(s) / cols;
     float q = 0.f;
 #pragma unroll
@@ -621,13 +609,6 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 using namespace dpn;
 
-// LayerNorm grids: resident CTAs only (each warp walks rows with the next one
-// prefetched); ~4 CTAs of 256 threads per SM at <= 1024 columns, 2 above
-static int ln_grid(long long rows, long long cols) {
-  const long long per_sm = cols <= 1024 ? 3 : 2;
-  return (int)std::max<long long>(1, std::min<long long>((rows + 7) / 8, 148 * per_sm));
-}
-
 #define LN_DISPATCH(KERNEL, GRID, SMEM, ...)                                       \
   do {                                                                             \
     const int nv = (int)((cols / 8 + 31) / 32);                                    \
@@ -650,7 +631,7 @@ extern "C" int dpn_layernorm_fwd(const void* x, const void* gamma, const void* b
   DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * kMaxVec, "cols must be a multiple of 8, <= 2048");
   DPN_REQUIRE(aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta), "16-byte alignment");
   if (rows == 0) return 0;
-  LN_DISPATCH(ln_fwd_kernel, ln_grid(rows, cols), 0, (const __nv_bfloat16*)x,
+  LN_DISPATCH(ln_fwd_kernel, grid_for(rows, 8), 0, (const __nv_bfloat16*)x,
               (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)beta, (__nv_bfloat16*)y, mean, rstd,
               rows, (int)cols, eps);
   DPN_LAUNCH_CHECK();
