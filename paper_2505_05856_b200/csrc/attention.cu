@@ -17,15 +17,16 @@
 //            O_j = P_j V_j (M=128,N=64,K=128) into TMEM O[j%2]
 //   warp 2   TMEM allocator
 //   warps 4-11 softmax, two warps per query row: warp w reads TMEM lanes
-//            32*(w%4).. (its 32 rows) and column half (w-4)/4 -- 64 keys of S_j,
-//            32 columns of O_j.  The two halves exchange their row maxima
-//            through shared memory (one named barrier per warp pair), keep
-//            partial row sums, write their own 64-key swizzle atom of P_j =
-//            exp2(S_j*scale*log2e - m) (bf16), and accumulate their 32 output
-//            columns O = O * alpha + O_j in registers.  The running max is only
-//            raised when it grows by more than 2^8 (conditional rescaling), so
-//            alpha is 1 on most tiles.  Finally O / l (bf16) and the natural-log
-//            LSE (fp32, for the backward).
+//            32*(w%4).. (its 32 rows) and key half (w-4)/4 -- 64 keys of S_j.
+//            Each key half keeps its own running max and sum and writes its
+//            64-key swizzle atom of P_j = exp2(S_j*scale*log2e - m_half); the
+//            MMA accumulates O_half += P_half V_half in TMEM (two K=64 chains),
+//            so there is no per-tile exchange between the halves and no O in
+//            registers.  A half's max is only raised when it grows by more than
+//            2^8 (conditional rescaling); then that warp rescales its O_half
+//            rows in TMEM (tcgen05.ld / st) before releasing P_j.  Per unit the
+//            halves exchange (m, l) once and combine the two accumulators into
+//            O / l (bf16) and the natural-log LSE (fp32, for the backward).
 // head_dim is 64 (one 128-byte swizzle row).
 #include "common.cuh"
 #include "../../include/dawnpiper.h"
@@ -93,6 +94,22 @@ __device__ __forceinline__ void regs_inc() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
 }
 
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_wait() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -110,8 +127,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* s_empty = s_full + 2;           // [2]
   uint64_t* p_full = s_empty + 2;           // [2]
   uint64_t* p_empty = p_full + 2;           // [2]
-  uint64_t* o_full = p_empty + 2;           // [2]
-  uint64_t* o_empty = o_full + 2;           // [2]
+  uint64_t* pv_done = p_empty + 2;          // one phase per KV tile
+  uint64_t* o_empty = pv_done + 1;          // [2] by unit parity
   uint64_t* q_empty = o_empty + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
 
@@ -142,9 +159,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&s_empty[i], 8);  // one arrival per softmax warp
       mbar_init(&p_full[i], 8);
       mbar_init(&p_empty[i], 1);
-      mbar_init(&o_full[i], 1);
       mbar_init(&o_empty[i], 8);
     }
+    mbar_init(pv_done, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -153,7 +170,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
-  // TMEM columns: S[0] 0..127, S[1] 128..255, O[0] 256..319, O[1] 320..383
+  // TMEM columns: S[0] 0..127, S[1] 128..255; O[unit parity][key half] at
+  // 256 + 128 * parity + 64 * half (64 columns each).  Each key half keeps its
+  // own running max: O_half accumulates P_half V_half in TMEM (rescaled in
+  // place on the rare tiles where that half's max grows by more than 2^8), and
+  // the halves are combined once per unit.
 
   if (warp == 0) {
     if (lane == 0) {
@@ -177,29 +198,34 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   } else if (warp == 1) {
     // S = Q K^T: A = Q (K-major, K = d), B = K_j (K-major over d)
     constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
-    // O = P V: A = P (K-major over keys: two 64-key atoms), B = V_j (MN-major: d contiguous)
+    // O_half += P_half V_half: A = P key-half atom (K-major, 64 keys), B = V rows of that
+    // half (MN-major: d contiguous)
     constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);
-    auto issue_o = [&](int j) {
-      const int i = j & 1;
-      mbar_wait(&p_full[i], (j >> 1) & 1);
-      mbar_wait(&o_empty[i], ((j >> 1) & 1) ^ 1);
+    // PV of global tile t (issued one tile late); first / ub describe t's unit
+    auto issue_pv = [&](int t, bool first, int ub, int ucount) {
+      const int i = t & 1;
+      mbar_wait(&p_full[i], (t >> 1) & 1);
+      if (first) mbar_wait(&o_empty[ub], ((ucount >> 1) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
-        const int st = j % kKVStages;
+        const int st = t % kKVStages;
         const uint32_t pa = smem_u32(sP + i * kPBytes), vb = smem_u32(sV + st * kTileBytes);
 #pragma unroll
         for (int k = 0; k < kTile / 16; ++k) {
           const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024);
           const uint64_t bd = smem_desc_sw128(vb + k * 2048, kD * 128, 1024);
-          umma_bf16(tmem + 256 + i * 64, ad, bd, idesc_o, k > 0 ? 1u : 0u);
+          umma_bf16(tmem + 256 + ub * 128 + (k >> 2) * 64, ad, bd, idesc_o,
+                    (first && (k & 3) == 0) ? 0u : 1u);
         }
-        umma_commit(&o_full[i]);
         umma_commit(&p_empty[i]);
         umma_commit(&kv_empty[st]);
+        umma_commit(pv_done);
       }
       __syncwarp();
     };
     int g = 0, uc = 0;
+    bool prev_first = false;
+    int prev_ub = 0, prev_uc = 0;
     for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
       int qt, h, bb;
       decode(u, qt, h, bb);
@@ -222,46 +248,43 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (j == n_kv - 1) umma_commit(q_empty);  // Q is free once the unit's S MMAs ran
         }
         __syncwarp();
-        if (g >= 1) issue_o(g - 1);
+        if (g >= 1) issue_pv(g - 1, prev_first, prev_ub, prev_uc);
+        prev_first = j == 0;
+        prev_ub = uc & 1;
+        prev_uc = uc;
       }
     }
-    if (g >= 1) issue_o(g - 1);
+    if (g >= 1) issue_pv(g - 1, prev_first, prev_ub, prev_uc);
   } else if (warp >= 4) {
-    // ---------------- softmax / correction ----------------
+    // ---------------- softmax ----------------
     const int quarter = warp & 3, half = (warp - 4) >> 2;
     const int r = quarter * 32 + lane;  // query row within the tile (== TMEM lane)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    float* xmax = reinterpret_cast<float*>(tmem_slot + 4);  // [2][128][2] row-max exchange
+    float* xs = reinterpret_cast<float*>(tmem_slot + 4);  // [2 units][128 rows][half][m, l]
     const float sl = p.scale_log2;
-    int gbase = 0;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-    int qt, h, bb;
-    decode(u, qt, h, bb);
-    const int n_kv = kv_tiles(qt), row0 = bb * p.seq;
-    const int q = qt * kTile + r;
-    float ms = -INFINITY;  // running max, scaled log2 units
-    float l = 0.f;         // partial row sum over this half's keys
-    float o[kD / 2];
-#pragma unroll
-    for (int c = 0; c < kD / 2; ++c) o[c] = 0.f;
-    float alpha_prev = 1.f;
-    for (int j = 0; j <= n_kv; ++j) {
-      const int gj = gbase + j;  // CTA-global tile index
-      if (j < n_kv) {
-        const int i = gj & 1;
+    int g = 0, uc = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+      int qt, h, bb;
+      decode(u, qt, h, bb);
+      const int n_kv = kv_tiles(qt), row0 = bb * p.seq, ub = uc & 1;
+      const int q = qt * kTile + r;
+      const uint32_t o_half = tmem + 256 + ub * 128 + half * 64 + lane_off;
+      float ms = -INFINITY;  // this key half's running max, scaled log2 units
+      float l = 0.f;         // this key half's running sum
+      for (int j = 0; j < n_kv; ++j) {
+        const int gj = g + j, i = gj & 1;
         const int k0 = j * kTile + half * 64;
         const bool mask = (j + 1) * kTile > p.seq || (p.causal && j == qt);
         mbar_wait(&s_full[i], (gj >> 1) & 1);
         tc_fence_after();
         float s[64];
         {
-          // both 32-column loads in flight, one wait
-          uint32_t u[64];
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + lane_off, u);
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, u + 32);
+          uint32_t uu[64];
+          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + lane_off, uu);
+          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, uu + 32);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(u[e]);
+          for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(uu[e]);
         }
         tc_fence_before();
         __syncwarp();
@@ -276,10 +299,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float mx = s[0];
 #pragma unroll
         for (int c = 1; c < 64; ++c) mx = fmaxf(mx, s[c]);
-        float* xm = xmax + (gj & 1) * 256 + r * 2;
-        xm[half] = mx;
-        pair_sync(quarter);
-        mx = fmaxf(xm[0], xm[1]) * sl;  // row max over all 128 keys (scaled)
+        mx *= sl;
         float alpha = 1.f;
         if (mx > ms + kRescaleLog2 || ms == -INFINITY) {
           alpha = (ms == -INFINITY) ? 0.f : ex2(ms - mx);
@@ -310,64 +330,67 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         l = l * alpha + (sum2.x + sum2.y);
         fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[i]);
-        // accumulate the previous O tile with its own correction factor
-        if (j >= 1) {
-          const int pi = (gj - 1) & 1;
-          mbar_wait(&o_full[pi], ((gj - 1) >> 1) & 1);
-          tc_fence_after();
-          uint32_t u[32];
-          tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + half * 32 + lane_off, u);
-          tmem_ld_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&o_empty[pi]);
+        if (j > 0) {
+          // O_half holds tiles < j once PV(j-1) is done; rescale rows whose max grew
+          mbar_wait(pv_done, (gj - 1) & 1);
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            tc_fence_after();
+            uint32_t ou[64];
+            tmem_ld_32x32b_x32(o_half, ou);
+            tmem_ld_32x32b_x32(o_half + 32, ou + 32);
+            tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; e += 2) {
-            const float2 t = fma2(make_float2(o[e], o[e + 1]), make_float2(alpha_prev, alpha_prev),
-                                  make_float2(__uint_as_float(u[e]), __uint_as_float(u[e + 1])));
-            o[e] = t.x;
-            o[e + 1] = t.y;
+            for (int e = 0; e < 64; ++e) ou[e] = __float_as_uint(__uint_as_float(ou[e]) * alpha);
+            tmem_st_32x32b_x32(o_half, ou);
+            tmem_st_32x32b_x32(o_half + 32, ou + 32);
+            tmem_st_wait();
           }
         }
-        alpha_prev = alpha;
-      } else {
-        const int pi = (gj - 1) & 1;
-        mbar_wait(&o_full[pi], ((gj - 1) >> 1) & 1);
-        tc_fence_after();
-        uint32_t u[32];
-        tmem_ld_32x32b_x32(tmem + 256 + pi * 64 + half * 32 + lane_off, u);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] = fmaf(o[e], alpha_prev, __uint_as_float(u[e]));
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&o_empty[pi]);  // the buffer serves the next unit
+        if (lane == 0) mbar_arrive(&p_full[i]);
       }
-    }
-    gbase += n_kv;
-    // combine the two halves' row sums
-    float* xs = xmax + 512 + r * 2;
-    xs[half] = l;
-    pair_sync(quarter);
-    l = xs[0] + xs[1];
-    if (q < p.seq) {
-      const float inv = l > 0.f ? 1.f / l : 0.f;
-      __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + half * 32;
+      // ---- unit epilogue: combine the key halves ----
+      mbar_wait(pv_done, (g + n_kv - 1) & 1);
+      tc_fence_after();
+      float* xm = xs + ub * 512 + r * 4;
+      xm[half * 2] = ms;
+      xm[half * 2 + 1] = l;
+      pair_sync(quarter);
+      const float m0 = xm[0], l0 = xm[1], m1 = xm[2], l1 = xm[3];
+      const float m = fmaxf(m0, m1);
+      const float a0 = m0 == -INFINITY ? 0.f : ex2(m0 - m), a1 = m1 == -INFINITY ? 0.f : ex2(m1 - m);
+      const float lt = l0 * a0 + l1 * a1;
+      // this warp writes output columns half*32.. from both halves' accumulators
+      uint32_t o0[32], o1[32];
+      tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + half * 32 + lane_off, o0);
+      tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + 64 + half * 32 + lane_off, o1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[ub]);
+      if (q < p.seq) {
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        const float s0 = a0 * inv, s1 = a1 * inv;
+        __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + half * 32;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint4 w;
-        w.x = pack_bf16(o[c * 8 + 0] * inv, o[c * 8 + 1] * inv);
-        w.y = pack_bf16(o[c * 8 + 2] * inv, o[c * 8 + 3] * inv);
-        w.z = pack_bf16(o[c * 8 + 4] * inv, o[c * 8 + 5] * inv);
-        w.w = pack_bf16(o[c * 8 + 6] * inv, o[c * 8 + 7] * inv);
-        reinterpret_cast<uint4*>(op)[c] = w;
+        for (int c = 0; c < 4; ++c) {
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            v[e] = fmaf(__uint_as_float(o0[c * 8 + e]), s0, __uint_as_float(o1[c * 8 + e]) * s1);
+          uint4 w;
+          w.x = pack_bf16(v[0], v[1]);
+          w.y = pack_bf16(v[2], v[3]);
+          w.z = pack_bf16(v[4], v[5]);
+          w.w = pack_bf16(v[6], v[7]);
+          reinterpret_cast<uint4*>(op)[c] = w;
+        }
+        // natural-log LSE of scale * S:  (m + log2 l) / log2(e)
+        if (half == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (m + log2f(lt)) / kLog2e;
       }
-      // natural-log LSE of scale * S:  (m + log2 l) / log2(e)
-      if (half == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (ms + log2f(l)) / kLog2e;
+      g += n_kv;
     }
-    }  // units
   }
   tc_fence_before();
   __syncthreads();
@@ -428,7 +451,8 @@ int map_2d_f32(CUtensorMap* map, const void* ptr, long long rows, long long cols
   return 0;
 }
 
-constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256 + 768 * 4;
+// + 256 B of barriers / TMEM slot, then the per-unit (m, l) exchange [2][128][2][2] f32
+constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256 + 1024 * 4;
 
 }  // namespace
 
