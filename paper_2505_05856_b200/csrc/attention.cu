@@ -138,8 +138,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const long long units = bh * n_kv_all;
   // unit -> (query tile, head, batch); query tiles outermost, longest first
   auto decode = [&](long long u, int& qt, int& h, int& bb) {
-    const int qi = (int)(u / bh);
-    const long long r = u - (long long)qi * bh;
+    // non-causal: query tiles fastest (concurrent CTAs share a head's K / V in
+    // L2); causal: query tiles outermost, longest first (balances the CTAs)
+    int qi;
+    long long r;
+    if (p.causal) {
+      qi = (int)(u / bh);
+      r = u - (long long)qi * bh;
+    } else {
+      qi = (int)(u % n_kv_all);
+      r = u / n_kv_all;
+    }
     qt = p.causal ? n_kv_all - 1 - qi : qi;
     h = (int)(r % p.heads);
     bb = (int)(r / p.heads);
@@ -457,8 +466,11 @@ constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes +
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// Backward, one CTA per (batch, head, 128-key tile) -- K_j, V_j stay in smem
-// while the CTA walks the query tiles i (causal: i >= j):
+// Backward: persistent, one CTA per SM walking units (batch, head, 128-key
+// tile) -- K_j, V_j stay in smem while the CTA walks the query tiles i
+// (causal: i >= j); barrier phases run on CTA-global counters, the dV / dK
+// drain of a unit runs on the dQ warpgroup while the softmax warps start the
+// next unit:
 //   S = Q_i K_j^T, dP = dO_i V_j^T                  (TMEM, M = queries)
 //   P = exp(scale*S - lse), dS = scale * P * (dP - D_i)   (softmax warps ->
 //       bf16 in 128-byte swizzled smem, double-buffered)
@@ -482,7 +494,7 @@ namespace {
 constexpr int kBwdThreads = 512;
 
 struct AttnBwdParams {
-  int seq, heads, H;
+  int batch, seq, heads, H;
   float scale, scale_log2;
   int causal;
   const float* lse;  // [b, heads, s]
@@ -528,15 +540,40 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dq_full = ds_empty + 2;  // [2] (dQ is double-buffered in TMEM)
   uint64_t* dq_empty = dq_full + 2;  // [2]
   uint64_t* dkv_full = dq_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_full + 1);
+  uint64_t* kv_empty = dkv_full + 1;   // K/V smem free for the next unit
+  uint64_t* dkv_empty = kv_empty + 1;  // dV/dK TMEM drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int kt = blockIdx.x, h = blockIdx.y, bb = blockIdx.z;
-  const int k0 = kt * kTile;
   const int n_q = (p.seq + kTile - 1) / kTile;
-  const int i0 = p.causal ? kt : 0;
-  const int n_it = n_q - i0;
-  const int row0 = bb * p.seq;
+  const long long bh = (long long)p.batch * p.heads;
+  const long long units = bh * n_q;
+  // unit -> (key tile, head, batch).  Every barrier phase below runs on CTA-global counters
+  // (units uc, query iterations G) so a unit's tail overlaps the next one.
+  struct Unit {
+    int kt, h, bb, k0, i0, n_it, row0;
+  };
+  auto decode = [&](long long u) {
+    Unit w;
+    // non-causal: key tiles fastest, so concurrently running CTAs walk the same
+    // (batch, head)'s query / dO tiles, which then stay in L2; causal: key tiles
+    // outermost, ascending -- the longest units first balance the CTAs
+    long long r;
+    if (p.causal) {
+      w.kt = (int)(u / bh);
+      r = u - (long long)w.kt * bh;
+    } else {
+      w.kt = (int)(u % n_q);
+      r = u / n_q;
+    }
+    w.h = (int)(r % p.heads);
+    w.bb = (int)(r / p.heads);
+    w.k0 = w.kt * kTile;
+    w.i0 = p.causal ? w.kt : 0;
+    w.n_it = n_q - w.i0;
+    w.row0 = w.bb * p.seq;
+    return w;
+  };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_qkv);
@@ -545,6 +582,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   if (warp == 1 && lane == 0) {
     mbar_init(kv_full, 1);
+    mbar_init(kv_empty, 1);
     mbar_init(sp_loaded, 8);
     mbar_init(p_empty, 1);
     for (int s = 0; s < 2; ++s) {
@@ -559,6 +597,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       mbar_init(&dq_empty[s], 4);
     }
     mbar_init(dkv_full, 1);
+    mbar_init(dkv_empty, 4);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -567,38 +606,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
-  if (p.trace && threadIdx.x == 0) {
-    const long long c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    uint64_t gt;
-    uint32_t smid;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    p.trace[c_ * 64 + 60] = (long long)gt;
-    p.trace[c_ * 64 + 62] = smid;
-    p.trace[c_ * 64 + 63] = clock64();
-  }
   // TMEM columns: S 0..127, dP 128..255, dV 256..319, dK 320..383, dQ[2] 384..511
 
   if (warp < 4) {
     regs_dec<56>();
     if (warp == 0 && lane == 0) {
-      mbar_expect_tx(kv_full, 2 * kTileBytes);
-      tma_load_2d(sK, &tm_qkv, kv_full, p.H + h * kD, row0 + k0);
-      tma_load_2d(sV, &tm_qkv, kv_full, 2 * p.H + h * kD, row0 + k0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, i = i0 + it;
-        mbar_wait(&q_empty[st], ((it >> 1) & 1) ^ 1);
-        mbar_expect_tx(&q_full[st], 2 * kTileBytes);
-        tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], h * kD, row0 + i * kTile);
-        tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], h * kD, row0 + i * kTile);
+      int G = 0, uc = 0;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+        const Unit w = decode(u);
+        mbar_wait(kv_empty, (uc & 1) ^ 1);
+        mbar_expect_tx(kv_full, 2 * kTileBytes);
+        tma_load_2d(sK, &tm_qkv, kv_full, p.H + w.h * kD, w.row0 + w.k0);
+        tma_load_2d(sV, &tm_qkv, kv_full, 2 * p.H + w.h * kD, w.row0 + w.k0);
+        for (int it = 0; it < w.n_it; ++it, ++G) {
+          const int st = G & 1, i = w.i0 + it;
+          mbar_wait(&q_empty[st], ((G >> 1) & 1) ^ 1);
+          mbar_expect_tx(&q_full[st], 2 * kTileBytes);
+          tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], w.h * kD, w.row0 + i * kTile);
+          tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], w.h * kD, w.row0 + i * kTile);
+        }
       }
     } else if (warp == 1) {
       constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // S, dP
       constexpr uint32_t id_kv = idesc_bf16(128, 64, 1, 1);   // dV, dK: A^T and B MN-major
       constexpr uint32_t id_q = idesc_bf16(128, 64, 0, 1);    // dQ: dS K-major, K_j MN-major
-      auto issue_sdp = [&](int it) {
-        const int st = it & 1;
-        mbar_wait(&q_full[st], (it >> 1) & 1);
+      auto issue_sdp = [&](int G) {
+        const int st = G & 1;
+        mbar_wait(&q_full[st], (G >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
@@ -615,235 +649,234 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
       };
-      ATTN_STAMP(0);
-      mbar_wait(kv_full, 0);
-      ATTN_STAMP(1);
-      if (n_it > 0) issue_sdp(0);
-      for (int it = 0; it < n_it; ++it) {
-        const int st = it & 1, b = it & 1;
-        mbar_wait(sp_loaded, it & 1);  // softmax holds S/dP(it) in registers
-        if (it + 1 < n_it) issue_sdp(it + 1);
-        mbar_wait(&ds_full[b], (it >> 1) & 1);
-        ATTN_STAMP(44 + it * 4);
-        tc_fence_after();
-        const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS + b * kPBytes);
-        const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
-        const uint32_t kb = smem_u32(sK);
-        if (lane == 0) {
-          // dV += P^T dO (K = queries: P read MN-major, two 64-key atoms 16 KB apart)
+      int G = 0, uc = 0;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+        const Unit w = decode(u);
+        mbar_wait(kv_full, uc & 1);
+        issue_sdp(G);
+        // the previous unit's dV / dK must have been drained before this unit's first
+        mbar_wait(dkv_empty, (uc & 1) ^ 1);
+        for (int it = 0; it < w.n_it; ++it, ++G) {
+          const int st = G & 1, b = G & 1;
+          mbar_wait(sp_loaded, G & 1);  // softmax holds S/dP(G) in registers
+          if (it + 1 < w.n_it) issue_sdp(G + 1);
+          mbar_wait(&ds_full[b], (G >> 1) & 1);
+          tc_fence_after();
+          const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS + b * kPBytes);
+          const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
+          const uint32_t kb = smem_u32(sK);
+          if (lane == 0) {
+            // dV += P^T dO (K = queries: P read MN-major, two 64-key atoms 16 KB apart)
 #pragma unroll
-          for (int k = 0; k < kTile / 16; ++k)
-            umma_bf16(tmem + 256, smem_desc_sw128(pa + k * 2048, kPBytes / 2, 1024),
-                      smem_desc_sw128(doa + k * 2048, kD * 128, 1024), id_kv,
-                      (it > 0 || k > 0) ? 1u : 0u);
-          umma_commit(p_empty);
+            for (int k = 0; k < kTile / 16; ++k)
+              umma_bf16(tmem + 256, smem_desc_sw128(pa + k * 2048, kPBytes / 2, 1024),
+                        smem_desc_sw128(doa + k * 2048, kD * 128, 1024), id_kv,
+                        (it > 0 || k > 0) ? 1u : 0u);
+            umma_commit(p_empty);
+          }
+          __syncwarp();
+          mbar_wait(&dq_empty[b], ((G >> 1) & 1) ^ 1);
+          tc_fence_after();
+          if (lane == 0) {
+            // dQ = dS K_j (K = keys: dS K-major, K_j MN-major)
+#pragma unroll
+            for (int k = 0; k < kTile / 16; ++k)
+              umma_bf16(tmem + 384 + b * 64,
+                        smem_desc_sw128(dsa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024),
+                        smem_desc_sw128(kb + k * 2048, kD * 128, 1024), id_q, k > 0 ? 1u : 0u);
+            umma_commit(&dq_full[b]);
+            // dK += dS^T Q
+#pragma unroll
+            for (int k = 0; k < kTile / 16; ++k)
+              umma_bf16(tmem + 320, smem_desc_sw128(dsa + k * 2048, kPBytes / 2, 1024),
+                        smem_desc_sw128(qa + k * 2048, kD * 128, 1024), id_kv,
+                        (it > 0 || k > 0) ? 1u : 0u);
+            umma_commit(&ds_empty[b]);
+            umma_commit(&q_empty[st]);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        mbar_wait(&dq_empty[b], ((it >> 1) & 1) ^ 1);
-        ATTN_STAMP(45 + it * 4);
-        tc_fence_after();
         if (lane == 0) {
-          // dQ = dS K_j (K = keys: dS K-major, K_j MN-major)
-#pragma unroll
-          for (int k = 0; k < kTile / 16; ++k)
-            umma_bf16(tmem + 384 + b * 64,
-                      smem_desc_sw128(dsa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024),
-                      smem_desc_sw128(kb + k * 2048, kD * 128, 1024), id_q, k > 0 ? 1u : 0u);
-          umma_commit(&dq_full[b]);
-          // dK += dS^T Q
-#pragma unroll
-          for (int k = 0; k < kTile / 16; ++k)
-            umma_bf16(tmem + 320, smem_desc_sw128(dsa + k * 2048, kPBytes / 2, 1024),
-                      smem_desc_sw128(qa + k * 2048, kD * 128, 1024), id_kv,
-                      (it > 0 || k > 0) ? 1u : 0u);
-          umma_commit(&ds_empty[b]);
-          umma_commit(&q_empty[st]);
+          umma_commit(dkv_full);
+          umma_commit(kv_empty);  // every MMA reading K / V of this unit has run
         }
         __syncwarp();
       }
-      if (lane == 0) umma_commit(dkv_full);
-      __syncwarp();
     }
   } else if (warp < 12) {
     regs_inc<184>();
     // two warps per TMEM lane quarter: warp w owns rows 32*(w%4).. and key
-    // half (w-4)/4 (64 keys of S / dP; 32 columns of dV / dK at the end)
+    // half (w-4)/4 (64 keys of S / dP)
     const int quarter = warp & 3, half = (warp - 4) >> 2;
-    const int r = quarter * 32 + lane;  // query row (S, dP) / key row (dV, dK)
+    const int r = quarter * 32 + lane;  // query row
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const float lse_scale = 1.4426950408889634f;
     const float sl = p.scale_log2, sc = p.scale;
-    // per-row lse / D, loaded one query tile ahead (their latency is not hidden otherwise)
-    const float* lse_row = p.lse + ((long long)bb * p.heads + h) * p.seq;
-    const float* d_row = p.D + ((long long)bb * p.heads + h) * p.seq;
-    auto row_stats = [&](int it, float& l2, float& dq) {
-      const int qq = (i0 + it) * kTile + r;
-      const bool ok = it < n_it && qq < p.seq;
-      l2 = ok ? lse_row[qq] : 0.f;
-      dq = ok ? d_row[qq] : 0.f;
-    };
-    float lse_next, d_next;
-    row_stats(0, lse_next, d_next);
-    for (int it = 0; it < n_it; ++it) {
-      const int i = i0 + it;
-      const int q = i * kTile + r;
-      const bool qok = q < p.seq;
-      const float lse2 = lse_next * lse_scale;
-      const float Dq = d_next * sc;
-      row_stats(it + 1, lse_next, d_next);
-      const bool mask = !qok || k0 + kTile > p.seq || (p.causal && i == kt);
-      const int pb = it & 1;
-      uint8_t* tdS = sdS + pb * kPBytes;
-      if (warp == 4) ATTN_STAMP(2 + it * 8);
-      mbar_wait(sp_full, it & 1);
-      if (warp == 4) ATTN_STAMP(3 + it * 8);
-      tc_fence_after();
-      uint32_t us[64], ud[64];
-      tmem_ld_32x32b_x32(tmem + half * 64 + lane_off, us);
-      tmem_ld_32x32b_x32(tmem + half * 64 + 32 + lane_off, us + 32);
-      tmem_ld_32x32b_x32(tmem + 128 + half * 64 + lane_off, ud);
-      tmem_ld_32x32b_x32(tmem + 128 + half * 64 + 32 + lane_off, ud + 32);
-      tmem_ld_wait();
-      if (warp == 4) ATTN_STAMP(4 + it * 8);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(sp_loaded);  // the MMA may overwrite S/dP now
-      mbar_wait(&ds_empty[pb], ((it >> 1) & 1) ^ 1);
-      if (warp == 4) ATTN_STAMP(5 + it * 8);
-      uint4 pk[8];  // P row chunk, packed bf16 (stored once dV(it-1) released sP)
-      // the key mask only exists on boundary tiles: two straight-line copies
-      auto tile = [&](auto masked) {
-        constexpr bool kMask = decltype(masked)::value;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this half's 64-key atom
-          float pv[8], dsv[8];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
-            const float2 a = fma2(make_float2(__uint_as_float(us[c * 8 + e]), __uint_as_float(us[c * 8 + e + 1])),
-                                  make_float2(sl, sl), make_float2(-lse2, -lse2));
-            float2 pr = make_float2(ex2(a.x), ex2(a.y));
-            if constexpr (kMask) {
-              const int key = k0 + half * 64 + c * 8 + e;
-              pr.x = (qok && key < p.seq && (!p.causal || key <= q)) ? pr.x : 0.f;
-              pr.y = (qok && key + 1 < p.seq && (!p.causal || key + 1 <= q)) ? pr.y : 0.f;
-            }
-            pv[e] = pr.x;
-            pv[e + 1] = pr.y;
-            const float2 ds = mul2(pr, fma2(make_float2(__uint_as_float(ud[c * 8 + e]), __uint_as_float(ud[c * 8 + e + 1])),
-                                            make_float2(sc, sc), make_float2(-Dq, -Dq)));
-            dsv[e] = ds.x;
-            dsv[e + 1] = ds.y;
-          }
-          pk[c].x = pack_bf16(pv[0], pv[1]);
-          pk[c].y = pack_bf16(pv[2], pv[3]);
-          pk[c].z = pack_bf16(pv[4], pv[5]);
-          pk[c].w = pack_bf16(pv[6], pv[7]);
-          uint4 b2;
-          b2.x = pack_bf16(dsv[0], dsv[1]);
-          b2.y = pack_bf16(dsv[2], dsv[3]);
-          b2.z = pack_bf16(dsv[4], dsv[5]);
-          b2.w = pack_bf16(dsv[6], dsv[7]);
-          *reinterpret_cast<uint4*>(tdS + half * (kPBytes / 2) + sw128(r, c)) = b2;
-        }
+    int G = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit w = decode(u);
+      const int kt = w.kt, k0 = w.k0, i0 = w.i0, n_it = w.n_it;
+      // per-row lse / D, loaded one query tile ahead (their latency is not hidden otherwise)
+      const float* lse_row = p.lse + ((long long)w.bb * p.heads + w.h) * p.seq;
+      const float* d_row = p.D + ((long long)w.bb * p.heads + w.h) * p.seq;
+      auto row_stats = [&](int it, float& l2, float& dq) {
+        const int qq = (i0 + it) * kTile + r;
+        const bool ok = it < n_it && qq < p.seq;
+        l2 = ok ? lse_row[qq] : 0.f;
+        dq = ok ? d_row[qq] : 0.f;
       };
-      if (mask) tile(std::true_type{});
-      else tile(std::false_type{});
-      if (warp == 4) ATTN_STAMP(6 + it * 8);
-      mbar_wait(p_empty, (it & 1) ^ 1);
-      if (warp == 4) ATTN_STAMP(7 + it * 8);
+      float lse_next, d_next;
+      row_stats(0, lse_next, d_next);
+      for (int it = 0; it < n_it; ++it, ++G) {
+        const int i = i0 + it;
+        const int q = i * kTile + r;
+        const bool qok = q < p.seq;
+        const float lse2 = lse_next * lse_scale;
+        const float Dq = d_next * sc;
+        row_stats(it + 1, lse_next, d_next);
+        const bool mask = !qok || k0 + kTile > p.seq || (p.causal && i == kt);
+        const int pb = G & 1;
+        uint8_t* tdS = sdS + pb * kPBytes;
+        mbar_wait(sp_full, G & 1);
+        tc_fence_after();
+        uint32_t us[64], ud[64];
+        tmem_ld_32x32b_x32(tmem + half * 64 + lane_off, us);
+        tmem_ld_32x32b_x32(tmem + half * 64 + 32 + lane_off, us + 32);
+        tmem_ld_32x32b_x32(tmem + 128 + half * 64 + lane_off, ud);
+        tmem_ld_32x32b_x32(tmem + 128 + half * 64 + 32 + lane_off, ud + 32);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sp_loaded);  // the MMA may overwrite S/dP now
+        mbar_wait(&ds_empty[pb], ((G >> 1) & 1) ^ 1);
+        uint4 pk[8];  // P row chunk, packed bf16 (stored once dV(G-1) released sP)
+        // the key mask only exists on boundary tiles: two straight-line copies
+        auto tile = [&](auto masked) {
+          constexpr bool kMask = decltype(masked)::value;
 #pragma unroll
-      for (int c = 0; c < 8; ++c)
-        *reinterpret_cast<uint4*>(sP + half * (kPBytes / 2) + sw128(r, c)) = pk[c];
-      fence_async_smem();
-      __syncwarp();
-      if (warp == 4) ATTN_STAMP(8 + it * 8);
-      if (lane == 0) mbar_arrive(&ds_full[pb]);
-    }
-    if (warp == 4) ATTN_STAMP(36);
-    // dV, dK of this key tile (TMEM lane = key row)
-    mbar_wait(dkv_full, 0);
-    if (warp == 4) ATTN_STAMP(37);
-    tc_fence_after();
-    const int key = k0 + r;
-    const bool any = n_it > 0;
-    if (key < p.seq) {
-      __nv_bfloat16* dk = p.dqkv + (long long)(row0 + key) * 3 * p.H + p.H + h * kD + half * 32;
-      __nv_bfloat16* dv = p.dqkv + (long long)(row0 + key) * 3 * p.H + 2 * p.H + h * kD + half * 32;
-      uint32_t uv[32], uk[32];
-      tmem_ld_32x32b_x32(tmem + 256 + half * 32 + lane_off, uv);
-      tmem_ld_32x32b_x32(tmem + 320 + half * 32 + lane_off, uk);
-      tmem_ld_wait();
+          for (int c = 0; c < 8; ++c) {  // 16-byte chunk c of this half's 64-key atom
+            float pv[8], dsv[8];
 #pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        uint4 a, b2;
-        float fv[8], fk[8];
+            for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
+              const float2 a = fma2(make_float2(__uint_as_float(us[c * 8 + e]), __uint_as_float(us[c * 8 + e + 1])),
+                                    make_float2(sl, sl), make_float2(-lse2, -lse2));
+              float2 pr = make_float2(ex2(a.x), ex2(a.y));
+              if constexpr (kMask) {
+                const int key = k0 + half * 64 + c * 8 + e;
+                pr.x = (qok && key < p.seq && (!p.causal || key <= q)) ? pr.x : 0.f;
+                pr.y = (qok && key + 1 < p.seq && (!p.causal || key + 1 <= q)) ? pr.y : 0.f;
+              }
+              pv[e] = pr.x;
+              pv[e + 1] = pr.y;
+              const float2 ds = mul2(pr, fma2(make_float2(__uint_as_float(ud[c * 8 + e]), __uint_as_float(ud[c * 8 + e + 1])),
+                                              make_float2(sc, sc), make_float2(-Dq, -Dq)));
+              dsv[e] = ds.x;
+              dsv[e + 1] = ds.y;
+            }
+            pk[c].x = pack_bf16(pv[0], pv[1]);
+            pk[c].y = pack_bf16(pv[2], pv[3]);
+            pk[c].z = pack_bf16(pv[4], pv[5]);
+            pk[c].w = pack_bf16(pv[6], pv[7]);
+            uint4 b2;
+            b2.x = pack_bf16(dsv[0], dsv[1]);
+            b2.y = pack_bf16(dsv[2], dsv[3]);
+            b2.z = pack_bf16(dsv[4], dsv[5]);
+            b2.w = pack_bf16(dsv[6], dsv[7]);
+            *reinterpret_cast<uint4*>(tdS + half * (kPBytes / 2) + sw128(r, c)) = b2;
+          }
+        };
+        if (mask) tile(std::true_type{});
+        else tile(std::false_type{});
+        mbar_wait(p_empty, (G & 1) ^ 1);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          fv[e] = any ? __uint_as_float(uv[w * 8 + e]) : 0.f;
-          fk[e] = any ? __uint_as_float(uk[w * 8 + e]) : 0.f;
-        }
-        a.x = pack_bf16(fv[0], fv[1]); a.y = pack_bf16(fv[2], fv[3]);
-        a.z = pack_bf16(fv[4], fv[5]); a.w = pack_bf16(fv[6], fv[7]);
-        b2.x = pack_bf16(fk[0], fk[1]); b2.y = pack_bf16(fk[2], fk[3]);
-        b2.z = pack_bf16(fk[4], fk[5]); b2.w = pack_bf16(fk[6], fk[7]);
-        reinterpret_cast<uint4*>(dv)[w] = a;
-        reinterpret_cast<uint4*>(dk)[w] = b2;
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(sP + half * (kPBytes / 2) + sw128(r, c)) = pk[c];
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ds_full[pb]);
       }
     }
   } else {
     regs_dec<88>();
-    // dQ drain: warp w reads TMEM lanes 32*(w%4).. (its 32 query rows), all 64 columns
+    // dQ drain per query tile: warp w reads TMEM lanes 32*(w%4).. (its 32 query
+    // rows), all 64 columns -> swizzled f32 staging -> TMA reduce-add; and per
+    // unit the dV / dK drain (TMEM lane = key row) -> bf16 dqkv, off the
+    // softmax warps (they start the next unit meanwhile)
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const bool issuer = warp == 12 && lane == 0;
-    for (int it = 0; it < n_it; ++it) {
-      const int b = it & 1;
-      mbar_wait(&dq_full[b], (it >> 1) & 1);
-      tc_fence_after();
-      uint32_t u[64];
-      tmem_ld_32x32b_x32(tmem + 384 + b * 64 + lane_off, u);
-      tmem_ld_32x32b_x32(tmem + 384 + b * 64 + 32 + lane_off, u + 32);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&dq_empty[b]);
-      // the previous reduce must have finished reading the staging tile
-      if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync 6, 128;" ::: "memory");
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(sdQ + hh * (kPBytes / 2) + sw128(r, c)) =
-              make_uint4(u[hh * 32 + c * 4], u[hh * 32 + c * 4 + 1], u[hh * 32 + c * 4 + 2],
-                         u[hh * 32 + c * 4 + 3]);
-      fence_async_smem();
-      asm volatile("bar.sync 6, 128;" ::: "memory");
-      if (issuer) {
-        // rows past seq carry zero (P = dS = 0 there), rows past the tensor are clipped
+    int G = 0, uc = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+      const Unit w = decode(u);
+      for (int it = 0; it < w.n_it; ++it, ++G) {
+        const int b = G & 1;
+        mbar_wait(&dq_full[b], (G >> 1) & 1);
+        tc_fence_after();
+        uint32_t uq[64];
+        tmem_ld_32x32b_x32(tmem + 384 + b * 64 + lane_off, uq);
+        tmem_ld_32x32b_x32(tmem + 384 + b * 64 + 32 + lane_off, uq + 32);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dq_empty[b]);
+        // the previous reduce must have finished reading the staging tile
+        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("bar.sync 6, 128;" ::: "memory");
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh)
-          asm volatile(
-              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
-              " [%0, {%2, %3}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&tm_dq)),
-              "r"(smem_u32(sdQ + hh * (kPBytes / 2))), "r"(h * kD + hh * 32),
-              "r"(row0 + (i0 + it) * kTile)
-              : "memory");
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            *reinterpret_cast<uint4*>(sdQ + hh * (kPBytes / 2) + sw128(r, c)) =
+                make_uint4(uq[hh * 32 + c * 4], uq[hh * 32 + c * 4 + 1], uq[hh * 32 + c * 4 + 2],
+                           uq[hh * 32 + c * 4 + 3]);
+        fence_async_smem();
+        asm volatile("bar.sync 6, 128;" ::: "memory");
+        if (issuer) {
+          // rows past seq carry zero (P = dS = 0 there), rows past the tensor are clipped
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            asm volatile(
+                "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
+                " [%0, {%2, %3}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&tm_dq)),
+                "r"(smem_u32(sdQ + hh * (kPBytes / 2))), "r"(w.h * kD + hh * 32),
+                "r"(w.row0 + (w.i0 + it) * kTile)
+                : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
+      // dV, dK of this key tile (TMEM lane = key row), 32 columns at a time
+      mbar_wait(dkv_full, uc & 1);
+      tc_fence_after();
+      const int key = w.k0 + r;
+#pragma unroll 1
+      for (int part = 0; part < 4; ++part) {  // dV cols 0-31, 32-63, dK cols 0-31, 32-63
+        uint32_t uv[32];
+        tmem_ld_32x32b_x32(tmem + 256 + part * 32 + lane_off, uv);
+        tmem_ld_wait();
+        if (key < p.seq) {
+          const int which = part >> 1;  // 0: dV, 1: dK
+          __nv_bfloat16* dst = p.dqkv + (long long)(w.row0 + key) * 3 * p.H +
+                               (which ? p.H : 2 * p.H) + w.h * kD + (part & 1) * 32;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 a;
+            a.x = pack_bf16(__uint_as_float(uv[c * 8 + 0]), __uint_as_float(uv[c * 8 + 1]));
+            a.y = pack_bf16(__uint_as_float(uv[c * 8 + 2]), __uint_as_float(uv[c * 8 + 3]));
+            a.z = pack_bf16(__uint_as_float(uv[c * 8 + 4]), __uint_as_float(uv[c * 8 + 5]));
+            a.w = pack_bf16(__uint_as_float(uv[c * 8 + 6]), __uint_as_float(uv[c * 8 + 7]));
+            reinterpret_cast<uint4*>(dst)[c] = a;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dkv_empty);
     }
     if (issuer) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   tc_fence_before();
   __syncthreads();
-  if (p.trace && threadIdx.x == 0) {
-    const long long c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-    uint64_t gt;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    p.trace[c_ * 64 + 61] = (long long)gt;
-    p.trace[c_ * 64 + 59] = clock64();
-  }
   if (warp == 2) {
     tc_fence_after();
     tmem_free<512>(tmem);
@@ -983,6 +1016,7 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
   rc = map_2d_f32(&tdq, dq, rows, H);
   if (rc) return rc;
   AttnBwdParams p{};
+  p.batch = (int)batch;
   p.seq = (int)seq;
   p.heads = (int)heads;
   p.H = (int)H;
@@ -1000,7 +1034,15 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
                                         kBwdSmem));
     set = true;
   }
-  dim3 grid((unsigned)((seq + kTile - 1) / kTile), (unsigned)heads, (unsigned)batch);
+  static int n_sm_b = 0;
+  if (n_sm_b == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm_b, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sm_b <= 0) n_sm_b = 148;
+  }
+  const long long units = (long long)((seq + kTile - 1) / kTile) * heads * batch;
+  const unsigned grid = (unsigned)std::min<long long>(units, n_sm_b);  // persistent
   DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, td, tdq, p));
   DPN_LAUNCH_CHECK();
   DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel, (unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0, st, 
