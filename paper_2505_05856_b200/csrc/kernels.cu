@@ -28,6 +28,12 @@ __device__ __forceinline__ void load8(const __nv_bfloat16* p, float* f) {
   }
 }
 
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void store8(__nv_bfloat16* p, const float* f) {
   uint4 u;
   u.x = pack_bf16(f[0], f[1]);
@@ -187,13 +193,15 @@ __device__ __forceinline__ void red_add_v4(float* addr, const float* v) {
 //   MODE 0: out0 += sum_r a[r]
 //   MODE 1: out0 += sum_r a[r] * (x[r] - mean[r]) * rstd[r],  out1 += sum_r a[r]
 constexpr int kColThreads = 512;
-constexpr int kColUnroll = 4;
+constexpr int kColUnrollSum = 8;   // MODE 0: rows in flight per lane
+constexpr int kColUnrollLn = 4;    // MODE 1 (two operands per row)
 template <int MODE>
 __global__ void __launch_bounds__(kColThreads) colred_kernel(
     const __nv_bfloat16* __restrict__ a, long long lda, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean, const float* __restrict__ rstd, long long rows, int cols,
     long long rows_per_cta, float* __restrict__ out0, float* __restrict__ out1) {
   pdl_wait();
+  constexpr int kColUnroll = MODE == 0 ? kColUnrollSum : kColUnrollLn;
   __shared__ float part[kColThreads * 8];
   const int nvec = cols >> 3;
   const int cw = min(nvec, 128);
@@ -444,11 +452,14 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
   __shared__ float red[32];
   const int tid = threadIdx.x, nw = blockDim.x >> 5;
   const int nvec = (vocab + 7) >> 3;  // columns >= vocab (pad) are masked out
+  const int nfull = vocab >> 3;       // vectors with all 8 columns < vocab
+  constexpr float kL2e = 1.4426950408889634f;
   for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
     const __nv_bfloat16* src = logits + r * ld;
-    float mx = -INFINITY;
-    // 8 row vectors in flight per thread (the whole 30K-50K row in one or two rounds)
-    constexpr int U = 8;
+    // pass 1: row -> smem, row max on packed bf16 pairs (max is exact in bf16)
+    __nv_bfloat162 mx2 = __floats2bfloat162_rn(-INFINITY, -INFINITY);
+    float mx_tail = -INFINITY;
+    constexpr int U = 8;  // 8 row vectors in flight per thread
     for (int c0 = tid; c0 < nvec; c0 += blockDim.x * U) {
       uint4 u[U];
 #pragma unroll
@@ -461,14 +472,20 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
         const int c = c0 + i * blockDim.x;
         if (c < nvec) {
           reinterpret_cast<uint4*>(row)[c] = u[i];
-          float v[8];
-          load8(reinterpret_cast<const __nv_bfloat16*>(&u[i]), v);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u[i]);
+          if (c < nfull) {
+            mx2 = __hmax2(mx2, __hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])));
+          } else {
+            float v[8];
+            load8(reinterpret_cast<const __nv_bfloat16*>(&u[i]), v);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            if (c * 8 + k < vocab) mx = fmaxf(mx, v[k]);
+            for (int k = 0; k < 8; ++k)
+              if (c * 8 + k < vocab) mx_tail = fmaxf(mx_tail, v[k]);
+          }
         }
       }
     }
+    float mx = fmaxf(fmaxf(__low2float(mx2), __high2float(mx2)), mx_tail);
     mx = warp_max(mx);
     if ((tid & 31) == 0) red[tid >> 5] = mx;
     __syncthreads();
@@ -480,15 +497,25 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
     __syncthreads();
     mx = red[0];
     __syncthreads();
-    float s = 0.f;
+    // pass 2: sum of exp2(x log2e - max log2e), two columns per packed FMA
+    const float mxl = mx * kL2e;
+    float2 s2 = make_float2(0.f, 0.f);
     for (int c = tid; c < nvec; c += blockDim.x) {
       float v[8];
       load8(row + c * 8, v);
+      if (c < nfull) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
-        if (c * 8 + k < vocab) s += __expf(v[k] - mx);
+        for (int k = 0; k < 8; k += 2) {
+          const float2 a = fma2(make_float2(v[k], v[k + 1]), make_float2(kL2e, kL2e), make_float2(-mxl, -mxl));
+          s2 = fma2(make_float2(1.f, 1.f), make_float2(ex2_approx(a.x), ex2_approx(a.y)), s2);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (c * 8 + k < vocab) s2.x += ex2_approx(fmaf(v[k], kL2e, -mxl));
+      }
     }
-    s = warp_sum(s);
+    float s = warp_sum(s2.x + s2.y);
     if ((tid & 31) == 0) red[tid >> 5] = s;
     __syncthreads();
     if (tid < 32) {
@@ -498,21 +525,36 @@ __global__ void __launch_bounds__(512) xent_kernel(const __nv_bfloat16* __restri
     }
     __syncthreads();
     const float sum = red[0];
-    const float inv = 1.f / sum;
+    const float gs = grad_scale / sum;  // dlogit = softmax * grad_scale - onehot * grad_scale
     const int lab = labels[r];
     if (tid == 0) {
       const float xl = __bfloat162float(row[lab]);
       atomicAdd(loss_sum, loss_scale * (logf(sum) + mx - xl));
     }
+    // pass 3: dlogits
     __nv_bfloat16* dst = dlogits + r * ld;
     for (int c = tid; c < nvec; c += blockDim.x) {
       float v[8];
       load8(row + c * 8, v);
+      if (c < nfull) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int col = c * 8 + k;
-        const float pr = col < vocab ? __expf(v[k] - mx) * inv : 0.f;
-        v[k] = col < vocab ? (pr - (col == lab ? 1.f : 0.f)) * grad_scale : 0.f;
+        for (int k = 0; k < 8; k += 2) {
+          const float2 a = fma2(make_float2(v[k], v[k + 1]), make_float2(kL2e, kL2e), make_float2(-mxl, -mxl));
+          const float2 o = mul2(make_float2(ex2_approx(a.x), ex2_approx(a.y)), make_float2(gs, gs));
+          v[k] = o.x;
+          v[k + 1] = o.y;
+        }
+        if (c == (lab >> 3)) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] -= k == (lab & 7) ? grad_scale : 0.f;
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int col = c * 8 + k;
+          const float pr = col < vocab ? ex2_approx(fmaf(v[k], kL2e, -mxl)) * gs : 0.f;
+          v[k] = col < vocab ? pr - (col == lab ? grad_scale : 0.f) : 0.f;
+        }
       }
       store8(dst + c * 8, v);
     }

@@ -362,8 +362,11 @@ def _attn_ref(qkv, b, s, A, causal):
     return o.transpose(1, 2).reshape(b * s, H), lse
 
 
+# the last two cases have more (tile, head, batch) units than SMs: the persistent
+# kernels walk several units per CTA (CTA-global barrier phases, buffer reuse)
 @pytest.mark.parametrize("b,s,A,causal", [(2, 128, 2, False), (2, 512, 3, False), (1, 512, 2, True),
-                                          (3, 64, 2, False), (2, 192, 2, True), (2, 1024, 1, True)])
+                                          (3, 64, 2, False), (2, 192, 2, True), (2, 1024, 1, True),
+                                          (8, 512, 16, False), (4, 1024, 8, True)])
 def test_fused_attention_forward(b, s, A, causal):
     k = K()
     qkv = rnd(b * s, 3 * A * 64, scale=1.5)
@@ -376,8 +379,30 @@ def test_fused_attention_forward(b, s, A, causal):
     assert (lse - lse_ref).abs().max().item() < 2e-2
 
 
+@pytest.mark.parametrize("causal", [False, True])
+def test_fused_attention_forward_rescale(causal):
+    """Keys of later tiles carry far larger logits, so each key half's running
+    max grows by more than 2^8 mid-row: the O accumulators in TMEM are rescaled
+    in place (the rare path of the split-key forward)."""
+    k = K()
+    b, s, A = 2, 512, 4
+    H = A * 64
+    qkv = rnd(b * s, 3 * H, scale=1.0)
+    kv = qkv.view(b, s, 3 * H)
+    for t in range(1, s // 128):  # K rows of tile t scaled up by 2.5^t
+        kv[:, t * 128:(t + 1) * 128, H:2 * H] *= 2.5 ** t
+    out = torch.empty(b * s, H, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, A, s, device="cuda")
+    k.attn_fwd(qkv, out, lse, b, s, A, causal)
+    torch.cuda.synchronize()
+    o_ref, lse_ref = _attn_ref(qkv, b, s, A, causal)
+    close(out, o_ref)
+    assert ((lse - lse_ref).abs() / lse_ref.abs().clamp_min(1)).max().item() < 2e-2
+
+
 @pytest.mark.parametrize("b,s,A,causal", [(2, 128, 2, False), (2, 512, 2, False), (1, 512, 2, True),
-                                          (3, 64, 2, False), (2, 192, 1, True), (1, 1024, 1, True)])
+                                          (3, 64, 2, False), (2, 192, 1, True), (1, 1024, 1, True),
+                                          (8, 512, 16, False), (4, 1024, 8, True)])
 def test_fused_attention_backward(b, s, A, causal):
     k = K()
     H = A * 64
