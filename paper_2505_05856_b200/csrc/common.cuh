@@ -163,6 +163,18 @@ __device__ __forceinline__ void tma_load_4d_pair(void* dst, const CUtensorMap* m
       : "memory");
 }
 
+// 2-CTA TMA load multicast to the CTAs in `mask` (same smem offset in each);
+// each destination's transaction bytes are counted on its pair leader's barrier.
+__device__ __forceinline__ void tma_load_4d_pair_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                    int c0, int c1, int c2, int c3, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      ".multicast::cluster.cta_group::2 [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & 0xFEFFFFFFu), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3), "h"(mask)
+      : "memory");
+}
+
 // ---- tcgen05 ----------------------------------------------------------------------
 
 __device__ __forceinline__ void tc_fence_before() {

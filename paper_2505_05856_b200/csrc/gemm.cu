@@ -80,9 +80,13 @@ constexpr int kEpiStage = 4096;
 constexpr int kEpiBytes = kEpiWarps * 2 * kEpiStage;
 constexpr int kMaxSmem = 232448;  // 227 KB per CTA on sm_100
 
+// CG: CTAs per cluster. 1 = one CTA per tile; 2 = a CTA pair on one 256-row
+// tile (tcgen05 cta_group::2); 4 = two pairs on N-adjacent tiles sharing their
+// A rows through TMA multicast (each CTA fetches half of its A tile from L2).
 template <int BN, int CG>
 struct Cfg {
-  static constexpr int kBRows = BN / CG;  // rows of B this CTA loads (pair: half of N)
+  static constexpr int kPair = CG == 1 ? 1 : 2;
+  static constexpr int kBRows = BN / kPair;  // rows of B this CTA loads (pair: half of N)
   static constexpr int kABytes = BM * BK * 2;
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
@@ -457,9 +461,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nk = (p.K + BK - 1) / BK;
-  // CTA pair (CG == 2): rank 0 leads -- it issues the MMAs and owns the
-  // full / tmem_empty barriers both CTAs' producers and epilogues report to.
-  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0;
+  // CTA pair (CG >= 2): the pair's rank-0 CTA leads -- it issues the MMAs and
+  // owns the full / tmem_empty barriers both CTAs' producers and epilogues
+  // report to.  CG == 4: pair `pr` of the cluster works on N-tile 2*nb + pr.
+  constexpr int kPair = C::kPair;
+  constexpr bool kMc = CG == 4;
+  const uint32_t crank = CG >= 2 ? cluster_ctarank() : 0;
+  const uint32_t rank = crank & 1u;       // rank within the pair
+  const uint32_t pr = crank >> 1;         // pair within the cluster
+  const uint32_t leader = crank & ~1u;    // cluster rank of this pair's leader
+  const uint32_t pair_mask = 0x3u << leader;
   const long long cluster_id = blockIdx.x / CG;
   const long long n_clusters = gridDim.x / CG;
 
@@ -474,19 +485,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < C::kStages; ++s) {
-      mbar_init(&full[s], CG);  // one arrival per producer of the pair
-      mbar_init(&empty[s], 1);
+      mbar_init(&full[s], kPair);  // one arrival per producer of the pair
+      mbar_init(&empty[s], kMc ? 2 : 1);  // multicast: both pairs must release the stage
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], CG * kEpiWarps);  // one arrival per epilogue warp of the pair
+      mbar_init(&tempty[a], kPair * kEpiWarps);  // one arrival per epilogue warp of the pair
     }
     for (int e = 0; e < kEpiWarps; ++e) mbar_init(&rbar[e], 1);
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<C::kTmemCols, CG>(tmem_slot);
+  if (warp == 2) tmem_alloc<C::kTmemCols, kPair>(tmem_slot);
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
+  if constexpr (CG >= 2) cluster_sync_all(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const long long t_start = clock64();
@@ -507,19 +518,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (long long u = cluster_id; u < p.units; u += n_clusters) {
         const Unit w = decode(p, u, nk);
         const int m0 = w.m0 + BM * (int)rank;
-        const int n0 = w.nb * BN + C::kBRows * (int)rank;
+        const int n0 = (w.nb * (kMc ? 2 : 1) + (int)pr) * BN + C::kBRows * (int)rank;
         for (int kb = w.kb0; kb < w.kb1; ++kb) {
           mbar_wait_t(&empty[stage], phase ^ 1, trace_w);
-          if (rank == 0) mbar_expect_tx(&full[stage], CG * C::kStageBytes);
-          else mbar_arrive_remote(&full[stage], 0);
+          if (rank == 0) mbar_expect_tx(&full[stage], kPair * C::kStageBytes);
+          else mbar_arrive_remote(&full[stage], leader);
           uint8_t* a_dst = sA + stage * C::kABytes;
           uint8_t* b_dst = sB + stage * C::kBBytes;
           const int k0 = kb * BK;
           auto load = [&](void* dst, const CUtensorMap* m, int c0, int c2) {
-            if constexpr (CG == 2) tma_load_4d_pair(dst, m, &full[stage], c0, w.z1, c2, w.z2);
+            if constexpr (CG >= 2) tma_load_4d_pair(dst, m, &full[stage], c0, w.z1, c2, w.z2);
             else tma_load_4d(dst, m, &full[stage], c0, w.z1, c2, w.z2);
           };
-          if (!A_MN) {
+          if constexpr (kMc) {
+            // this CTA fetches 64 of its 128 A rows and multicasts them to the
+            // same-rank CTA of the other pair (which fetches the other 64)
+            const uint16_t mc = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
+            if (!A_MN) tma_load_4d_pair_mc(a_dst + pr * 64 * 128, &tmA, &full[stage], k0, w.z1,
+                                           m0 + 64 * (int)pr, w.z2, mc);
+            else tma_load_4d_pair_mc(a_dst + pr * 64 * BK * 2, &tmA, &full[stage], m0 + 64 * (int)pr,
+                                     w.z1, k0, w.z2, mc);
+          } else if (!A_MN) {
             load(a_dst, &tmA, k0, m0);
           } else {
 #pragma unroll
@@ -541,7 +560,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (pair leader only) ----------------
     if (rank == 0) {
-      constexpr uint32_t idesc = idesc_bf16(BM * CG, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      constexpr uint32_t idesc = idesc_bf16(BM * kPair, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       // K-major SW128: rows of 128 B, 8-row atoms 1024 B apart; +32 B per K=16 step.
       // MN-major SW128: 64-element MN atoms BK*128 B apart (LBO), 8-row K groups
       // 1024 B apart (SBO); +16 rows * 128 B = 2048 B per K=16 step.
@@ -567,12 +586,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               const uint64_t ad = smem_desc_sw128(a_addr + k * a_kstep, a_lbo, 1024);
               const uint64_t bd = smem_desc_sw128(b_addr + k * b_kstep, b_lbo, 1024);
               const uint32_t accum = (kb > w.kb0 || k > 0) ? 1u : 0u;
-              if constexpr (CG == 2) umma_bf16_pair(tmem_d, ad, bd, idesc, accum);
+              if constexpr (CG >= 2) umma_bf16_pair(tmem_d, ad, bd, idesc, accum);
               else umma_bf16(tmem_d, ad, bd, idesc, accum);
             }
-            if constexpr (CG == 2) {
-              umma_commit_pair(&empty[stage], 0x3);
-              if (kb == w.kb1 - 1) umma_commit_pair(&tfull[acc], 0x3);
+            if constexpr (CG >= 2) {
+              // multicast: the stage is free only once both pairs consumed it
+              umma_commit_pair(&empty[stage], kMc ? 0xF : pair_mask);
+              if (kb == w.kb1 - 1) umma_commit_pair(&tfull[acc], pair_mask);
             } else {
               umma_commit(&empty[stage]);
               if (kb == w.kb1 - 1) umma_commit(&tfull[acc]);
@@ -602,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t rphase = 0;
     for (long long u = cluster_id; u < p.units; u += n_clusters) {
       const Unit w = decode(p, u, nk);
-      const int n0 = w.nb * BN;
+      const int n0 = (w.nb * (kMc ? 2 : 1) + (int)pr) * BN;
       if (p.tma_epi) {
         const int row_base = w.m0 + BM * (int)rank + lanes;
         // the first residual tile loads while the accumulator is still being built
@@ -619,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          if constexpr (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
+          if constexpr (CG >= 2) mbar_arrive_remote(&tempty[acc], leader);
           else mbar_arrive(&tempty[acc]);
         }
         if (++acc == 2) {
@@ -647,7 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (CG == 2) mbar_arrive_remote(&tempty[acc], 0);
+        if constexpr (CG >= 2) mbar_arrive_remote(&tempty[acc], leader);
         else mbar_arrive(&tempty[acc]);
       }
       if (++acc == 2) {
@@ -665,10 +685,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
+  if constexpr (CG >= 2) cluster_sync_all(); else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_free<C::kTmemCols, CG>(tmem_base);
+    tmem_free<C::kTmemCols, kPair>(tmem_base);
   }
 }
 
@@ -825,8 +845,8 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
   CUtensorMap ta, tb;
   const int Z1 = (int)g->batch1, Z2 = (int)g->batch2;
   int rc;
-  if (!A_MN)
-    rc = make_map(&ta, g->A, g->K, g->M, g->lda, Z1, g->a_s1, Z2, g->a_s2, BM);
+  if (!A_MN)  // multicast clusters fetch A in 64-row halves
+    rc = make_map(&ta, g->A, g->K, g->M, g->lda, Z1, g->a_s1, Z2, g->a_s2, CG == 4 ? 64 : BM);
   else
     rc = make_map(&ta, g->A, g->M, g->K, g->lda, Z1, g->a_s1, Z2, g->a_s2, BK);
   if (rc) return rc;
@@ -848,12 +868,35 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
     if (!rc && p.aux) rc = make_epi_map(&tx, p.aux, g->M, g->N, g->ldc, false);
     if (rc) return rc;
   }
-  p.tile_m = BM * CG;
+  p.tile_m = BM * C::kPair;
   p.tiles_m = (p.M + p.tile_m - 1) / p.tile_m;
   p.tiles_n = (p.N + BN - 1) / BN;
+  if (CG == 4) p.tiles_n = (p.tiles_n + 1) / 2;  // a unit is two N-adjacent tiles
   const long long tiles = (long long)p.tiles_m * p.tiles_n * p.Z;
   const int nk = (p.K + BK - 1) / BK;
-  const int clusters_max = sm_count() / CG;
+  static int clusters_max = 0;  // co-resident clusters of this configuration
+  if (clusters_max == 0) {
+    clusters_max = sm_count() / CG;
+    if (CG > 2) {
+      cudaLaunchConfig_t qc{};
+      qc.gridDim = dim3((unsigned)(sm_count() / CG * CG));
+      qc.blockDim = dim3(kThreads);
+      qc.dynamicSmemBytes = C::kSmem;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = CG;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      qc.attrs = qa;
+      qc.numAttrs = 1;
+      int n = 0;
+      cudaFuncSetAttribute(gemm_kernel<BN, A_MN, B_MN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           C::kSmem);
+      if (cudaOccupancyMaxActiveClusters(&n, gemm_kernel<BN, A_MN, B_MN, CG>, &qc) == cudaSuccess && n > 0)
+        clusters_max = std::min(clusters_max, n);
+      cudaGetLastError();
+    }
+  }
   int splits = 1;
   if (p.c_f32 && !p.bias && !p.res && !p.gelu && g->split_k != 1) {
     if (g->split_k > 1) {
@@ -988,13 +1031,15 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   } else if (g->cta_group > 0) {
     cg = g->cta_group;
   }
-  DPN_REQUIRE(cg == 1 || (cg == 2 && bn >= 128), "cta_group 2 needs block_n 128 or 256");
+  DPN_REQUIRE(cg == 1 || (cg == 2 && bn >= 128) || (cg == 4 && bn == 256),
+              "cta_group 2 needs block_n 128 or 256; 4 (two multicast pairs) block_n 256");
   switch (bn * 10 + cg) {
     case 641: return dispatch_major<64, 1>(g, p, s);
     case 1281: return dispatch_major<128, 1>(g, p, s);
     case 2561: return dispatch_major<256, 1>(g, p, s);
     case 1282: return dispatch_major<128, 2>(g, p, s);
     case 2562: return dispatch_major<256, 2>(g, p, s);
-    default: DPN_REQUIRE(false, "block_n must be 0, 64, 128 or 256; cta_group 0, 1 or 2");
+    case 2564: return dispatch_major<256, 4>(g, p, s);
+    default: DPN_REQUIRE(false, "block_n must be 0, 64, 128 or 256; cta_group 0, 1, 2 or 4");
   }
 }

@@ -43,7 +43,8 @@ def rnd(*shape, dtype=torch.bfloat16, scale=1.0):
                                            (512, 768, 1024, 256, 1), (384, 1024, 512, 128, 1),
                                            (77, 136, 40, 0, 0), (512, 768, 1024, 256, 2),
                                            (384, 1024, 512, 128, 2), (700, 520, 200, 256, 2),
-                                           (200, 384, 64, 128, 2)])
+                                           (200, 384, 64, 128, 2), (512, 1024, 512, 256, 4),
+                                           (700, 520, 200, 256, 4), (1024, 768, 1024, 256, 4)])
 @pytest.mark.parametrize("epi", [0, 1])
 def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn, cg, epi):
     k = K()
@@ -66,7 +67,8 @@ def test_gemm_layouts(a_mn, b_mn, M, N, K_, bn, cg, epi):
 @pytest.mark.parametrize("mode", ["plain", "bias", "bias_res", "gelu_aux", "gelu_grad"])
 @pytest.mark.parametrize("M,N,K_,bn,cg", [(512, 384, 256, 0, 0), (300, 200, 96, 0, 0),
                                            (77, 136, 40, 0, 0), (1024, 1024, 1024, 256, 2),
-                                           (384, 512, 128, 128, 1), (640, 320, 192, 128, 2)])
+                                           (384, 512, 128, 128, 1), (640, 320, 192, 128, 2),
+                                           (1024, 1024, 1024, 256, 4), (640, 320, 192, 256, 4)])
 @pytest.mark.parametrize("epi", [0, 1])
 def test_gemm_bf16_epilogues(mode, M, N, K_, bn, cg, epi):
     """bf16 outputs through the TMA-staged epilogue (epi 0) and the direct-store
