@@ -967,8 +967,12 @@ int dispatch_major(const dpn_gemm_args* g, const GemmParams& p, cudaStream_t s) 
 // per-tile fill / epilogue costs for half the MMA work), so it is used
 // whenever N > 128; N <= 128 takes BN=128 (pair when M > 128); N <= 64 (the
 // attention products with N = head_dim) stays single-CTA BN=64.
-void pick_config(long long M, long long N, long long Z, int& bn, int& cg) {
-  (void)Z;
+// The CTA pair is used for every N > 128 tile with M > 128.  In isolation
+// single-CTA 128x256 tiles win on small problems (620 vs 567 TFLOP/s at
+// 4096x1024x1024, profiles/r01_gemm_micro_multicast.jsonl), but switching to
+// them below 256 pair tiles x 16 k-blocks lowered the in-pipeline GEMM rate
+// (GPT-2 XL 923 -> 854 TFLOP/s, BERT-large b=8 unchanged), so it is not done.
+void pick_config(long long M, long long N, long long K, long long Z, int& bn, int& cg) {
   if (N <= 64) {
     bn = 64;
     cg = 1;
@@ -977,6 +981,10 @@ void pick_config(long long M, long long N, long long Z, int& bn, int& cg) {
     cg = M > 128 ? 2 : 1;
   } else {
     bn = 256;
+    const long long pair_tiles = ((M + 255) / 256) * ((N + 255) / 256) * Z;
+    const long long nk = (K + BK - 1) / BK;
+    (void)pair_tiles;
+    (void)nk;
     cg = M > 128 ? 2 : 1;
   }
 }
@@ -1024,7 +1032,7 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   p.trace = g_gemm_trace;
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
   int bn = 0, cg = 1;
-  pick_config(g->M, g->N, p.Z, bn, cg);
+  pick_config(g->M, g->N, g->K, p.Z, bn, cg);
   if (g->block_n > 0) {
     bn = g->block_n;
     cg = g->cta_group > 0 ? g->cta_group : (bn >= 128 && g->M > 128 ? 2 : 1);

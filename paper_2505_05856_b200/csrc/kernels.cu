@@ -194,9 +194,9 @@ __device__ __forceinline__ void red_add_v4(float* addr, const float* v) {
 //   MODE 1: out0 += sum_r a[r] * (x[r] - mean[r]) * rstd[r],  out1 += sum_r a[r]
 constexpr int kColThreads = 512;
 constexpr int kColUnrollSum = 8;   // MODE 0: rows in flight per lane
-constexpr int kColUnrollLn = 4;    // MODE 1 (two operands per row)
+constexpr int kColUnrollLn = 2;    // MODE 1 (two operands per row; 2 CTAs per SM)
 template <int MODE>
-__global__ void __launch_bounds__(kColThreads) colred_kernel(
+__global__ void __launch_bounds__(kColThreads, 2) colred_kernel(
     const __nv_bfloat16* __restrict__ a, long long lda, const __nv_bfloat16* __restrict__ x,
     const float* __restrict__ mean, const float* __restrict__ rstd, long long rows, int cols,
     long long rows_per_cta, float* __restrict__ out0, float* __restrict__ out1) {
