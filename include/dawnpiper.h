@@ -90,6 +90,18 @@ int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float
                  float* workspace, int64_t workspace_floats, int64_t batch, int64_t seq,
                  int64_t heads, int64_t head_dim, float scale, int causal, void* stream);
 
+/* Cross-attention (T5 decoder): q [batch*q_seq, heads*64], kv [batch*kv_seq,
+ * 2*heads*64] (K | V column blocks), out [batch*q_seq, heads*64], lse [batch,
+ * heads, q_seq]; no mask.  Backward writes dq (like q) and dkv (like kv);
+ * workspace >= batch*q_seq*heads*64 + batch*heads*q_seq floats. */
+int dpn_attn_fwd_cross(const void* q, const void* kv, void* out, float* lse, int64_t batch,
+                       int64_t q_seq, int64_t kv_seq, int64_t heads, int64_t head_dim, float scale,
+                       void* stream);
+int dpn_attn_bwd_cross(const void* q, const void* kv, const void* out, const void* dout,
+                       const float* lse, void* dq, void* dkv, float* workspace,
+                       int64_t workspace_floats, int64_t batch, int64_t q_seq, int64_t kv_seq,
+                       int64_t heads, int64_t head_dim, float scale, void* stream);
+
 /* ---- node kernels (bf16 storage, fp32 math) ------------------------------ */
 /* ln1 / ln2 / lnf: y = (x - mean) * rstd * gamma + beta; mean/rstd saved (f32 [rows]). */
 int dpn_layernorm_fwd(const void* x, const void* gamma, const void* beta, void* y, float* mean,

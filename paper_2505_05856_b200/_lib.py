@@ -50,6 +50,9 @@ SIGNATURES = {
     "dpn_gemm": [C.POINTER(GemmArgs), _vp],
     "dpn_attn_fwd": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, C.c_int, _vp],
     "dpn_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, C.c_int, _vp],
+    "dpn_attn_fwd_cross": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp],
+    "dpn_attn_bwd_cross": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
+                           _f32, _vp],
     "dpn_layernorm_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp],
     "dpn_layernorm_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp],
     "dpn_softmax_fwd": [_vp, _vp, _i64, _i64, _i64, _f32, C.c_int, _vp],

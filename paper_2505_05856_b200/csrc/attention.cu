@@ -48,7 +48,9 @@ constexpr float kRescaleLog2 = 8.f;  // raise the running max only past 2^8
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct AttnParams {
-  int batch, seq, heads, H;  // H = heads * 64
+  int batch, seq, heads, H;  // seq = query rows per sequence; H = heads * 64
+  int kv_seq;                // key rows per sequence (== seq for self-attention)
+  int q_col, k_col, v_col;   // column of head 0's Q / K / V in its buffer
   float scale_log2;          // softmax scale * log2(e)
   float scale;
   int causal;
@@ -111,7 +113,8 @@ __device__ __forceinline__ void tmem_st_wait() {
 }
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
-    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_qkv, const AttnParams p) {
+    attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
+                    const AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -133,9 +136,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_kv_all = (p.seq + kTile - 1) / kTile;
+  const int n_kv_all = (p.kv_seq + kTile - 1) / kTile;
+  const int n_qt = (p.seq + kTile - 1) / kTile;
   const long long bh = (long long)p.batch * p.heads;
-  const long long units = bh * n_kv_all;
+  const long long units = bh * n_qt;
   // unit -> (query tile, head, batch); query tiles outermost, longest first
   auto decode = [&](long long u, int& qt, int& h, int& bb) {
     // non-causal: query tiles fastest (concurrent CTAs share a head's K / V in
@@ -146,16 +150,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       qi = (int)(u / bh);
       r = u - (long long)qi * bh;
     } else {
-      qi = (int)(u % n_kv_all);
-      r = u / n_kv_all;
+      qi = (int)(u % n_qt);
+      r = u / n_qt;
     }
-    qt = p.causal ? n_kv_all - 1 - qi : qi;
+    qt = p.causal ? n_qt - 1 - qi : qi;
     h = (int)(r % p.heads);
     bb = (int)(r / p.heads);
   };
   auto kv_tiles = [&](int qt) { return p.causal ? min(n_kv_all, qt + 1) : n_kv_all; };
 
-  if (warp == 0 && lane == 0) prefetch_tmap(&tm_qkv);
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_q);
+    prefetch_tmap(&tm_kv);
+  }
   if (warp == 1 && lane == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
@@ -191,16 +198,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
         int qt, h, bb;
         decode(u, qt, h, bb);
-        const int n_kv = kv_tiles(qt), row0 = bb * p.seq;
+        const int n_kv = kv_tiles(qt), row0 = bb * p.seq, krow0 = bb * p.kv_seq;
         mbar_wait(q_empty, (uc & 1) ^ 1);
         mbar_expect_tx(q_full, kTileBytes);
-        tma_load_2d(sQ, &tm_qkv, q_full, h * kD, row0 + qt * kTile);
+        tma_load_2d(sQ, &tm_q, q_full, p.q_col + h * kD, row0 + qt * kTile);
         for (int j = 0; j < n_kv; ++j, ++g) {
           const int st = g % kKVStages;
           mbar_wait(&kv_empty[st], ((g / kKVStages) & 1) ^ 1);
           mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-          tma_load_2d(sK + st * kTileBytes, &tm_qkv, &kv_full[st], p.H + h * kD, row0 + j * kTile);
-          tma_load_2d(sV + st * kTileBytes, &tm_qkv, &kv_full[st], 2 * p.H + h * kD, row0 + j * kTile);
+          tma_load_2d(sK + st * kTileBytes, &tm_kv, &kv_full[st], p.k_col + h * kD, krow0 + j * kTile);
+          tma_load_2d(sV + st * kTileBytes, &tm_kv, &kv_full[st], p.v_col + h * kD, krow0 + j * kTile);
         }
       }
     }
@@ -283,7 +290,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       for (int j = 0; j < n_kv; ++j) {
         const int gj = g + j, i = gj & 1;
         const int k0 = j * kTile + half * 64;
-        const bool mask = (j + 1) * kTile > p.seq || (p.causal && j == qt);
+        const bool mask = (j + 1) * kTile > p.kv_seq || (p.causal && j == qt);
         mbar_wait(&s_full[i], (gj >> 1) & 1);
         tc_fence_after();
         float s[64];
@@ -302,7 +309,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
           for (int c = 0; c < 64; ++c) {
             const int key = k0 + c;
-            if (!(key < p.seq && (!p.causal || key <= q))) s[c] = -INFINITY;
+            if (!(key < p.kv_seq && (!p.causal || key <= q))) s[c] = -INFINITY;
           }
         }
         float mx = s[0];
@@ -494,7 +501,12 @@ namespace {
 constexpr int kBwdThreads = 512;
 
 struct AttnBwdParams {
-  int batch, seq, heads, H;
+  int batch, seq, heads, H;  // seq = query rows per sequence
+  int kv_seq;                // key rows per sequence
+  int q_col, k_col, v_col;   // column of head 0's Q / K / V in its buffer
+  __nv_bfloat16* dk;         // dK / dV of head 0, row stride dkv_ld
+  __nv_bfloat16* dv;
+  long long dkv_ld;
   float scale, scale_log2;
   int causal;
   const float* lse;  // [b, heads, s]
@@ -516,6 +528,7 @@ struct AttnBwdParams {
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tm_qkv,
+                    const __grid_constant__ CUtensorMap tm_kv,
                     const __grid_constant__ CUtensorMap tm_do,
                     const __grid_constant__ CUtensorMap tm_dq, const AttnBwdParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -546,12 +559,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_q = (p.seq + kTile - 1) / kTile;
+  const int n_k = (p.kv_seq + kTile - 1) / kTile;
   const long long bh = (long long)p.batch * p.heads;
-  const long long units = bh * n_q;
+  const long long units = bh * n_k;
   // unit -> (key tile, head, batch).  Every barrier phase below runs on CTA-global counters
   // (units uc, query iterations G) so a unit's tail overlaps the next one.
   struct Unit {
-    int kt, h, bb, k0, i0, n_it, row0;
+    int kt, h, bb, k0, i0, n_it, row0, krow0;
   };
   auto decode = [&](long long u) {
     Unit w;
@@ -563,8 +577,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       w.kt = (int)(u / bh);
       r = u - (long long)w.kt * bh;
     } else {
-      w.kt = (int)(u % n_q);
-      r = u / n_q;
+      w.kt = (int)(u % n_k);
+      r = u / n_k;
     }
     w.h = (int)(r % p.heads);
     w.bb = (int)(r / p.heads);
@@ -572,11 +586,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     w.i0 = p.causal ? w.kt : 0;
     w.n_it = n_q - w.i0;
     w.row0 = w.bb * p.seq;
+    w.krow0 = w.bb * p.kv_seq;
     return w;
   };
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tm_qkv);
+    prefetch_tmap(&tm_kv);
     prefetch_tmap(&tm_do);
     prefetch_tmap(&tm_dq);
   }
@@ -616,13 +632,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const Unit w = decode(u);
         mbar_wait(kv_empty, (uc & 1) ^ 1);
         mbar_expect_tx(kv_full, 2 * kTileBytes);
-        tma_load_2d(sK, &tm_qkv, kv_full, p.H + w.h * kD, w.row0 + w.k0);
-        tma_load_2d(sV, &tm_qkv, kv_full, 2 * p.H + w.h * kD, w.row0 + w.k0);
+        tma_load_2d(sK, &tm_kv, kv_full, p.k_col + w.h * kD, w.krow0 + w.k0);
+        tma_load_2d(sV, &tm_kv, kv_full, p.v_col + w.h * kD, w.krow0 + w.k0);
         for (int it = 0; it < w.n_it; ++it, ++G) {
           const int st = G & 1, i = w.i0 + it;
           mbar_wait(&q_empty[st], ((G >> 1) & 1) ^ 1);
           mbar_expect_tx(&q_full[st], 2 * kTileBytes);
-          tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], w.h * kD, w.row0 + i * kTile);
+          tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], p.q_col + w.h * kD, w.row0 + i * kTile);
           tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], w.h * kD, w.row0 + i * kTile);
         }
       }
@@ -734,7 +750,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const float lse2 = lse_next * lse_scale;
         const float Dq = d_next * sc;
         row_stats(it + 1, lse_next, d_next);
-        const bool mask = !qok || k0 + kTile > p.seq || (p.causal && i == kt);
+        const bool mask = !qok || k0 + kTile > p.kv_seq || (p.causal && i == kt);
         const int pb = G & 1;
         uint8_t* tdS = sdS + pb * kPBytes;
         mbar_wait(sp_full, G & 1);
@@ -763,8 +779,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               float2 pr = make_float2(ex2(a.x), ex2(a.y));
               if constexpr (kMask) {
                 const int key = k0 + half * 64 + c * 8 + e;
-                pr.x = (qok && key < p.seq && (!p.causal || key <= q)) ? pr.x : 0.f;
-                pr.y = (qok && key + 1 < p.seq && (!p.causal || key + 1 <= q)) ? pr.y : 0.f;
+                pr.x = (qok && key < p.kv_seq && (!p.causal || key <= q)) ? pr.x : 0.f;
+                pr.y = (qok && key + 1 < p.kv_seq && (!p.causal || key + 1 <= q)) ? pr.y : 0.f;
               }
               pv[e] = pr.x;
               pv[e + 1] = pr.y;
@@ -854,10 +870,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t uv[32];
         tmem_ld_32x32b_x32(tmem + 256 + part * 32 + lane_off, uv);
         tmem_ld_wait();
-        if (key < p.seq) {
+        if (key < p.kv_seq) {
           const int which = part >> 1;  // 0: dV, 1: dK
-          __nv_bfloat16* dst = p.dqkv + (long long)(w.row0 + key) * 3 * p.H +
-                               (which ? p.H : 2 * p.H) + w.h * kD + (part & 1) * 32;
+          __nv_bfloat16* dst = (which ? p.dk : p.dv) + (long long)(w.krow0 + key) * p.dkv_ld +
+                               w.h * kD + (part & 1) * 32;
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint4 a;
@@ -920,9 +936,9 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16*
   }
 }
 
-// dqkv[:, 0:H] = bf16(dq)
+// dst[:, 0:H] (row stride ld) = bf16(dq)
 __global__ void attn_dq_store_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
-                                     long long rows, int H) {
+                                     long long rows, int H, long long ld) {
   pdl_wait();
   const long long n4 = rows * H / 4;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
@@ -932,7 +948,7 @@ __global__ void attn_dq_store_kernel(const float* __restrict__ dq, __nv_bfloat16
     uint2 w;
     w.x = pack_bf16(v.x, v.y);
     w.y = pack_bf16(v.z, v.w);
-    *reinterpret_cast<uint2*>(dqkv + row * 3 * H + col) = w;
+    *reinterpret_cast<uint2*>(dqkv + row * ld + col) = w;
   }
 }
 
@@ -956,6 +972,10 @@ extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batc
   AttnParams p{};
   p.batch = (int)batch;
   p.seq = (int)seq;
+  p.kv_seq = (int)seq;
+  p.q_col = 0;
+  p.k_col = (int)H;
+  p.v_col = (int)(2 * H);
   p.heads = (int)heads;
   p.H = (int)H;
   p.scale = scale;
@@ -978,7 +998,7 @@ extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batc
   }
   const long long units = (long long)((seq + kTile - 1) / kTile) * heads * batch;
   const unsigned grid = (unsigned)std::min<long long>(units, n_sm);  // persistent: one CTA per SM
-  DPN_CHECK_CUDA(launch_pdl(attn_fwd_kernel, grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream, tm, p));
+  DPN_CHECK_CUDA(launch_pdl(attn_fwd_kernel, grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream, tm, tm, p));
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -988,13 +1008,17 @@ static long long* g_attn_trace = nullptr;
 // backward kernel into buf[cta * 64 + slot]; nullptr turns it off.
 extern "C" void dpn_attn_debug_trace(void* buf) { g_attn_trace = static_cast<long long*>(buf); }
 
-extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
-                            void* dqkv, float* workspace, int64_t workspace_floats, int64_t batch,
-                            int64_t seq, int64_t heads, int64_t head_dim, float scale, int causal,
-                            void* stream) {
-  DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
-  DPN_REQUIRE(seq % 64 == 0 && seq > 0, "seq must be a positive multiple of 64");
-  const long long H = heads * head_dim, rows = batch * seq;
+namespace dpn {
+namespace {
+// Backward launcher shared by self- and cross-attention: q_src / kv_src hold Q
+// and K|V (columns q_col / k_col / v_col of head 0), dq_dst (row stride dq_ld)
+// receives dQ, dk / dv (row stride dkv_ld) dK and dV.
+int attn_bwd_launch(const void* q_src, long long q_ld, const void* kv_src, long long kv_ld, int q_col,
+                    int k_col, int v_col, const void* out, const void* dout, const float* lse,
+                    __nv_bfloat16* dq_dst, long long dq_ld, __nv_bfloat16* dk, __nv_bfloat16* dv,
+                    long long dkv_ld, float* workspace, int64_t workspace_floats, int64_t batch,
+                    int64_t seq, int64_t kv_seq, int64_t heads, float scale, int causal, void* stream) {
+  const long long H = heads * kD, rows = batch * seq;
   DPN_REQUIRE(workspace != nullptr && workspace_floats >= rows * H + batch * heads * seq,
               "workspace must hold batch*seq*(heads*64) + batch*heads*seq floats");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1007,17 +1031,22 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
                               (const __nv_bfloat16*)dout, D, dq, rows, (int)seq, (int)heads));
     DPN_LAUNCH_CHECK();
   }
-  CUtensorMap tq, td;
-  int rc = map_2d(&tq, qkv, rows, 3 * H);
-  if (rc) return rc;
-  rc = map_2d(&td, dout, rows, H);
-  if (rc) return rc;
-  CUtensorMap tdq;
-  rc = map_2d_f32(&tdq, dq, rows, H);
+  CUtensorMap tq, tkv, td, tdq;
+  int rc = map_2d(&tq, q_src, rows, q_ld);
+  if (!rc) rc = map_2d(&tkv, kv_src, batch * kv_seq, kv_ld);
+  if (!rc) rc = map_2d(&td, dout, rows, H);
+  if (!rc) rc = map_2d_f32(&tdq, dq, rows, H);
   if (rc) return rc;
   AttnBwdParams p{};
   p.batch = (int)batch;
   p.seq = (int)seq;
+  p.kv_seq = (int)kv_seq;
+  p.q_col = q_col;
+  p.k_col = k_col;
+  p.v_col = v_col;
+  p.dk = dk;
+  p.dv = dv;
+  p.dkv_ld = dkv_ld;
   p.heads = (int)heads;
   p.H = (int)H;
   p.scale = scale;
@@ -1026,8 +1055,8 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
   p.lse = lse;
   p.D = D;
   p.dq = dq;
-  p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
-  p.trace = g_attn_trace;
+  p.dqkv = dq_dst;
+  p.trace = nullptr;
   static bool set = false;
   if (!set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1041,12 +1070,85 @@ extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, 
     cudaDeviceGetAttribute(&n_sm_b, cudaDevAttrMultiProcessorCount, dev);
     if (n_sm_b <= 0) n_sm_b = 148;
   }
-  const long long units = (long long)((seq + kTile - 1) / kTile) * heads * batch;
+  const long long units = (long long)((kv_seq + kTile - 1) / kTile) * heads * batch;
   const unsigned grid = (unsigned)std::min<long long>(units, n_sm_b);  // persistent
-  DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, td, tdq, p));
+  DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, tkv, td, tdq, p));
   DPN_LAUNCH_CHECK();
-  DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel, (unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0, st, 
-      dq, (__nv_bfloat16*)dqkv, rows, (int)H));
+  DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel,
+                            (unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0,
+                            st, dq, dq_dst, rows, (int)H, dq_ld));
   DPN_LAUNCH_CHECK();
   return 0;
+}
+}  // namespace
+}  // namespace dpn
+
+extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                            void* dqkv, float* workspace, int64_t workspace_floats, int64_t batch,
+                            int64_t seq, int64_t heads, int64_t head_dim, float scale, int causal,
+                            void* stream) {
+  DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
+  DPN_REQUIRE(seq % 64 == 0 && seq > 0, "seq must be a positive multiple of 64");
+  const long long H = heads * head_dim;
+  __nv_bfloat16* d = static_cast<__nv_bfloat16*>(dqkv);
+  return attn_bwd_launch(qkv, 3 * H, qkv, 3 * H, 0, (int)H, (int)(2 * H), out, dout, lse, d, 3 * H,
+                         d + H, d + 2 * H, 3 * H, workspace, workspace_floats, batch, seq, seq, heads,
+                         scale, causal, stream);
+}
+
+extern "C" int dpn_attn_fwd_cross(const void* q, const void* kv, void* out, float* lse, int64_t batch,
+                                  int64_t q_seq, int64_t kv_seq, int64_t heads, int64_t head_dim,
+                                  float scale, void* stream) {
+  DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
+  DPN_REQUIRE(q_seq % 64 == 0 && kv_seq % 64 == 0 && q_seq > 0 && kv_seq > 0,
+              "sequence lengths must be positive multiples of 64");
+  DPN_REQUIRE(q && kv && out && lse, "null pointer");
+  const long long H = heads * head_dim;
+  CUtensorMap tq, tkv;
+  int rc = map_2d(&tq, q, batch * q_seq, H);
+  if (!rc) rc = map_2d(&tkv, kv, batch * kv_seq, 2 * H);
+  if (rc) return rc;
+  AttnParams p{};
+  p.batch = (int)batch;
+  p.seq = (int)q_seq;
+  p.kv_seq = (int)kv_seq;
+  p.q_col = 0;
+  p.k_col = 0;
+  p.v_col = (int)H;
+  p.heads = (int)heads;
+  p.H = (int)H;
+  p.scale = scale;
+  p.scale_log2 = scale * kLog2e;
+  p.causal = 0;
+  p.out = static_cast<__nv_bfloat16*>(out);
+  p.lse = lse;
+  static bool set = false;
+  if (!set) {
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kFwdSmem));
+    set = true;
+  }
+  int n_sm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  if (n_sm <= 0) n_sm = 148;
+  const long long units = (long long)((q_seq + kTile - 1) / kTile) * heads * batch;
+  const unsigned grid = (unsigned)std::min<long long>(units, n_sm);
+  DPN_CHECK_CUDA(launch_pdl(attn_fwd_kernel, grid, kFwdThreads, kFwdSmem, (cudaStream_t)stream, tq, tkv, p));
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_attn_bwd_cross(const void* q, const void* kv, const void* out, const void* dout,
+                                  const float* lse, void* dq, void* dkv, float* workspace,
+                                  int64_t workspace_floats, int64_t batch, int64_t q_seq, int64_t kv_seq,
+                                  int64_t heads, int64_t head_dim, float scale, void* stream) {
+  DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
+  DPN_REQUIRE(q_seq % 64 == 0 && kv_seq % 64 == 0 && q_seq > 0 && kv_seq > 0,
+              "sequence lengths must be positive multiples of 64");
+  const long long H = heads * head_dim;
+  __nv_bfloat16* dkvp = static_cast<__nv_bfloat16*>(dkv);
+  return attn_bwd_launch(q, H, kv, 2 * H, 0, 0, (int)H, out, dout, lse, static_cast<__nv_bfloat16*>(dq),
+                         H, dkvp, dkvp + H, 2 * H, workspace, workspace_floats, batch, q_seq, kv_seq,
+                         heads, scale, 0, stream);
 }

@@ -163,6 +163,29 @@ def attn_bwd(qkv, out, dout, lse, dqkv, batch, seq, heads, causal, scale=None, s
           "dpn_attn_bwd")
 
 
+def attn_fwd_cross(q, kv, out, lse, batch, q_seq, kv_seq, heads, scale=None, stream=None):
+    """Fused cross-attention forward: q [b*t, H], kv [b*s, 2H] (K | V) -> out, lse [b, A, t]."""
+    d = 64
+    INSTR.launches += 1
+    check(lib().dpn_attn_fwd_cross(q.data_ptr(), kv.data_ptr(), out.data_ptr(), lse.data_ptr(), batch,
+                                   q_seq, kv_seq, heads, d, scale if scale is not None else d ** -0.5,
+                                   _s(stream)), "dpn_attn_fwd_cross")
+
+
+def attn_bwd_cross(q, kv, out, dout, lse, dq, dkv, batch, q_seq, kv_seq, heads, scale=None,
+                   stream=None):
+    """Fused cross-attention backward -> dq [b*t, H], dkv [b*s, 2H]."""
+    d = 64
+    H = heads * d
+    INSTR.launches += 3
+    ws = _workspace(q.device, batch * q_seq * H + batch * heads * q_seq, stream)
+    check(lib().dpn_attn_bwd_cross(q.data_ptr(), kv.data_ptr(), out.data_ptr(), dout.data_ptr(),
+                                   lse.data_ptr(), dq.data_ptr(), dkv.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), batch, q_seq, kv_seq, heads, d,
+                                   scale if scale is not None else d ** -0.5, _s(stream)),
+          "dpn_attn_bwd_cross")
+
+
 def layernorm_fwd(x, gamma, beta, y, mean, rstd, eps=1e-5, stream=None):
     rows, cols = x.shape
     INSTR.launches += 1

@@ -17,7 +17,8 @@ Encoder-decoder (T5-large, BASELINE.json configs[3]): the encoder stack above
 tokens (`dembed`) and runs blocks d{i} = causal self-attention sub-block,
 cross-attention sub-block, FFN sub-block:
     c = lnx(y); q = c Wq^T + bq; kv = E Wkv^T + bkv; P = softmax(q K^T/sqrt(d));
-    ctx = P V (node `xattn`, q / kv / P saved inside it); y2 = ctx Wo^T + bo + y
+    ctx = P V (node `xattn`: projections + fused cross-attention, q / kv / LSE
+    saved inside it); y2 = ctx Wo^T + bo + y
 then `lnf` and `head` over the target tokens.  The cross-attention is one
 node (its K/V projection reads E) so that, in the reference's canonical order
 (depth, fwd_start, id; graph.py:133), the K/V projections stay with their
@@ -255,8 +256,12 @@ def internal_specs(cfg: TransformerConfig, node: NodeDef, b: int):
     if node.kind != "xattn":
         return {}
     t, s, H = node.seq, cfg.seq, cfg.hidden
-    return {"q": ((b * t, H), torch.bfloat16), "kv": ((b * s, 2 * H), torch.bfloat16),
-            "p": ((b, cfg.heads, t, s), torch.bfloat16)}
+    out = {"q": ((b * t, H), torch.bfloat16), "kv": ((b * s, 2 * H), torch.bfloat16)}
+    if cfg.fused_attention:  # flash-style kernel: only the per-row log-sum-exp is kept
+        out["lse"] = ((b, cfg.heads, t), torch.float32)
+    else:                    # materialised probabilities (reference vocabulary)
+        out["p"] = ((b, cfg.heads, t, s), torch.bfloat16)
+    return out
 
 
 def stats_bytes(cfg: TransformerConfig, node: NodeDef, b: int) -> int:
@@ -305,6 +310,7 @@ def backward_readers(nodes: List[NodeDef]) -> Dict[str, List[str]]:
         elif n.kind == "xattn":
             readers[n.inputs[0]].append(n.id)         # c for the q-projection wgrad
             readers[n.inputs[1]].append(n.id)         # E for the kv-projection wgrad
+            readers[n.id].append(n.id)                # O for D = rowsum(dO * O) (fused kernel)
             # (q, kv and P are internal tensors of the node itself)
         elif n.kind in ("bn", "pw", "dw"):
             readers[n.inputs[0]].append(n.id)         # x for BN's xhat / the weight gradients

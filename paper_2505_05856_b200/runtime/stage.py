@@ -669,9 +669,13 @@ class StageExecutor:
         t, s, d, A, H, b = n.seq, cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
         q = self.buf(internal_tid(n.id, "q"), slot, phase)
         kv = self.buf(internal_tid(n.id, "kv"), slot, phase)
-        P = self.buf(internal_tid(n.id, "p"), slot, phase)
         K.linear_fwd(c, W("q_weight"), q, bias=W("q_bias"), stream=st)
         K.linear_fwd(E, W("kv_weight"), kv, bias=W("kv_bias"), stream=st)
+        if cfg.fused_attention:  # flash-style cross-attention, P never materialised
+            K.attn_fwd_cross(q, kv, out, self.buf(internal_tid(n.id, "lse"), slot, phase), b, t, s, A,
+                             stream=st)
+            return
+        P = self.buf(internal_tid(n.id, "p"), slot, phase)
         # S = q K^T per (batch, head): [t, s]
         K.gemm_raw(M=t, N=s, K=d, A=q, lda=H, a_s=(d, t * H), B=kv, ldb=2 * H, b_s=(d, s * 2 * H),
                    batch1=A, batch2=b, Cout=P, ldc=s, c_s=(t * s, A * t * s), stream=st)
@@ -688,10 +692,21 @@ class StageExecutor:
         c, E = self.buf(c_t, slot, "bwd"), self.buf(e_t, slot, "bwd")
         q = self.buf(internal_tid(n.id, "q"), slot, "bwd")
         kv = self.buf(internal_tid(n.id, "kv"), slot, "bwd")
-        P = self.buf(internal_tid(n.id, "p"), slot, "bwd")
-        dS = torch.empty_like(P)
         dq = torch.empty_like(q)
         dkv = torch.empty_like(kv)
+        if cfg.fused_attention:
+            K.attn_bwd_cross(q, kv, self.buf(out_tid(n.id), slot, "bwd"), dy,
+                             self.buf(internal_tid(n.id, "lse"), slot, "bwd"), dq, dkv, b, t, s, A,
+                             stream=st)
+        else:
+            self._xattn_bwd_unfused(n, dy, q, kv, dq, dkv, slot)
+        self._xattn_proj_bwd(n, c_t, c, e_t, E, dq, dkv, W, G)
+
+    def _xattn_bwd_unfused(self, n: NodeDef, dy, q, kv, dq, dkv, slot: int) -> None:
+        cfg, st = self.cfg, self.stream
+        t, s, d, A, H, b = n.seq, cfg.seq, cfg.head_dim, cfg.heads, cfg.hidden, self.b
+        P = self.buf(internal_tid(n.id, "p"), slot, "bwd")
+        dS = torch.empty_like(P)
         # dP = dO V^T
         K.gemm_raw(M=t, N=s, K=d, A=dy, lda=H, a_s=(d, t * H), B=kv[:, H:], ldb=2 * H,
                    b_s=(d, s * 2 * H), batch1=A, batch2=b, Cout=dS, ldc=s, c_s=(t * s, A * t * s),
@@ -707,6 +722,9 @@ class StageExecutor:
         K.gemm_raw(M=s, N=d, K=t, A=dS, lda=s, a_mn=True, a_s=(t * s, A * t * s), B=q, ldb=H,
                    b_mn=True, b_s=(d, t * H), batch1=A, batch2=b, Cout=dkv, ldc=2 * H,
                    c_s=(d, s * 2 * H), stream=st)
+
+    def _xattn_proj_bwd(self, n: NodeDef, c_t, c, e_t, E, dq, dkv, W, G) -> None:
+        st = self.stream
         # projections: dc (+)= dq Wq, dE (+)= dkv Wkv, weight / bias gradients
         for g_in, w, x_t, x, wn, bn in ((dq, W("q_weight"), c_t, c, "q_weight", "q_bias"),
                                          (dkv, W("kv_weight"), e_t, E, "kv_weight", "kv_bias")):

@@ -421,3 +421,34 @@ def test_fused_attention_backward(b, s, A, causal):
     o_ref.backward(dout.float())
     for part in range(3):
         close(dqkv[:, part * H:(part + 1) * H], x.grad[:, part * H:(part + 1) * H])
+
+
+@pytest.mark.parametrize("b,t,s,A", [(2, 128, 512, 2), (3, 64, 192, 2), (16, 128, 512, 16)])
+def test_fused_cross_attention(b, t, s, A):
+    """T5 cross-attention: queries from the decoder (t), keys / values from the
+    encoder output (s), separate buffers, forward and backward."""
+    k = K()
+    H = A * 64
+    q = rnd(b * t, H, scale=1.5)
+    kv = rnd(b * s, 2 * H, scale=1.5)
+    out = torch.empty(b * t, H, device="cuda", dtype=torch.bfloat16)
+    lse = torch.empty(b, A, t, device="cuda")
+    k.attn_fwd_cross(q, kv, out, lse, b, t, s, A)
+    dout = rnd(b * t, H)
+    dq = torch.empty_like(q)
+    dkv = torch.empty_like(kv)
+    k.attn_bwd_cross(q, kv, out, dout, lse, dq, dkv, b, t, s, A)
+    torch.cuda.synchronize()
+    qr = q.float().requires_grad_()
+    kvr = kv.float().requires_grad_()
+    qh = qr.reshape(b, t, A, 64).transpose(1, 2)
+    kh = kvr[:, :H].reshape(b, s, A, 64).transpose(1, 2)
+    vh = kvr[:, H:].reshape(b, s, A, 64).transpose(1, 2)
+    sc = qh @ kh.transpose(-1, -2) / 8.0
+    o_ref = (torch.softmax(sc, -1) @ vh).transpose(1, 2).reshape(b * t, H)
+    close(out, o_ref)
+    assert (lse - torch.logsumexp(sc, -1)).abs().max().item() < 2e-2
+    o_ref.backward(dout.float())
+    close(dq, qr.grad)
+    close(dkv[:, :H], kvr.grad[:, :H])
+    close(dkv[:, H:], kvr.grad[:, H:])

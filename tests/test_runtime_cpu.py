@@ -87,7 +87,7 @@ def test_encdec_profile_graph(name, tmp_path):
     e = g.nodes[ids.index("enc_ln")]
     assert sorted(e.consumers) == sorted(f"d{i}.xattn" for i in range(cfg.dec_layers))
     x = g.nodes[ids.index("d0.xattn")]
-    assert {t.id for t in x.saved} == {"d0.xattn.out", "d0.xattn.q", "d0.xattn.kv", "d0.xattn.p"}
+    assert {t.id for t in x.saved} == {"d0.xattn.out", "d0.xattn.q", "d0.xattn.kv", "d0.xattn.lse"}
     P.save_profile(g, tmp_path / "p.json")
     assert P.canonical_hash(P.load_profile(tmp_path / "p.json")) == P.canonical_hash(g)
     params = init_params(cfg, 0) if name == "tiny-t5" else None
