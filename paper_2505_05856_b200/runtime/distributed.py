@@ -137,8 +137,6 @@ def run_bench_distributed(args) -> None:
     from .stage import StageExecutor
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("DPN_SINGLE_DEVICE"):  # test hook: every rank on GPU 0
-        local = 0
     torch.cuda.set_device(local)
     init_device(local)
     rank, world = init_process_group_from_env("nccl")

@@ -4,6 +4,7 @@
 """
 import collections
 import csv
+import gzip
 import io
 import subprocess
 import sys
@@ -15,7 +16,8 @@ METRICS = ["gpu__time_duration.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_p
 
 
 def launches(path):
-    rows = list(csv.reader(open(path)))
+    opener = gzip.open if path.endswith(".gz") else open
+    rows = list(csv.reader(opener(path, "rt")))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[hi]
     ki, mi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
@@ -48,7 +50,11 @@ def report(path):
     txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
+    if len(rows) < 3:
+        return [f"`{path}`: no kernels captured", ""]
     hdr, units = rows[0], rows[1]
+    if any(m not in hdr for m in METRICS):
+        return [f"`{path}`: metrics missing ({[m for m in METRICS if m not in hdr]})", ""]
     idx = [hdr.index(m) for m in METRICS]
     ki = hdr.index("Kernel Name")
     scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "nsecond": 1e-3, "usecond": 1.0,
@@ -71,7 +77,7 @@ def main():
     out_md, paths = sys.argv[1], sys.argv[2:]
     lines = []
     for p in paths:
-        lines += (launches(p) if p.endswith(".csv") else report(p)) + [""]
+        lines += (launches(p) if p.endswith((".csv", ".csv.gz")) else report(p)) + [""]
     open(out_md, "w").write("\n".join(lines) + "\n")
 
 
