@@ -45,10 +45,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
               "-I", str(ROOT / "include"), "--expt-relaxed-constexpr"]
     if verbose:
         common += ["-Xptxas", "-v"]
-    for src in SOURCES:
+    def compile_one(src):
         obj = tmp / (Path(src).stem + ".o")
         cmd = common + ["-c", str(CSRC / src), "-o", str(obj)]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # the translation units compile independently: one nvcc per source in parallel
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    for src, obj, r in results:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         if verbose:
