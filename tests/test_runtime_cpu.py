@@ -164,3 +164,20 @@ def test_oracle_cnn_is_partition_invariant():
     assert abs(one[0][0] - three[0][0]) < 1e-4
     import math
     assert abs(one[0][0] - math.log(cfg.classes)) < 1.0
+
+
+@pytest.mark.parametrize("stages,m", [(1, 1), (2, 3), (4, 8)])
+def test_sync_order_is_gpipe(stages, m):
+    """The co-located GPipe issue order: per stage exactly sync_ops (all
+    forwards, then backwards in reverse micro-batch order), dependencies kept."""
+    from paper_2505_05856_b200.runtime.pipeline import sync_order
+    order = sync_order(stages, m)
+    for x in range(1, stages + 1):
+        mine = [(k, j) for (s, k, j) in order if s == x]
+        assert mine == [(k, j) for k, j, _ in P.sync_ops(stages, m, x)]
+    pos = {(s, k, j): i for i, (s, k, j) in enumerate(order)}
+    for (s, k, j), i in pos.items():
+        if k == "fwd" and s > 1:
+            assert pos[(s - 1, "fwd", j)] < i
+        if k == "bwd" and s < stages:
+            assert pos[(s + 1, "bwd", j)] < i
