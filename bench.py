@@ -147,6 +147,32 @@ def cpu_port_sample(model_name: str, stages: int, samples: int = 1):
 
 # ---------------------------------------------------------------- ours ------
 
+def gemm_traffic():
+    """DRAM bytes (read + write) per GEMM launch from the committed ncu launch list
+    of the bench step (profiles/, cold-cache replay), else None."""
+    import gzip
+    import csv as _csv
+    p = ROOT / "profiles" / "r01_launches_step_b32.csv.gz"
+    if not p.exists():
+        return None
+    try:
+        rows = list(_csv.reader(gzip.open(p, "rt")))
+        hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+        h = rows[hi]
+        ki, ni, vi, ui = (h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
+                          h.index("Metric Unit"))
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot, ids = 0.0, set()
+        for r in rows[hi + 1:]:
+            if len(r) > vi and "gemm_kernel" in r[ki] and r[ni].startswith("dram__bytes"):
+                tot += float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
+                ids.add(r[0])
+        return {"bytes_per_launch": round(tot / len(ids)), "launches": len(ids),
+                "source": "profiles/r01_launches_step_b32.csv.gz (ncu dram__bytes_read+write, cold cache)"} if ids else None
+    except Exception:
+        return None
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -234,6 +260,7 @@ def run_ours(args):
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("bf16_tflops_sustained", 1400.0)
     achieved = gemm_flops / (gemm_ms / 1e3) / 1e12
+    traffic = gemm_traffic()
     # the same step's GEMM kernels timed by CUPTI (kernel start to end; the
     # per-GEMM events above also hold the launch gap that programmatic
     # dependent launch otherwise hides)
@@ -255,7 +282,9 @@ def run_ours(args):
     except Exception as e:  # the profiler is optional evidence
         cupti = {"error": str(e)[:200]}
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
+                "frac": round(achieved / peak, 4), "traffic": (traffic or {}).get("bytes_per_launch"),
+                "traffic_unit": "bytes per GEMM launch (DRAM read + write)",
+                "traffic_source": (traffic or {}).get("source"),
                 "kernel": "dpn gemm_kernel (tcgen05, all launches of one step)",
                 "launches_per_step": len(evs), "gemm_ms_per_step": round(gemm_ms, 3),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
