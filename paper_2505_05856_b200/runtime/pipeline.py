@@ -206,9 +206,12 @@ class Pipeline:
         out = {}
         with torch.cuda.stream(sst):
             for tid in src.send_ids:
-                a = src.send_buffer(tid, j)
-                msg = torch.empty_like(a)
-                K.copy_d2d(msg, a, stream=sst)
+                # buffers the sender's backward never reads change owner (no copy)
+                msg = src.release_send_buffer(tid, j)
+                if msg is None:
+                    a = src.send_buffer(tid, j)
+                    msg = torch.empty_like(a)
+                    K.copy_d2d(msg, a, stream=sst)
                 msg.record_stream(self.stage_streams[x])
                 out[tid] = msg
             ev = torch.cuda.Event()

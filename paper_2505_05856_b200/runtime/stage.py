@@ -451,6 +451,23 @@ class StageExecutor:
     def send_buffer(self, tid: str, mb: int) -> torch.Tensor:
         return self.buf(tid, self.slot_of(mb), "fwd")
 
+    def release_send_buffer(self, tid: str, mb: int) -> Optional[torch.Tensor]:
+        """Give away this stage's buffer of boundary tensor tid for micro-batch mb
+        (co-located zero-copy send) when the stage's own backward never reads it;
+        a fresh buffer takes its place.  None when it must be copied instead."""
+        if tid in self.needed or tid in self.evicted:
+            return None
+        slot = self.slot_of(mb)
+        if tid in self.slot_buf[slot]:
+            t = self.slot_buf[slot][tid]
+            self.slot_buf[slot][tid] = torch.empty_like(t)
+            return t
+        if tid in self.work:
+            t = self.work[tid]
+            self.work[tid] = torch.empty_like(t)
+            return t
+        return None
+
     def _outputs(self, n: NodeDef) -> List[str]:
         outs = [out_tid(n.id)] + self.self_tids(n)
         if n.id in self.fwd_gelu_of:
