@@ -260,7 +260,10 @@ class StageExecutor:
         # D2H completes; if the host link falls behind compute, the forward
         # waits for the oldest transfer instead of piling up device memory
         self.d2h_pending: List[Tuple[torch.cuda.Event, int]] = []
-        self.d2h_budget = 1 << 30
+        # bytes of swapped tensors whose D2H is still in flight: device memory the
+        # planner's model does not see (memopt.py:156-158 frees a swapped tensor
+        # at once); 256 MiB is ~5 ms of the measured 55 GB/s host link
+        self.d2h_budget = 256 << 20
         # recompute chains (memopt.py:91-115), replayed in forward order
         self.chains: Dict[str, List[int]] = {}
         for tid in sorted(self.recompute_ids):
