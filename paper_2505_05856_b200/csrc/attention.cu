@@ -513,17 +513,7 @@ struct AttnBwdParams {
   const float* D;    // [b, heads, s]
   float* dq;         // [b*s, H] f32 accumulator (zeroed)
   __nv_bfloat16* dqkv;  // [b*s, 3H]
-  long long* trace;     // debug: per-CTA clock64 stamps (nullptr = off)
 };
-
-// debug timeline of one CTA role (dpn_attn_debug_trace): slot k of CTA c
-#define ATTN_STAMP(slot)                                                              \
-  do {                                                                                \
-    if (p.trace && lane == 0) {                                                       \
-      const long long c_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z); \
-      p.trace[c_ * 64 + (slot)] = clock64();                                          \
-    }                                                                                 \
-  } while (0)
 
 
 __global__ void __launch_bounds__(kBwdThreads, 1)
@@ -1003,10 +993,6 @@ extern "C" int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batc
   return 0;
 }
 
-static long long* g_attn_trace = nullptr;
-// debug hook (not in the public header): per-CTA clock64 timeline of the
-// backward kernel into buf[cta * 64 + slot]; nullptr turns it off.
-extern "C" void dpn_attn_debug_trace(void* buf) { g_attn_trace = static_cast<long long*>(buf); }
 
 namespace dpn {
 namespace {
@@ -1056,7 +1042,6 @@ int attn_bwd_launch(const void* q_src, long long q_ld, const void* kv_src, long 
   p.D = D;
   p.dq = dq;
   p.dqkv = dq_dst;
-  p.trace = nullptr;
   static bool set = false;
   if (!set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
