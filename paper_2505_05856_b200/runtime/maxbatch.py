@@ -119,6 +119,11 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
         return StageCheck(x, True, torch.cuda.max_memory_allocated(device))
     except torch.OutOfMemoryError as e:
         return StageCheck(x, False, torch.cuda.max_memory_allocated(device), str(e).split("\n")[0][:200])
+    except RuntimeError as e:  # pinned host slots for swaps beyond what the OS lets us lock
+        if "pin" not in str(e).lower() and "OS call failed" not in str(e):
+            raise
+        return StageCheck(x, False, torch.cuda.max_memory_allocated(device),
+                          "pinned host allocation failed: " + str(e).split("\n")[0][:160])
     finally:
         del ex
         gc.collect()
