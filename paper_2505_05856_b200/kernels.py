@@ -49,6 +49,15 @@ def _workspace(device, floats: int, stream) -> torch.Tensor:
     return t
 
 
+def release_workspaces(device=None) -> None:
+    """Drop the cached scratch buffers (all devices, or one). Callers that create
+    short-lived streams (per-trial executors) call this when they are done: the
+    cache is keyed by stream handle, so it would otherwise keep one buffer per
+    stream the pool ever handed out."""
+    for key in [k for k in _WS if device is None or k[0] == device]:
+        del _WS[key]
+
+
 class _nullctx:
     def __enter__(self):
         return None

@@ -31,6 +31,7 @@ import torch
 
 from .. import planner as P
 from .._lib import init_device
+from ..kernels import release_workspaces
 from ..planner.memplan import MemOptPlan
 from ..planner.schedule import async_ops
 from .graph import profile_graph
@@ -126,6 +127,7 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
                           "pinned host allocation failed: " + str(e).split("\n")[0][:160])
     finally:
         del ex
+        release_workspaces()  # per-stream scratch of this trial's stream
         gc.collect()
         torch.cuda.synchronize(device)
         torch.cuda.empty_cache()
