@@ -193,8 +193,6 @@ class Pipeline:
             tot += t.numel() * t.element_size()
         for d in s.slot_buf:
             tot += sum(t.numel() * t.element_size() for t in d.values())
-        for d in (s.work,):
-            tot += sum(t.numel() * t.element_size() for t in d.values())
         return tot
 
     def _send_fwd_streams(self, x: int, j: int):

@@ -229,10 +229,12 @@ class StageExecutor:
         # recompute before their first backward reader until their last -- so
         # they cost no device memory in between (the planner's
         # w * (micro_peak - saved) model, memopt.py:156-158); transient
-        # un-saved tensors share one workspace buffer.
+        # un-saved tensors ("ephemeral") live the same way, from production to
+        # their last in-stage forward reader (the m_d release of the profile,
+        # runtime/graph.py), never across micro-batches.
         self.evicted = self.swap_ids | self.recompute_ids
         self.slot_buf: List[Dict[str, torch.Tensor]] = [{} for _ in range(self.w)]
-        self.work: Dict[str, torch.Tensor] = {}
+        self.ephemeral: Set[str] = set()
         self.host: Dict[str, List[torch.Tensor]] = {}
         self.live: Dict[str, torch.Tensor] = {}
         ids_needed = {out_tid(n) for n in self._produced_or_received()}
@@ -247,7 +249,7 @@ class StageExecutor:
                     self.host[tid] = [torch.empty(shape, dtype=dt, pin_memory=True)
                                       for _ in range(self.w)]
             else:
-                self.work[tid] = torch.empty(shape, dtype=dt, device=device)
+                self.ephemeral.add(tid)
         if self.needs_ids:
             ishape, idt = cfg.input_spec(micro_batch)
             self.ids = [torch.empty(ishape, dtype=idt, device=device) for _ in range(self.w)]
@@ -304,7 +306,7 @@ class StageExecutor:
         # lifetimes of evicted tensors (positions within this stage's node list)
         pos = {n.id: i for i, n in enumerate(self.nodes)}
         self.fwd_last: Dict[str, float] = {}
-        for tid in self.evicted:
+        for tid in self.evicted | self.ephemeral:
             src, kind = tid.rsplit(".", 1)
             users = [src] if kind != "out" else [n.id for n in self.nodes if src in n.inputs]
             last = max((pos[u] for u in users), default=-1)
@@ -362,12 +364,10 @@ class StageExecutor:
     def buf(self, tid: str, slot: int, phase: str) -> torch.Tensor:
         if tid in self.slot_buf[slot]:
             return self.slot_buf[slot][tid]
-        if tid in self.evicted:
+        if tid in self.evicted or tid in self.ephemeral:
             if tid not in self.live:
-                raise KeyError(f"stage {self.stage}: evicted tensor {tid} is not materialised")
+                raise KeyError(f"stage {self.stage}: tensor {tid} is not materialised")
             return self.live[tid]
-        if tid in self.work:
-            return self.work[tid]
         raise KeyError(f"stage {self.stage}: no buffer for {tid}")
 
     def _alloc_live(self, tid: str) -> torch.Tensor:
@@ -405,7 +405,7 @@ class StageExecutor:
             for tid in self.recv_ids:
                 if tid in self.swap_ids:
                     self._swap_out(tid, slot)
-                if tid in self.evicted and self.fwd_last[tid] < 0:
+                if (tid in self.evicted or tid in self.ephemeral) and self.fwd_last[tid] < 0:
                     del self.live[tid]
             fused_gelus = set(self.fwd_gelu_of.values()) | set(self.fwd_add_of.values())
             for i, n in enumerate(self.nodes):
@@ -413,7 +413,7 @@ class StageExecutor:
                 if any(t in self.swap_ids for t in produced):
                     self._d2h_backpressure()
                 for t in produced:
-                    if t in self.evicted:
+                    if t in self.evicted or t in self.ephemeral:
                         self._alloc_live(t)
                 if self.node_timer is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
@@ -430,7 +430,7 @@ class StageExecutor:
                     del self.live[t]  # last in-stage forward reader done (swaps: D2H ordered)
 
     def recv_buffer(self, tid: str, mb: int) -> torch.Tensor:
-        if tid in self.evicted:
+        if tid in self.evicted or tid in self.ephemeral:
             self._drop_leftovers()
             return self._alloc_live(tid)
         return self.buf(tid, self.slot_of(mb), "fwd")
@@ -439,15 +439,13 @@ class StageExecutor:
         """Zero-copy receive (co-located stages): the message buffer becomes this
         stage's buffer of tid for micro-batch mb.  The sender hands over a
         private copy, so nothing else writes it."""
-        if tid in self.evicted:
+        if tid in self.evicted or tid in self.ephemeral:
             self._drop_leftovers()
             self.live[tid] = msg
             return
         slot = self.slot_of(mb)
         if tid in self.slot_buf[slot]:
             self.slot_buf[slot][tid] = msg
-        elif tid in self.work:
-            self.work[tid] = msg
         else:
             raise KeyError(f"stage {self.stage}: no buffer for {tid}")
 
@@ -465,10 +463,8 @@ class StageExecutor:
             t = self.slot_buf[slot][tid]
             self.slot_buf[slot][tid] = torch.empty_like(t)
             return t
-        if tid in self.work:
-            t = self.work[tid]
-            self.work[tid] = torch.empty_like(t)
-            return t
+        if tid in self.ephemeral and tid in self.live:
+            return self.live.pop(tid)
         return None
 
     def _outputs(self, n: NodeDef) -> List[str]:
@@ -844,6 +840,8 @@ class StageExecutor:
                         self._alloc_live(t)
                         for i in self.chains[t]:
                             self._node_fwd_replay(self.all_nodes[i], slot, ver)
+                        for e in [e for e in self.live if e in self.ephemeral]:
+                            del self.live[e]  # chain intermediates
                 if self.node_timer is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(st)
@@ -892,9 +890,10 @@ class StageExecutor:
 
     def _node_fwd_replay(self, n: NodeDef, slot: int, ver: int) -> None:
         # outputs of a replayed node land in a live buffer if evicted, else in
-        # their normal home (slot buffer or workspace)
+        # their normal home (slot buffer); ephemeral ones in a live buffer that
+        # the backward drops once the chain is replayed
         for t in [out_tid(n.id)] + self.self_tids(n):
-            if t in self.evicted and t not in self.live:
+            if (t in self.evicted or t in self.ephemeral) and t not in self.live:
                 self._alloc_live(t)
         self._node_fwd(n, slot, ver, "bwd")
 

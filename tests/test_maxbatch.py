@@ -1,8 +1,11 @@
 """Max-trainable-batch harness (runtime/maxbatch.py): planning arms on CPU, the
 on-GPU stage check (cap enforcement, no memory carried between trials) on a B200."""
+import gc
+
 import pytest
 import torch
 
+from paper_2505_05856_b200.kernels import release_workspaces
 from paper_2505_05856_b200.runtime.maxbatch import GIB, check_stage, max_batch, try_batch
 from paper_2505_05856_b200.runtime.model import PRESETS
 from paper_2505_05856_b200.runtime.graph import profile_graph
@@ -43,6 +46,8 @@ def test_check_stage_no_carryover_gpu():
     from paper_2505_05856_b200 import planner as P
     ample = P.PlanConfig(stages=2, schedule=P.SCHEDULE_ASYNC, capacity=1 << 62, bandwidth=BW)
     plan = P.plan_from_cuts(g, ample, r["cuts"])
+    release_workspaces()  # scratch cached by earlier tests in this process
+    gc.collect()
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated()
     peaks = []
