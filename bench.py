@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="bert-large")
     ap.add_argument("--micro-batch", type=int, default=32)
-    ap.add_argument("--stages", type=int, default=0, help="default: 8 at N=1, N otherwise")
+    ap.add_argument("--stages", type=int, default=0, help="default: 8 at N=1, N otherwise; "
+                    "l < N at N>1 runs N/l data-parallel replicas of an l-stage pipeline")
     ap.add_argument("--micro-batches", type=int, default=32)
     ap.add_argument("--capacity-gib", type=float, default=160.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

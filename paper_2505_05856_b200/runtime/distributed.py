@@ -16,8 +16,20 @@ grad(j) on one side, the reverse on the other) can deadlock; with one
 communicator per direction each stream carries a single, identically ordered
 message sequence (simulate.py's per-direction `_Channel`, :103-114).
 
+Data-parallel replicas of a shallower pipeline (beyond
+the reference): with world = l * d ranks, rank r runs stage r % l + 1 of
+replica r // l (a replica's stages are consecutive ranks; on NVSwitch the
+mapping is free).  Replicas train on different micro-batches with identical
+weights: after every backward (1F1B, before the per-micro-batch AdamW) or once
+before the iteration's optimizer step (GPipe), each stage all-reduces its flat
+fp32 weight gradient over the d ranks holding the same stage (one NCCL
+communicator per stage); the 1/d of the mean is folded into the loss-gradient
+scale, so every replica applies the same update and the stashed weight
+versions stay identical.
+
 The same code runs with the gloo backend on CPU tensors (tests/test_distributed_cpu.py
-drives it with a stand-in stage to check ordering and message matching).
+drives it with a stand-in stage to check ordering, message matching and the
+replica gradient sum).
 """
 
 from __future__ import annotations
@@ -34,16 +46,43 @@ from ..planner.schedule import async_ops, sync_ops
 
 
 class BoundaryChannels:
-    """Per-direction process groups for every stage boundary."""
+    """Per-direction process groups for every stage boundary of every replica,
+    plus one data-parallel group per stage when there are several replicas.
 
-    def __init__(self, world: int):
-        self.world = world
-        self.fwd: List[Optional[object]] = []
-        self.bwd: List[Optional[object]] = []
+    fwd[k][p] / bwd[k][p]: boundary p (stage p+1 -> p+2) of replica k;
+    dp[p]: the ranks holding stage p+1 in every replica (None if d = 1)."""
+
+    def __init__(self, world: int, stages: Optional[int] = None):
+        l = stages or world
+        if l < 1 or world % l:
+            raise ValueError(f"world size {world} is not a multiple of the stage count {l}")
+        self.world, self.stages, self.replicas = world, l, world // l
+        self.fwd: List[List[object]] = []
+        self.bwd: List[List[object]] = []
         # every rank must create every group, in the same order
-        for x in range(world - 1):
-            self.fwd.append(dist.new_group([x, x + 1]))
-            self.bwd.append(dist.new_group([x, x + 1]))
+        for k in range(self.replicas):
+            base = k * l
+            fw, bw = [], []
+            for p in range(l - 1):
+                fw.append(dist.new_group([base + p, base + p + 1]))
+                bw.append(dist.new_group([base + p, base + p + 1]))
+            self.fwd.append(fw)
+            self.bwd.append(bw)
+        self.dp: List[Optional[object]] = [None] * l
+        if self.replicas > 1:
+            self.dp = [dist.new_group([k * l + p for k in range(self.replicas)]) for p in range(l)]
+
+    def position(self, rank: int) -> Tuple[int, int]:
+        """(replica k, 0-based stage index p) of a rank."""
+        return rank // self.stages, rank % self.stages
+
+
+def _dp_sync(stage, group) -> None:
+    """Sum the stage's weight gradients over its data-parallel group."""
+    if group is None:
+        return
+    for t in stage.dp_grads():
+        dist.all_reduce(t, group=group)
 
 
 def _send(ts: List[torch.Tensor], dst: int, group, copy: bool = False) -> List[object]:
@@ -73,39 +112,48 @@ def run_stage_step(stage, chans: BoundaryChannels, rank: int, world: int, m: int
 
     `stage` provides recv_ids/send_ids, recv_buffer/send_buffer(tid, j),
     forward(j, ids, labels, loss_out), backward(j) -> {tid: grad},
-    set_recv_grad(tid, t), finish_backward(j), grad_like(tid) (a fresh buffer)."""
-    x = rank + 1
+    set_recv_grad(tid, t), finish_backward(j), grad_like(tid) (a fresh buffer),
+    and, with data-parallel replicas (chans.replicas > 1), dp_grads() -> the
+    tensors to all-reduce.  `world` is the stage count of one replica's plan
+    times the replica count (chans decides the split)."""
+    k, p = chans.position(rank)
+    l = chans.stages
+    x = p + 1
+    fwd_ch, bwd_ch, dp = chans.fwd[k], chans.bwd[k], chans.dp[p]
     pending: List[object] = []
     stream = getattr(stage, "stream", None)
     ctx = torch.cuda.stream(stream) if stream is not None else _nullctx()
     with ctx:
-        ops = sync_ops(world, m, x) if schedule == SCHEDULE_SYNC else async_ops(world, m, x)
+        ops = sync_ops(l, m, x) if schedule == SCHEDULE_SYNC else async_ops(l, m, x)
         for kind, j, _ in ops:
             if on_op is not None:
                 on_op("start", kind, j)
             if kind == "fwd":
                 if x > 1:
                     _recv([stage.recv_buffer(t, j) for t in stage.recv_ids], rank - 1,
-                          chans.fwd[rank - 1])
+                          fwd_ch[p - 1])
                 stage.forward(j, ids=None if ids is None else ids[j - 1],
                               labels=None if labels is None else labels[j - 1],
                               loss_out=None if loss is None else loss[j - 1:j])
-                if x < world:
+                if x < l:
                     pending += _send([stage.send_buffer(t, j) for t in stage.send_ids], rank + 1,
-                                     chans.fwd[rank], copy=True)
+                                     fwd_ch[p], copy=True)
             else:
-                if x < world:
+                if x < l:
                     bufs = [stage.grad_like(t) for t in stage.send_ids]
-                    _recv(bufs, rank + 1, chans.bwd[rank])
+                    _recv(bufs, rank + 1, bwd_ch[p])
                     for t, b in zip(stage.send_ids, bufs):
                         stage.set_recv_grad(t, b)
                 grads = stage.backward(j)
                 if x > 1:
-                    pending += _send([grads[t] for t in stage.recv_ids], rank - 1, chans.bwd[rank - 1])
+                    pending += _send([grads[t] for t in stage.recv_ids], rank - 1, bwd_ch[p - 1])
+                if schedule != SCHEDULE_SYNC:
+                    _dp_sync(stage, dp)  # before this micro-batch's AdamW
                 stage.finish_backward(j)
             if on_op is not None:
                 on_op("end", kind, j)
         if schedule == SCHEDULE_SYNC:
+            _dp_sync(stage, dp)
             stage.optimizer_step()
         for w, _ in pending:
             w.wait()
@@ -127,7 +175,8 @@ def init_process_group_from_env(backend: str) -> Tuple[int, int]:
 
 
 def run_bench_distributed(args) -> None:
-    """bench.py at N>1 (torchrun): an l=N stage plan, stage x on rank x-1."""
+    """bench.py at N>1 (torchrun): an l-stage plan (l = --stages, default N), one
+    stage per GPU; N/l data-parallel replicas of it when l < N."""
     import json
     from .. import kernels as K
     from .. import planner as P
@@ -140,20 +189,22 @@ def run_bench_distributed(args) -> None:
     torch.cuda.set_device(local)
     init_device(local)
     rank, world = init_process_group_from_env("nccl")
-    chans = BoundaryChannels(world)
+    stages = args.stages or world
+    chans = BoundaryChannels(world, stages)
+    rep_k, pos = chans.position(rank)
+    d = chans.replicas
     cfg = PRESETS[args.model]
     b, m = args.micro_batch, args.micro_batches
-    stages = world
     g = profile_graph(cfg, b)
     plan = P.plan(g, P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC,
                                   capacity=int(args.capacity_gib * (1 << 30)), bandwidth=64 << 30))
-    lo, hi = P.stage_bounds(plan.cuts, len(g))[rank]
+    lo, hi = P.stage_bounds(plan.cuts, len(g))[pos]
     dev = torch.device("cuda", local)
     stream = torch.cuda.Stream(device=dev)
-    stage = StageExecutor(cfg=cfg, g=g, nodes=build_nodes(cfg), lo=lo, hi=hi, stage=rank + 1,
-                          stages=stages, micro_batch=b, memopt=plan.memopt[rank],
-                          init=init_params(cfg, 0), device=dev, stream=stream)
-    ids, labels = synthetic_batch(cfg, m, b, seed=0)
+    stage = StageExecutor(cfg=cfg, g=g, nodes=build_nodes(cfg), lo=lo, hi=hi, stage=pos + 1,
+                          stages=stages, micro_batch=b, memopt=plan.memopt[pos],
+                          init=init_params(cfg, 0), device=dev, stream=stream, dp_replicas=d)
+    ids, labels = synthetic_batch(cfg, m, b, seed=rep_k)  # each replica its own data
     ids_d = ids.to(dev) if stage.needs_ids else None
     lab_d = labels.to(dev) if stage.is_last else None
     loss = torch.zeros(m, device=dev) if stage.is_last else None
@@ -189,7 +240,7 @@ def run_bench_distributed(args) -> None:
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     launches = torch.tensor([(K.INSTR.launches - l0) // args.steps], device=dev, dtype=torch.int64)
     dist.all_reduce(launches)
-    value = args.steps * m * b / (ms.item() / 1e3)
+    value = args.steps * m * b * d / (ms.item() / 1e3)
 
     # e2e: inputs copied H2D from pinned memory on the ranks that embed, the loss
     # vector read back on the last rank, every step; wall time, max over ranks
@@ -216,19 +267,23 @@ def run_bench_distributed(args) -> None:
                         + (labels.numel() * labels.element_size() if stage.is_last else 0)],
                        device=dev, dtype=torch.int64)
     dist.all_reduce(h2d)
-    e2e = {"value": args.steps * m * b / wall.item(), "unit": "samples/s",
-           "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": m * 4}
+    e2e = {"value": args.steps * m * b * d / wall.item(), "unit": "samples/s",
+           "h2d_bytes_per_step": int(h2d.item()), "d2h_bytes_per_step": m * 4 * d}
     if rank == 0:
         out = {"metric": "samples/sec at 1/2/4/8 stages; max trainable batch under per-GPU mem cap",
                "value": round(value, 2), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms.item() / args.steps, 3),
-               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+               "higher_is_better": True, "scaling": "strong" if d == 1 else "weak",
+               "vs_baseline": None, "dtype": "bf16",
                "data": "synthetic",
                "config": {"workload": f"{args.model} s{cfg.seq}, {stages}-stage DawnPiper 1F1B plan, "
-                                      f"one stage per GPU, NCCL P2P boundaries, b={b}, m={m}",
-                          "model": args.model, "global_batch": b * m, "seq_len": cfg.seq,
-                          "micro_batch": b, "micro_batches": m, "stages": stages,
-                          "cuts": list(plan.cuts.positions), "parallelism": f"pp{stages}"},
+                                      f"one stage per GPU, NCCL P2P boundaries, b={b}, m={m}"
+                                      + (f", {d} data-parallel replicas (per-update gradient "
+                                         f"all-reduce)" if d > 1 else ""),
+                          "model": args.model, "global_batch": b * m * d, "seq_len": cfg.seq,
+                          "micro_batch": b, "micro_batches": m, "stages": stages, "replicas": d,
+                          "cuts": list(plan.cuts.positions),
+                          "parallelism": f"pp{stages}" + (f"xdp{d}" if d > 1 else "")},
                "gpu_launches": int(launches.item()), "e2e": e2e, "clocks": clk,
                "roofline": None, "model_tflops": round(value * cfg.flops_per_sample() / 1e12, 1)}
         print(json.dumps(out), flush=True)

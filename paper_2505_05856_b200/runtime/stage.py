@@ -154,7 +154,8 @@ class StageExecutor:
                  lo: int, hi: int, stage: int, stages: int, micro_batch: int, memopt: MemOptPlan,
                  init: Dict[str, torch.Tensor], device: torch.device, stream: torch.cuda.Stream,
                  opt: AdamWConfig = AdamWConfig(), slots: Optional[int] = None,
-                 schedule: str = SCHEDULE_ASYNC, micro_batches: Optional[int] = None):
+                 schedule: str = SCHEDULE_ASYNC, micro_batches: Optional[int] = None,
+                 dp_replicas: int = 1):
         self.cfg, self.g = cfg, g
         self.all_nodes = list(nodes)
         self.nodes = self.all_nodes[lo:hi + 1]
@@ -187,7 +188,10 @@ class StageExecutor:
         # dense weight gradients are written by the first backward of an
         # iteration and accumulated by the rest (sync only)
         self._wgrad_acc = False
-        self.grad_scale = 1.0 / (self.out_rows * self.m_sync)  # mean over the iteration's tokens
+        # mean over the iteration's tokens (and, with data-parallel replicas whose
+        # gradients are summed by an all-reduce, over the replicas)
+        self.dp_replicas = dp_replicas
+        self.grad_scale = 1.0 / (self.out_rows * self.m_sync * dp_replicas)
         self.is_first = lo == 0
         # stages holding an embedding node take the micro-batch's token ids
         # (encoder-decoder: `dembed` may sit behind a cut at position 0)
@@ -876,6 +880,11 @@ class StageExecutor:
         self.grad_init = set()
         self._skip_bwd = set()
         self.shared_grads = set()
+
+    def dp_grads(self) -> List[torch.Tensor]:
+        """Tensors a data-parallel all-reduce sums before the optimizer step: the
+        stage's flat fp32 weight gradient (runtime/distributed.py)."""
+        return [self.params.grad]
 
     def optimizer_step(self) -> None:
         """Sync schedule: one AdamW step over the gradients accumulated by the

@@ -17,10 +17,12 @@ import torch.multiprocessing as mp
 class FakeStage:
     """y = x + 10*stage (+ ids for stage 1); grad in = grad out + stage."""
 
-    def __init__(self, rank, world):
+    def __init__(self, rank, world, stages=None):
+        l = stages or world
         self.rank, self.world = rank, world
-        self.x = rank + 1
-        self.is_first, self.is_last = rank == 0, rank == world - 1
+        self.replica = rank // l
+        self.x = rank % l + 1
+        self.is_first, self.is_last = self.x == 1, self.x == l
         self.recv_ids = [] if self.is_first else ["act"]
         self.send_ids = [] if self.is_last else ["act"]
         self.inbox = {}
@@ -28,6 +30,8 @@ class FakeStage:
         self.grads = {}
         self.log = []
         self.results = {}
+        self.wgrad = torch.zeros(3)
+        self.synced = []  # weight gradient seen by each optimizer update
 
     def recv_buffer(self, tid, j):
         self.inbox[j] = torch.zeros(4)
@@ -52,14 +56,22 @@ class FakeStage:
 
     def backward(self, j):
         self.log.append(("bwd", j))
+        self.wgrad += float((self.replica + 1) * j)  # replica-specific weight gradient
         g = self.grads.get("act", torch.full((4,), float(j)))  # last stage seeds with j
         return {"act": g + self.x}
 
+    def dp_grads(self):
+        return [self.wgrad]
+
     def finish_backward(self, j):
         self.grads = {}
+        if not self.sync:
+            self.synced.append(self.wgrad[0].item())
+            self.wgrad.zero_()
 
     def optimizer_step(self):
         self.log.append(("opt", 0))
+        self.synced.append(self.wgrad[0].item())
 
 
 def _free_port():
@@ -70,15 +82,19 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, m, q, schedule="async_1f1b"):
+def _worker(rank, world, port, m, q, schedule="async_1f1b", stages=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2505_05856_b200.runtime.distributed import BoundaryChannels, run_stage_step
     from paper_2505_05856_b200.planner.schedule import async_ops, sync_ops
-    chans = BoundaryChannels(world)
-    st = FakeStage(rank, world)
-    ids = torch.arange(m * 4, dtype=torch.int32).reshape(m, 4) if rank == 0 else None
+    chans = BoundaryChannels(world, stages)
+    l = chans.stages
+    st = FakeStage(rank, world, stages)
+    st.sync = schedule == "sync"
+    # replica k's ids are offset by 1000 k: a message crossing replicas shows up
+    ids = (torch.arange(m * 4, dtype=torch.int32).reshape(m, 4) + 1000 * st.replica
+           if st.is_first else None)
     grads_seen = {}
     orig_set = st.set_recv_grad
 
@@ -88,11 +104,11 @@ def _worker(rank, world, port, m, q, schedule="async_1f1b"):
     st.set_recv_grad = spy
     run_stage_step(st, chans, rank, world, m, ids=ids, schedule=schedule)
     if schedule == "sync":
-        expect = [(k, j) for k, j, _ in sync_ops(world, m, rank + 1)] + [("opt", 0)]
+        expect = [(k, j) for k, j, _ in sync_ops(l, m, st.x)] + [("opt", 0)]
     else:
-        expect = [(k, j) for k, j, _ in async_ops(world, m, rank + 1)]
+        expect = [(k, j) for k, j, _ in async_ops(l, m, st.x)]
     q.put((rank, st.log == expect, {j: v.tolist() for j, v in st.results.items()},
-           {k: v.tolist() for k, v in grads_seen.items()}))
+           {k: v.tolist() for k, v in grads_seen.items()}, st.synced))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -108,7 +124,7 @@ def test_gloo_pipeline_order_and_matching(world, m, schedule):
         p.start()
     out = {}
     for _ in range(world):
-        rank, ok, res, grads = q.get(timeout=120)
+        rank, ok, res, grads, _ = q.get(timeout=120)
         out[rank] = (ok, res, grads)
     for p in procs:
         p.join(timeout=60)
@@ -128,3 +144,38 @@ def test_gloo_pipeline_order_and_matching(world, m, schedule):
         for k in range(1, m + 1):
             j = m + 1 - k if schedule == "sync" else k
             assert grads[k] == [float(j + add)] * 4
+
+
+@pytest.mark.parametrize("world,stages,m,schedule", [(4, 2, 5, "async_1f1b"), (4, 2, 4, "sync"),
+                                                     (6, 3, 5, "async_1f1b")])
+def test_gloo_data_parallel_replicas(world, stages, m, schedule):
+    """world = l * d: every replica runs its own pipeline on its own data, and
+    every optimizer update sees the weight gradient summed over the replicas."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, q, schedule, stages))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        rank, ok, res, grads, synced = q.get(timeout=120)
+        out[rank] = (ok, res, grads, synced)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    d = world // stages
+    shift = 10 * sum(range(1, stages + 1))
+    for r in range(world):
+        k, x = r // stages, r % stages + 1
+        assert out[r][0], f"rank {r} did not run the {schedule} op order"
+        if x == stages:  # last stage of replica k: its own replica's ids only
+            for j in range(1, m + 1):
+                assert out[r][1][j] == [float((j - 1) * 4 + i + shift + 1000 * k) for i in range(4)]
+        # replica k contributes (k+1)*j per backward; the all-reduce sums replicas
+        rep_sum = sum(range(1, d + 1))
+        if schedule == "sync":
+            assert out[r][3] == [float(rep_sum * sum(range(1, m + 1)))]
+        else:
+            assert out[r][3] == [float(rep_sum * j) for j in range(1, m + 1)]

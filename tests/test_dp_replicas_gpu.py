@@ -1,0 +1,73 @@
+"""Data-parallel replicas (runtime/distributed.py) on the
+real stage executor: two replicas of a one-stage pipeline, each on its own
+half of the data, whose weight gradients are summed before every AdamW update
+(what the per-stage all-reduce does), must train like one replica on the
+concatenated micro-batches.  The gloo tests cover the communication; this
+covers the executor side (dp_grads, the 1/d folded into the loss gradient)."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _executor(cfg, g, b, d, init):
+    from paper_2505_05856_b200 import planner as P
+    from paper_2505_05856_b200.runtime.model import build_nodes
+    from paper_2505_05856_b200.runtime.stage import StageExecutor
+    ample = P.PlanConfig(stages=1, schedule=P.SCHEDULE_ASYNC, capacity=1 << 62, bandwidth=1 << 40)
+    plan = P.plan_from_cuts(g, ample, [])
+    dev = torch.device("cuda", 0)
+    return StageExecutor(cfg=cfg, g=g, nodes=build_nodes(cfg), lo=0, hi=len(g) - 1, stage=1,
+                         stages=1, micro_batch=b, memopt=plan.memopt[0], init=init, device=dev,
+                         stream=torch.cuda.Stream(device=dev), dp_replicas=d)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny-causal"])
+def test_two_replicas_match_one_double_batch(name):
+    from paper_2505_05856_b200._lib import init_device
+    from paper_2505_05856_b200.runtime.graph import profile_graph
+    from paper_2505_05856_b200.runtime.model import PRESETS, init_params, synthetic_batch
+    init_device(0)
+    cfg = PRESETS[name]
+    b, m = 2, 4
+    init = init_params(cfg, 0)
+    dev = torch.device("cuda", 0)
+    halves = [synthetic_batch(cfg, m, b, seed=k) for k in range(2)]
+    ids = [[h[0][j].to(dev) for j in range(m)] for h in halves]
+    lab = [[h[1][j].to(dev) for j in range(m)] for h in halves]
+
+    one = _executor(cfg, profile_graph(cfg, 2 * b), 2 * b, 1, init)
+    reps = [_executor(cfg, profile_graph(cfg, b), b, 2, init) for _ in range(2)]
+    loss1 = torch.zeros(m, device=dev)
+    lossr = [torch.zeros(m, device=dev) for _ in range(2)]
+    w0 = one.params.master.clone()
+    for j in range(1, m + 1):
+        with torch.cuda.stream(one.stream):
+            one.forward(j, ids=torch.cat([ids[0][j - 1], ids[1][j - 1]]),
+                        labels=torch.cat([lab[0][j - 1], lab[1][j - 1]]), loss_out=loss1[j - 1:j])
+            one.backward(j)
+            one.finish_backward(j)
+        for k, r in enumerate(reps):
+            with torch.cuda.stream(r.stream):
+                r.forward(j, ids=ids[k][j - 1], labels=lab[k][j - 1], loss_out=lossr[k][j - 1:j])
+                r.backward(j)
+        torch.cuda.synchronize()
+        total = reps[0].dp_grads()[0] + reps[1].dp_grads()[0]  # the all-reduce (sum)
+        for r in reps:
+            r.dp_grads()[0].copy_(total)
+        torch.cuda.synchronize()
+        for r in reps:
+            with torch.cuda.stream(r.stream):
+                r.finish_backward(j)
+        torch.cuda.synchronize()
+    # replicas apply identical updates
+    assert torch.equal(reps[0].params.master, reps[1].params.master)
+    assert torch.equal(reps[0].params.ring, reps[1].params.ring)
+    # ... equal to one replica on the concatenated data (bf16 GEMMs at b vs 2b)
+    d1 = (one.params.master - w0).double()
+    dr = (reps[0].params.master - w0).double()
+    cos = torch.nn.functional.cosine_similarity(d1, dr, dim=0).item()
+    rel = ((d1 - dr).norm() / d1.norm()).item()
+    assert cos > 0.98 and rel < 0.2, (cos, rel)
+    # the mean of the replicas' per-token losses is the double batch's loss
+    torch.testing.assert_close((lossr[0] + lossr[1]) / 2, loss1, rtol=2e-2, atol=1e-3)
