@@ -3,6 +3,9 @@ next to torch SDPA (cuDNN / flash backends) for scale."""
 import sys, json, torch
 sys.path.insert(0, ".")
 from paper_2505_05856_b200 import _lib, kernels as k
+if len(sys.argv) > 1:  # A/B: another build of the library
+    from pathlib import Path
+    _lib.SO_PATH = Path(sys.argv[1]).resolve()
 _lib.init_device(0)
 
 
