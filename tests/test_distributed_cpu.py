@@ -179,3 +179,10 @@ def test_gloo_data_parallel_replicas(world, stages, m, schedule):
             assert out[r][3] == [float(rep_sum * sum(range(1, m + 1)))]
         else:
             assert out[r][3] == [float(rep_sum * j) for j in range(1, m + 1)]
+
+
+def test_replica_layout_rejects_ragged_world():
+    """world must be a whole number of replicas of the stage plan."""
+    from paper_2505_05856_b200.runtime.distributed import BoundaryChannels
+    with pytest.raises(ValueError, match="multiple of the stage count"):
+        BoundaryChannels(6, 4)  # raises before any process group is created
