@@ -14,7 +14,10 @@ For each micro-batch size b:
      standing in for its neighbours.  The cap is enforced on the caching
      allocator (torch.cuda.set_per_process_memory_fraction); an allocation
      beyond it raises OutOfMemoryError.
-b is trainable iff the planner returns a plan and every stage completes.
+b is trainable iff the planner returns a plan and every stage completes; for
+the planned strategies a stage that runs out of memory on the GPU sends b back
+to the planner with a 10% / 20% smaller capacity first (`max_batch`, measured-
+memory feedback for what the profile's memory model leaves out).
 
 The baseline is the even-compute split: `compute_balanced` cuts with empty
 memopt plans (`plan_from_cuts(..., require_feasible=False)`, as the reference
@@ -143,11 +146,15 @@ def host_bytes(plan, stages: int) -> List[int]:
 
 def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth: int,
               strategy: str, device: int = 0, times=None, run_gpu: bool = True,
-              host_cap: int = 96 * GIB) -> dict:
+              host_cap: int = 96 * GIB, margin: float = 0.0) -> dict:
+    """One trial; `margin` shrinks the capacity handed to the planner by that
+    fraction (the measured-memory feedback of `max_batch`)."""
     g = profile_graph(model, b, times=times)
     reserve = optimizer_reserve(model, g, stages, b=b)
-    pcap = cap - reserve
+    pcap = int((cap - reserve) * (1.0 - margin))
     rec = {"b": b, "strategy": strategy, "planner_capacity": pcap, "reserve": reserve}
+    if margin:
+        rec["margin"] = margin
     cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=max(1, pcap),
                        bandwidth=bandwidth)
     if pcap <= 0:
@@ -163,9 +170,9 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
                 rec.update(feasible=False, reason=f"planner: {e}")
                 return rec
             need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b)
-            if cap - need >= cfg.capacity:
+            if int((cap - need) * (1.0 - margin)) >= cfg.capacity:
                 break
-            pcap = cap - need
+            pcap = int((cap - need) * (1.0 - margin))
             if pcap <= 0:
                 rec.update(feasible=False, reason="stage overhead alone exceeds the cap")
                 return rec
@@ -218,17 +225,28 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
 
 def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, strategy: str,
               b_max: int = 64, device: int = 0, log=None, host_cap: int = 96 * GIB,
-              run_gpu: bool = True) -> Tuple[int, List[dict]]:
-    """Largest feasible b (0 if none) by doubling then bisection."""
+              run_gpu: bool = True, margins: Tuple[float, ...] = (0.1, 0.2)) -> Tuple[int, List[dict]]:
+    """Largest feasible b (0 if none) by doubling then bisection.
+
+    Measured-memory feedback for the planned strategies: the planner's memory
+    model (the reference's) has no term for backward gradient buffers or kernel
+    scratch, so when a plan's stage runs out of memory on the GPU the same b is
+    re-planned with the capacity shrunk by each of `margins` in turn before it
+    counts as infeasible (the fixed even-compute split has nothing to re-plan)."""
     hist: List[dict] = []
 
     def ok(b: int) -> bool:
-        r = try_batch(model, b, stages, cap, bandwidth, strategy, device, host_cap=host_cap,
-                      run_gpu=run_gpu)
-        hist.append(r)
-        if log:
-            log(r)
-        return bool(r.get("feasible"))
+        for margin in (0.0,) + (tuple(margins) if strategy != "even_compute" else ()):
+            r = try_batch(model, b, stages, cap, bandwidth, strategy, device, host_cap=host_cap,
+                          run_gpu=run_gpu, margin=margin)
+            hist.append(r)
+            if log:
+                log(r)
+            if r.get("feasible"):
+                return True
+            if "OOM on GPU" not in r.get("reason", ""):
+                return False  # planner / host-memory infeasibility: a margin cannot help
+        return False
 
     if not ok(1):
         return 0, hist

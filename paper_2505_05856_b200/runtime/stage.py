@@ -225,6 +225,19 @@ class StageExecutor:
         unknown = (self.swap_ids | self.recompute_ids) - needed
         if unknown:
             raise ValueError(f"stage {stage}: memopt names tensors it does not hold: {sorted(unknown)}")
+        # recompute chains (memopt.py:91-115), replayed in forward order.  What a
+        # chain reads from outside itself must still be there at backward time:
+        # the chain stops at saved tensors inside the stage, but a boundary
+        # tensor received from the previous stage can feed it directly, so such
+        # inputs are kept resident like saved tensors.
+        self.chains: Dict[str, List[int]] = {}
+        for tid in sorted(self.recompute_ids):
+            p = self.index[tid.rsplit(".", 1)[0]]
+            chain, _ = producer_chain(g, p, lo, hi)
+            self.chains[tid] = chain
+            inside = {self.all_nodes[i].id for i in chain}
+            for i in chain:
+                needed.update(out_tid(u) for u in self.all_nodes[i].inputs if u not in inside)
 
         # Residency classes: resident saved tensors get one static buffer per
         # in-flight slot; evicted tensors (memopt actions) are allocated only
@@ -270,12 +283,6 @@ class StageExecutor:
         # planner's model does not see (memopt.py:156-158 frees a swapped tensor
         # at once); 256 MiB is ~5 ms of the measured 55 GB/s host link
         self.d2h_budget = 256 << 20
-        # recompute chains (memopt.py:91-115), replayed in forward order
-        self.chains: Dict[str, List[int]] = {}
-        for tid in sorted(self.recompute_ids):
-            p = self.index[tid.rsplit(".", 1)[0]]
-            chain, _ = producer_chain(g, p, lo, hi)
-            self.chains[tid] = chain
         # per-slot micro-batch bookkeeping
         self.slot_mb = [0] * self.w
         self.grads: Dict[str, torch.Tensor] = {}
