@@ -69,3 +69,16 @@ def test_check_stage_enforces_cap_gpu():
     plan = P.plan_from_cuts(g, ample, P.compute_balanced(g, 0, len(g) - 1, [1, 1]).positions)
     c = check_stage(cfg, g, plan, 1, b, 1 << 20)  # 1 MiB: the weights alone do not fit
     assert not c.ok and "memory" in c.error.lower()
+
+
+def test_release_workspaces_cpu():
+    """The per-stream scratch cache drops its buffers (all, or one device's)."""
+    from paper_2505_05856_b200 import kernels as K
+    K._WS.clear()
+    K._workspace("cpu", 16, 1234)     # integer stream handles: no CUDA needed
+    K._workspace("meta", 16, 1234)
+    assert len(K._WS) == 2
+    release_workspaces("cpu")
+    assert list(K._WS) == [("meta", 1234)]
+    release_workspaces()
+    assert not K._WS
