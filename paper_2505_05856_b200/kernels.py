@@ -35,16 +35,25 @@ INSTR = _Instrument()
 _WS = {}
 
 
+def _dev_index(device) -> int:
+    d = torch.device(device) if not isinstance(device, int) else torch.device("cuda", device)
+    return d.index if d.index is not None else torch.cuda.current_device()
+
+
 def _workspace(device, floats: int, stream) -> torch.Tensor:
     """Per-(device, stream) f32 scratch for two-phase reductions / attention.
-    Kernels on one stream use it in stream order; streams never share one."""
-    handle = _s(stream)
-    key = (device, handle)
+    Kernels on one stream use it in stream order; streams never share one.
+    The buffer is allocated in that stream's order (None = the current stream,
+    a raw handle is wrapped), so the caching allocator never hands its memory
+    to another stream while kernels on this one may still use it."""
+    ts = _torch_stream(stream)
+    if ts is None:
+        ts = torch.cuda.ExternalStream(int(stream), device=torch.device("cuda", _dev_index(device)))
+    key = (_dev_index(device), ts.cuda_stream)
     t = _WS.get(key)
     if t is None or t.numel() < floats:
-        ts = _torch_stream(stream)
-        with torch.cuda.stream(ts) if ts is not None else _nullctx():
-            t = torch.empty(max(floats, 1 << 20), dtype=F32, device=device)
+        with torch.cuda.stream(ts):
+            t = torch.empty(max(floats, 1 << 20), dtype=F32, device=torch.device("cuda", key[0]))
         _WS[key] = t
     return t
 
@@ -54,7 +63,8 @@ def release_workspaces(device=None) -> None:
     short-lived streams (per-trial executors) call this when they are done: the
     cache is keyed by stream handle, so it would otherwise keep one buffer per
     stream the pool ever handed out."""
-    for key in [k for k in _WS if device is None or k[0] == device]:
+    want = None if device is None else _dev_index(device)
+    for key in [k for k in _WS if want is None or k[0] == want]:
         del _WS[key]
 
 

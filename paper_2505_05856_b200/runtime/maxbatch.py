@@ -138,10 +138,10 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
 
 
 def host_bytes(plan, stages: int) -> List[int]:
-    """Pinned host bytes per stage: w = l-x+1 slots of every swapped tensor."""
-    return [(stages - x) * sum(a.size for a in m.actions if a.kind == "swap")
-            + sum(a.size for a in m.actions if a.kind == "swap")
-            for x, m in enumerate(plan.memopt)]
+    """Pinned host bytes per stage: w = l-x+1 slots (x 1-based, as
+    StageExecutor allocates them) of every swapped tensor."""
+    return [(stages - x + 1) * sum(a.size for a in m.actions if a.kind == "swap")
+            for x, m in enumerate(plan.memopt, start=1)]
 
 
 def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth: int,

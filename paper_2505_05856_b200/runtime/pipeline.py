@@ -157,9 +157,11 @@ class Pipeline:
                     from .._lib import check, lib
                     check(lib().dpn_enable_peer(a, b), "dpn_enable_peer")
         if cfg.capacity is not None:
+            # the plan's capacity is per stage; stages sharing a GPU share its cap
             for d in set(self.stage_dev):
                 total = torch.cuda.get_device_properties(d).total_memory
-                torch.cuda.set_per_process_memory_fraction(min(1.0, cfg.capacity / total), d)
+                share = cfg.capacity * self.stage_dev.count(d)
+                torch.cuda.set_per_process_memory_fraction(min(1.0, share / total), d)
         self.streams = {d: torch.cuda.Stream(device=d) for d in set(self.stage_dev)}
         # one stream per stage when several stages share a device (see RunConfig)
         self.multi = cfg.concurrent_stages and len(set(self.stage_dev)) < self.l
@@ -195,34 +197,57 @@ class Pipeline:
             tot += sum(t.numel() * t.element_size() for t in d.values())
         return tot
 
+    def _peer_msg(self, src: torch.Tensor, d_src: int, d_dst: int, sst, dst_st) -> torch.Tensor:
+        """Copy src (on device d_src, live in stream sst) into a fresh buffer on
+        d_dst, pushed by the sender: the buffer is allocated in the receiver's
+        stream order, the copy runs on sst (so the sender cannot overwrite or
+        free src before it is read), and the receiver waits on the returned
+        buffer through the caller's event."""
+        with torch.cuda.device(d_dst), torch.cuda.stream(dst_st):
+            msg = torch.empty(src.shape, dtype=src.dtype, device=torch.device("cuda", d_dst))
+            ready = torch.cuda.Event()
+            ready.record(dst_st)
+        sst.wait_event(ready)
+        K.copy_d2d(msg, src, dst_dev=d_dst, src_dev=d_src, stream=sst)
+        msg.record_stream(sst)
+        return msg
+
     def _send_fwd_streams(self, x: int, j: int):
         """Concurrent co-located stages: the sender copies its boundary
         activations into message buffers on its own stream; the receiver's
         stream waits on the recorded event before delivering."""
         src = self.stages[x - 1]
-        sst = self.stage_streams[x - 1]
+        sst, dst_st = self.stage_streams[x - 1], self.stage_streams[x]
+        d_src, d_dst = self.stage_dev[x - 1], self.stage_dev[x]
         out = {}
         with torch.cuda.stream(sst):
             for tid in src.send_ids:
+                if d_src != d_dst:  # stages on different GPUs: peer copy
+                    out[tid] = self._peer_msg(src.send_buffer(tid, j), d_src, d_dst, sst, dst_st)
+                    continue
                 # buffers the sender's backward never reads change owner (no copy)
                 msg = src.release_send_buffer(tid, j)
                 if msg is None:
                     a = src.send_buffer(tid, j)
                     msg = torch.empty_like(a)
-                    K.copy_d2d(msg, a, stream=sst)
-                msg.record_stream(self.stage_streams[x])
+                    K.copy_d2d(msg, a, dst_dev=d_src, src_dev=d_src, stream=sst)
+                msg.record_stream(dst_st)
                 out[tid] = msg
             ev = torch.cuda.Event()
             ev.record(sst)
         return out, ev
 
     def _send_bwd_streams(self, x: int, grads: Dict[str, torch.Tensor]):
-        """Gradients of stage x's inputs handed to stage x-1 (same device)."""
+        """Gradients of stage x's inputs handed to stage x-1."""
         sst, dst = self.stage_streams[x - 1], self.stage_streams[x - 2]
+        d_src, d_dst = self.stage_dev[x - 1], self.stage_dev[x - 2]
         out = {}
         seen = set()
         with torch.cuda.stream(sst):
             for tid, g in grads.items():
+                if d_src != d_dst:
+                    out[tid] = self._peer_msg(g, d_src, d_dst, sst, dst)
+                    continue
                 # the sender drops its gradient buffers after this backward, so they
                 # are handed over as they are; one buffer aliased by two tensors'
                 # gradients is copied (the receiver may update either in place)
@@ -242,18 +267,21 @@ class Pipeline:
         a free slot yet -- exactly like a posted NCCL send)."""
         src = self.stages[x - 1]
         d_src, d_dst = self.stage_dev[x - 1], self.stage_dev[x]
-        st = self.streams[d_dst]
+        sst, st = self.streams[d_src], self.streams[d_dst]
+        out = {}
+        for tid in src.send_ids:
+            a = src.send_buffer(tid, j)
+            if d_src != d_dst:
+                out[tid] = self._peer_msg(a, d_src, d_dst, sst, st)
+            else:
+                with torch.cuda.stream(st):
+                    msg = torch.empty_like(a)
+                    K.copy_d2d(msg, a, dst_dev=d_dst, src_dev=d_src, stream=st)
+                out[tid] = msg
         if d_src != d_dst:
             ev = torch.cuda.Event()
-            ev.record(self.streams[d_src])
+            ev.record(sst)
             st.wait_event(ev)
-        out = {}
-        with torch.cuda.stream(st):
-            for tid in src.send_ids:
-                a = src.send_buffer(tid, j)
-                msg = torch.empty_like(a, device=torch.device("cuda", d_dst))
-                K.copy_d2d(msg, a, dst_dev=d_dst, src_dev=d_src, stream=st)
-                out[tid] = msg
         return out
 
     def _deliver_fwd(self, x: int, j: int, msgs: Dict[str, torch.Tensor]) -> None:
@@ -267,17 +295,20 @@ class Pipeline:
     def _send_bwd(self, x: int, grads: Dict[str, torch.Tensor]) -> Dict[str, torch.Tensor]:
         # x is the sending stage (1-based); returns fresh buffers owned by stage x-1
         d_src, d_dst = self.stage_dev[x - 1], self.stage_dev[x - 2]
-        st = self.streams[d_dst]
+        sst, st = self.streams[d_src], self.streams[d_dst]
+        out = {}
+        for tid, gsrc in grads.items():
+            if d_src != d_dst:
+                out[tid] = self._peer_msg(gsrc, d_src, d_dst, sst, st)
+            else:
+                with torch.cuda.stream(st):
+                    gdst = torch.empty_like(gsrc)
+                    K.copy_d2d(gdst, gsrc, dst_dev=d_dst, src_dev=d_src, stream=st)
+                out[tid] = gdst
         if d_src != d_dst:
             ev = torch.cuda.Event()
-            ev.record(self.streams[d_src])
+            ev.record(sst)
             st.wait_event(ev)
-        out = {}
-        with torch.cuda.stream(st):
-            for tid, gsrc in grads.items():
-                gdst = torch.empty_like(gsrc, device=torch.device("cuda", d_dst))
-                K.copy_d2d(gdst, gsrc, dst_dev=d_dst, src_dev=d_src, stream=st)
-                out[tid] = gdst
         return out
 
     def step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
@@ -432,6 +463,16 @@ def run(plan: PartitionPlan, g: ComputationGraph, cfg: RunConfig,
             raise ValueError(f"cannot infer the model of graph {g.name!r}; pass model=")
         model = PRESETS[base]
     pipe = Pipeline(model, g, plan, cfg)
+    try:
+        return _run(pipe, model, cfg, ids, labels, steps)
+    finally:
+        if cfg.capacity is not None:  # the cap does not outlive the run
+            for d in set(pipe.stage_dev):
+                torch.cuda.set_per_process_memory_fraction(1.0, d)
+
+
+def _run(pipe: Pipeline, model, cfg: RunConfig, ids, labels, steps: int) -> RunReport:
+    from .model import synthetic_batch
     if ids is None:
         ids, labels = synthetic_batch(model, cfg.micro_batches, cfg.micro_batch_size, cfg.seed)
     d0, dl = pipe.stage_dev[0], pipe.stage_dev[-1]

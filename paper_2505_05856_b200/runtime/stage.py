@@ -336,6 +336,7 @@ class StageExecutor:
                 self.bwd_last[t] = min(self.bwd_last.get(t, pos[n.id]), pos[n.id])
                 self.bwd_first[t] = max(self.bwd_first.get(t, pos[n.id]), pos[n.id])
         self.swap_lookahead = 2
+        self._recv_mb = 0  # micro-batch whose boundary inputs are being delivered
         # profiler hook: when a list, every node forward / backward is bracketed
         # with CUDA events on the compute stream -> (node id, "fwd"|"bwd", e0, e1)
         self.node_timer: Optional[list] = None
@@ -394,6 +395,14 @@ class StageExecutor:
         for t in [t for t in self.live if self.fwd_last.get(t) == math.inf]:
             del self.live[t]
 
+    def _begin_recv(self, mb: int) -> None:
+        """First delivery of micro-batch mb: the previous forward's send-only
+        leftovers go now, once -- not per delivered tensor, which would drop a
+        relayed tensor of mb itself delivered earlier in the same batch."""
+        if self._recv_mb != mb:
+            self._drop_leftovers()
+            self._recv_mb = mb
+
     def slot_of(self, mb: int) -> int:
         return (mb - 1) % self.w
 
@@ -442,7 +451,7 @@ class StageExecutor:
 
     def recv_buffer(self, tid: str, mb: int) -> torch.Tensor:
         if tid in self.evicted or tid in self.ephemeral:
-            self._drop_leftovers()
+            self._begin_recv(mb)
             return self._alloc_live(tid)
         return self.buf(tid, self.slot_of(mb), "fwd")
 
@@ -451,7 +460,7 @@ class StageExecutor:
         stage's buffer of tid for micro-batch mb.  The sender hands over a
         private copy, so nothing else writes it."""
         if tid in self.evicted or tid in self.ephemeral:
-            self._drop_leftovers()
+            self._begin_recv(mb)
             self.live[tid] = msg
             return
         slot = self.slot_of(mb)
@@ -817,6 +826,7 @@ class StageExecutor:
         ver = self.params.pinned(mb)
         with torch.cuda.stream(st):
             self._drop_leftovers()
+            self._recv_mb = 0
             if not self._wgrad_acc:
                 self.params.zero_accum_grads(stream=st)
             # swap-ins in first-use order (backward runs right to left), kept

@@ -72,13 +72,35 @@ def test_check_stage_enforces_cap_gpu():
 
 
 def test_release_workspaces_cpu():
-    """The per-stream scratch cache drops its buffers (all, or one device's)."""
+    """The per-stream scratch cache drops its buffers (all, or one device's);
+    torch.device / "cuda:k" / k name the same device key."""
     from paper_2505_05856_b200 import kernels as K
     K._WS.clear()
-    K._workspace("cpu", 16, 1234)     # integer stream handles: no CUDA needed
-    K._workspace("meta", 16, 1234)
-    assert len(K._WS) == 2
-    release_workspaces("cpu")
-    assert list(K._WS) == [("meta", 1234)]
+    K._WS[(0, 1234)] = torch.empty(1)
+    K._WS[(1, 1234)] = torch.empty(1)
+    K._WS[(1, 99)] = torch.empty(1)
+    release_workspaces(torch.device("cuda", 0))
+    assert sorted(K._WS) == [(1, 99), (1, 1234)]
+    release_workspaces("cuda:1")
+    assert not K._WS
+    K._WS[(0, 5)] = torch.empty(1)
     release_workspaces()
     assert not K._WS
+
+
+def test_host_bytes_match_executor_slots_cpu():
+    """Pinned host bytes per stage = (l - x + 1) slots (1-based x, the ring depth
+    StageExecutor allocates) of every swapped tensor."""
+    from paper_2505_05856_b200 import planner as P
+    from paper_2505_05856_b200.runtime.maxbatch import host_bytes
+    cfg = PRESETS["tiny"]
+    g = profile_graph(cfg, 8)
+    cb = P.compute_balanced(g, 0, len(g) - 1, [1] * 3)
+    top = max(s.sched_peak for s in P.stage_profiles(g, cb, 3, P.SCHEDULE_ASYNC))
+    plan = P.plan(g, P.PlanConfig(stages=3, schedule=P.SCHEDULE_ASYNC, capacity=int(0.6 * top),
+                                  bandwidth=16 << 30))
+    hb = host_bytes(plan, 3)
+    for x, m in enumerate(plan.memopt, start=1):
+        swap = sum(a.size for a in m.actions if a.kind == "swap")
+        assert hb[x - 1] == (3 - x + 1) * swap
+    assert any(hb)

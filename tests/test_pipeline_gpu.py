@@ -192,3 +192,18 @@ def test_pipeline_amoebanet_memopt_and_sync():
     _compare(cfg, g, plan, b=4, m=6, cos_min=CNN_COS, aggregate=True)
     cfg, g, plan = _setup("tiny-amoeba", 2, 4.0, 16 << 30, b=4, schedule="sync")
     _compare(cfg, g, plan, b=4, m=4, cos_min=CNN_COS, aggregate=True)
+
+
+def test_pipeline_middle_stage_relays_several_tensors():
+    """A one-node middle stage (d0.ln1, cuts 2|3) receives embed.out and
+    b0.ln1.out, which it only passes on, besides its own input: every relayed
+    tensor must survive until the stage's sends (regression: each delivery used
+    to drop the previously delivered send-only tensors of the same micro-batch)."""
+    from paper_2505_05856_b200 import planner as P
+    from paper_2505_05856_b200.runtime.graph import profile_graph
+    from paper_2505_05856_b200.runtime.model import PRESETS
+    cfg = PRESETS["tiny-t5"]
+    g = profile_graph(cfg, 2)
+    pc = P.PlanConfig(stages=4, schedule="async_1f1b", capacity=1 << 40, bandwidth=16 << 30)
+    plan = P.plan_from_cuts(g, pc, (2, 3, 20))
+    _compare(cfg, g, plan)
