@@ -27,6 +27,7 @@ only by tests and diagnostics.
 from __future__ import annotations
 
 from dataclasses import dataclass
+from bisect import bisect_left
 from fractions import Fraction
 from typing import Callable, List, Optional, Sequence, Tuple
 
@@ -211,27 +212,54 @@ def compute_balanced(g: ComputationGraph, lo: int, hi: int, weights: Sequence) -
 # -- memory balance ----------------------------------------------------------------
 
 
+def _first_reach(g: ComputationGraph, start: int, hi: int, reached: Callable[[int], bool]) -> int:
+    """Smallest k in [start, hi] whose running peak from `start` satisfies
+    `reached`, or hi + 1.  The running peak of a segment grown to the right is
+    non-decreasing (segment_peak is a range max), so this is a bisection over
+    O(1) range-max queries instead of a node-by-node walk."""
+    a, b = start, hi + 1
+    while a < b:
+        k = (a + b) // 2
+        if reached(g.segment_peak(start, k)):
+            b = k
+        else:
+            a = k + 1
+    return a
+
+
 def _crossing_walk(g: ComputationGraph, lo: int, hi: int, nbound: int,
                    target_of: Callable[[int], Fraction]) -> List[int]:
-    """First-crossing walk over [lo, hi]: cut when the running peak of the
-    current segment reaches its target; at most nbound cuts."""
+    """First-crossing cuts over [lo, hi]: a segment ends at the first node at
+    which its running peak (from zero at the segment start) reaches the
+    segment's target; at most nbound cuts."""
     cuts: List[int] = []
-    target = target_of(0)
-    cur = peak = 0
-    nodes = g.nodes
-    for k in range(lo, hi + 1):
-        nd = nodes[k]
-        cur += nd.m_a + nd.m_p
-        if cur > peak:
-            peak = cur
-        cur -= nd.m_d
-        if peak >= target:
-            cuts.append(k)
-            if len(cuts) == nbound:
-                break
-            target = target_of(len(cuts))
-            cur = peak = 0
+    start = lo
+    while len(cuts) < nbound and start <= hi:
+        target = Fraction(target_of(len(cuts)))
+        num, den = target.numerator, target.denominator
+        k = _first_reach(g, start, hi, lambda peak: peak * den >= num)
+        if k > hi:
+            break
+        cuts.append(k)
+        start = k + 1
     return cuts
+
+
+def _halving_cut(g: ComputationGraph, lo: int, hi: int) -> int:
+    """compute_balanced(g, lo, hi, [1, 1]).positions[0] by bisection over the
+    time prefix sums: left time L(e) grows with e and right time R(e) shrinks,
+    so max(L, R) is R until L >= R (from e*) and L after; the answer is the
+    first e attaining the minimum."""
+    pre = g._ptime
+    base = pre[lo]
+    total = pre[hi + 1] - base
+    e_star = bisect_left(pre, base + (total + 1) // 2, lo + 1, hi + 1) - 1
+    left_best = total - (pre[e_star] - base) if e_star > lo else None  # R(e* - 1)
+    right_best = pre[e_star + 1] - base if e_star < hi else None      # L(e*)
+    if right_best is None or (left_best is not None and left_best <= right_best):
+        # first e with R(e) <= left_best, i.e. prefix index e + 1 reaching total - best
+        return bisect_left(pre, base + total - left_best, lo + 1, e_star + 1) - 1
+    return e_star
 
 
 def _first_crossing(g: ComputationGraph, stages: int,
@@ -274,7 +302,10 @@ def split_pair(g: ComputationGraph, lo: int, hi: int, stages: int, schedule: str
     seq = list(left_stages) + list(right_stages)
     parts = len(seq)
     nl = len(left_stages)
-    cb = compute_balanced(g, lo, hi, [1] * parts).positions[nl - 1]
+    if parts == 2:
+        cb = _halving_cut(g, lo, hi)
+    else:
+        cb = compute_balanced(g, lo, hi, [1] * parts).positions[nl - 1]
 
     if schedule == SCHEDULE_ASYNC:
         weights = [Fraction(1, stages - x + 1) for x in seq]

@@ -1,3 +1,4 @@
+import pathlib
 """Host-side runtime logic that needs no GPU: profile graphs built from the
 model definition, the co-located issue order, plan <-> executor tensor naming."""
 import json
@@ -27,14 +28,31 @@ def test_profile_graph_is_a_valid_schema1_profile(name, tmp_path):
             assert t.id in (out_tid(n.id), stats_tid(n.id))
 
 
-def test_profile_loads_in_the_reference_format(tmp_path):
-    """Documents written by the B200 side parse with the strict reference schema
-    rules restated in planner.profile (unknown/missing fields rejected)."""
+def test_profile_parser_rejects_unknown_fields(tmp_path):
+    """The schema rules restated in planner.profile reject unknown node fields."""
     g = profile_graph(PRESETS["tiny"], 2)
     doc = P.profile_doc(g)
     doc["nodes"][0]["extra"] = 1
     with pytest.raises(P.ProfileParseError, match="unknown node field"):
         P.graph_from_doc(doc)
+
+
+@pytest.mark.skipif(not pathlib.Path("/root/reference/pkg/src").exists(),
+                    reason="reference not mounted")
+@pytest.mark.parametrize("model,b", [("tiny", 2), ("tiny-t5", 2), ("bert-large", 8),
+                                     ("gpt2-xl", 1), ("t5-large", 4), ("amoebanet-d", 16)])
+def test_profile_loads_in_the_reference(tmp_path, model, b):
+    """Profiles written by the B200 side load in the unmodified reference's
+    strict `load_profile` with the same canonical hash."""
+    import sys
+    sys.path.insert(0, "/root/reference/pkg/src")
+    import dawnplan
+    g = profile_graph(PRESETS[model], b)
+    f = tmp_path / "g.json"
+    P.save_profile(g, f)
+    rg = dawnplan.load_profile(f)
+    assert dawnplan.canonical_hash(rg) == P.canonical_hash(g)
+    assert len(rg.nodes) == len(g)
 
 
 def test_param_count_matches_model_definition():
