@@ -37,7 +37,8 @@ def _setup(name, stages, cap_frac, bandwidth, b=2, m=6, schedule="async_1f1b"):
     return cfg, g, P.plan(g, pc)
 
 
-def _compare(cfg, g, plan, b=2, m=6, steps=2, cos_min=0.95, aggregate=False):
+def _compare(cfg, g, plan, b=2, m=6, steps=2, cos_min=0.95, aggregate=False, seed=3,
+             ratio_tol=0.1, lr=1e-3):
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -46,10 +47,10 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2, cos_min=0.95, aggregate=False):
     from paper_2505_05856_b200.runtime.model import AdamWConfig, build_nodes, init_params, synthetic_batch
     from paper_2505_05856_b200.runtime.pipeline import Pipeline, RunConfig
 
-    opt = AdamWConfig(lr=1e-3)
+    opt = AdamWConfig(lr=lr)
     rc = RunConfig(micro_batches=m, micro_batch_size=b, opt=opt, trace=False)
     pipe = Pipeline(cfg, g, plan, rc)
-    ids, labels = synthetic_batch(cfg, m, b, seed=3)
+    ids, labels = synthetic_batch(cfg, m, b, seed=seed)
     gpu_losses = []
     for _ in range(steps):
         gpu_losses.append(pipe.step(ids.cuda(), labels.cuda()).tolist())
@@ -80,6 +81,7 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2, cos_min=0.95, aggregate=False):
         ratio = float(dg.norm() / dr.norm())
         assert rel <= REL and cos >= cos_min and abs(ratio - 1) <= 0.1, (rel, cos, ratio)
         return gpu_losses
+    stats = []
     for s in pipe.stages:
         for name in s.params.slots:
             got = s.params.master_view(name).float().cpu()
@@ -104,8 +106,11 @@ def _compare(cfg, g, plan, b=2, m=6, steps=2, cos_min=0.95, aggregate=False):
             # zero-init parameters (biases, LN beta) *are* their update, whose
             # bf16-vs-fp32 Adam noise is a few %: judged with every parameter on
             # the update's direction (cos) and magnitude (norm ratio).
-            if (w0.norm() > 0 and rel > REL) or cos < cos_min or abs(ratio - 1) > 0.1:
+            stats.append((name, round(rel, 5), round(cos, 4), round(ratio, 4)))
+            if (w0.norm() > 0 and rel > REL) or cos < cos_min or abs(ratio - 1) > ratio_tol:
                 bad.append((name, round(rel, 5), round(cos, 4), round(ratio, 4)))
+    worst = sorted(stats, key=lambda r: -r[1])[:3]
+    print(f"{cfg.name}: worst rel {worst}; min cos {min(r[2] for r in stats):.4f}")
     assert not bad, bad
     return gpu_losses
 

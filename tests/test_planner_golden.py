@@ -65,3 +65,38 @@ def test_plans_byte_identical(planner_golden):
                 assert hashlib.sha256(P.trace_to_csv(r).encode()).hexdigest() == sim["csv_sha256"]
             checked += 1
     assert checked > 300
+
+
+def test_measured_baseline_profiles_plans_byte_identical():
+    """Plans on the B200-measured BERT-base / BERT-large / GPT-2 XL / T5-large
+    profiles (111-509 nodes, memopt-active capacities) against the unmodified
+    reference's output (oracle/gen_golden_large.py)."""
+    import gzip
+    from pathlib import Path
+    here = Path(__file__).parent / "golden"
+    doc = json.loads(gzip.decompress((here / "planner_golden_large.json.gz").read_bytes()))
+    graphs = {}
+    big = 0
+    for rec in doc["cases"]:
+        name = rec["profile"]
+        if name not in graphs:
+            graphs[name] = P.graph_from_doc(json.loads(gzip.decompress(
+                (here / "profiles" / f"{name}.json.gz").read_bytes())))
+        g = graphs[name]
+        assert P.canonical_hash(g) == rec["hash"]
+        cfg = P.PlanConfig(stages=rec["stages"], schedule=rec["schedule"], capacity=rec["capacity"],
+                           bandwidth=rec["bandwidth"])
+        if "error" in rec:
+            with pytest.raises(P.InfeasibleModelError) as ei:
+                P.plan(g, cfg)
+            assert str(ei.value) == rec["error"]
+            continue
+        p, trace = P.plan_with_trace(g, cfg)
+        pj = P.plan_json(p)
+        assert hashlib.sha256(pj.encode()).hexdigest() == rec["plan_json_sha256"], (name, rec["stages"])
+        assert [[s.lo, s.hi, s.first_stage, s.last_stage, s.cb, s.mb, s.chosen] for s in trace] == rec["trace"]
+        r = P.simulate(p, g, P.SimConfig(micro_batches=rec["sim"]["m"], schedule=rec["schedule"],
+                                         bandwidth=rec["bandwidth"], capacity=rec["capacity"]))
+        assert hashlib.sha256(P.report_json(r).encode()).hexdigest() == rec["sim"]["report_sha256"]
+        big += len(g) >= 200 and any(m.actions for m in p.memopt)
+    assert big >= 3
