@@ -121,29 +121,52 @@ class Clocks:
 
 # ---------------------------------------------------------------- oracle ----
 
-def cpu_port_sample(model_name: str, stages: int, samples: int = 1):
-    """Time the oracle CPU port (fp32, all host threads) on `samples` samples of
-    the workload: one micro-batch of b=samples through every stage, forward,
-    backward and AdamW, in 1F1B order.  Returns (samples/s, cores, description)."""
-    import torch
-    from oracle.train_ref import reference_train
-    from paper_2505_05856_b200.runtime.model import PRESETS, build_nodes, init_params, synthetic_batch
-    torch.set_num_threads(os.cpu_count() or 1)
-    cfg = PRESETS[model_name]
-    nodes = [n.id for n in build_nodes(cfg)]
-    per = (len(nodes) + stages - 1) // stages
-    stage_nodes = [nodes[i:i + per] for i in range(0, len(nodes), per)]
-    from oracle.train_ref import dims_from
-    dims = dims_from(cfg, build_nodes(cfg))
-    init = init_params(cfg, 0)
-    ids, labels = synthetic_batch(cfg, 1, samples, seed=0)
-    opt = dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
-    t0 = time.perf_counter()
-    reference_train(dims, init, ids, labels, stage_nodes, opt, steps=1)
-    dt = time.perf_counter() - t0
-    return samples / dt, torch.get_num_threads(), (
-        f"{samples} sample(s) of {model_name} s{cfg.seq}: fwd+bwd+AdamW through {len(stage_nodes)} "
-        f"stages in 1F1B order, fp32 torch on CPU, {dt:.1f} s")
+CPU_SAMPLE = {"micro_batch": 2, "micro_batches": 2}
+
+
+def committed_profile(model: str, b: int):
+    """A B200-measured profile committed under tests/golden/profiles (the
+    inputs of the reference-generated large goldens), or None."""
+    import gzip
+    from paper_2505_05856_b200 import planner as P
+    f = ROOT / "tests" / "golden" / "profiles" / f"{model}_b{b}.json.gz"
+    if not f.exists():
+        return None
+    return P.graph_from_doc(json.loads(gzip.decompress(f.read_bytes())))
+
+
+class CpuPort:
+    """The oracle CPU port (fp32 torch, all host threads) of the training step
+    on a bounded sample of the workload: the same model and the same stage
+    cuts, m micro-batches of b samples in 1F1B order, forward + backward +
+    PipeDream AdamW after every backward.  Model construction, parameter init
+    and Adam state are built here, outside any timed region; `step()` times
+    one training iteration alone."""
+
+    def __init__(self, model_name: str, cuts, b: int = CPU_SAMPLE["micro_batch"],
+                 m: int = CPU_SAMPLE["micro_batches"]):
+        import torch
+        from oracle.train_ref import RefPipeline, dims_from
+        from paper_2505_05856_b200.runtime.model import PRESETS, build_nodes, init_params, synthetic_batch
+        torch.set_num_threads(os.cpu_count() or 1)
+        self.cores = torch.get_num_threads()
+        cfg = PRESETS[model_name]
+        nodes = build_nodes(cfg)
+        ids = [n.id for n in nodes]
+        edges = [-1, *cuts, len(ids) - 1]
+        stage_nodes = [ids[edges[i] + 1:edges[i + 1] + 1] for i in range(len(edges) - 1)]
+        self.ids, self.labels = synthetic_batch(cfg, m, b, seed=0)
+        self.ref = RefPipeline(dims_from(cfg, nodes), init_params(cfg, 0), stage_nodes,
+                               dict(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01))
+        self.samples = b * m
+        self.sample = (f"{m} micro-batches x b={b} of {model_name} s{cfg.seq} through the same "
+                       f"{len(stage_nodes)}-stage cuts in 1F1B order: fwd + bwd + AdamW per "
+                       f"micro-batch, fp32 torch on CPU (setup excluded)")
+
+    def step(self) -> float:
+        t0 = time.perf_counter()
+        self.ref.train(self.ids, self.labels)
+        return time.perf_counter() - t0
 
 
 # ---------------------------------------------------------------- ours ------
@@ -307,39 +330,144 @@ def run_ours(args):
         "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk,
         "losses_last_step": [round(x, 4) for x in losses.tolist()[:4]],
     }
+    out["model_vs_measured"] = model_vs_measured(pipe, g, plan, ids_d, lab_d, b, m, value)
+    out["planner"] = planner_timing(args.model, b, stages, t_plan)
     if not args.no_cpu_baseline:
-        v, cores, sample = cpu_port_sample(args.model, stages)
-        out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": cores, "kind": "port",
-                               "sample": sample}
+        port = CpuPort(args.model, plan.cuts.positions)
+        port.step()  # first touch of the fp32 buffers
+        dt = port.step()
+        out["cpu_baseline"] = {"value": round(port.samples / dt, 4), "unit": UNIT, "cores": port.cores,
+                               "kind": "port", "sample": port.sample + f", {dt:.1f} s"}
     print(json.dumps(out), flush=True)
 
 
+def model_vs_measured(pipe, g, plan, ids_d, lab_d, b: int, m: int, measured: float) -> dict:
+    """The cost model (profile + plan + simulate, simulate.py:130-166,
+    326-336) beside what the run measures.
+
+    * per stage: forward / backward time of one micro-batch as the planner
+      models it (segment times of the measured profile; memopt added_time
+      charged to the backward, simulate.py:136-138) vs the stage's mean
+      forward / backward in a step with the stages chained op by op (no
+      co-located overlap);
+    * simulate()'s iteration time and samples/s for the plan on l GPUs (what
+      the plan predicts for the 8-GPU deployment);
+    * the 1-GPU co-located prediction -- all stages' work on one device:
+      b / sum_x (T_x + added_x) -- vs the measured samples/s and the measured
+      steady-state iteration time (async_iteration on a traced step)."""
+    import torch
+    from paper_2505_05856_b200 import planner as P
+    from paper_2505_05856_b200.planner import stage_bounds
+    bounds = stage_bounds(plan.cuts, len(g))
+    ev: list = []
+    pipe.serialize = True
+    pipe.step(ids_d, lab_d, ev)
+    torch.cuda.synchronize()
+    pipe.serialize = False
+    per = {}
+    for x, j, kind, e0, e1 in ev:
+        per.setdefault((x, kind), []).append(e0.elapsed_time(e1) * 1e3)
+    stages = []
+    for x, (lo, hi) in enumerate(bounds, start=1):
+        mf = sum(per[(x, "fwd")]) / len(per[(x, "fwd")])
+        mb = sum(per[(x, "bwd")]) / len(per[(x, "bwd")])
+        stages.append({"stage": x, "fwd_us_model": g.segment_fwd_time(lo, hi), "fwd_us_measured": round(mf, 1),
+                       "bwd_us_model": g.segment_bwd_time(lo, hi) + plan.memopt[x - 1].added_time,
+                       "bwd_us_measured": round(mb, 1)})
+    # measured steady-state iteration of the real (concurrent) schedule
+    ev = []
+    t0 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    t0.record(pipe.streams[pipe.stage_dev[0]])
+    losses = pipe.step(ids_d, lab_d, ev)
+    rep = pipe.report(ev, t0, losses, 0.0)
+    sim = P.simulate(plan, g, P.SimConfig(micro_batches=m, schedule=plan.schedule,
+                                          bandwidth=plan.config.bandwidth, capacity=plan.config.capacity))
+    serial_us = sum(s.time + mo.added_time for s, mo in zip(plan.stages, plan.memopt))
+    return {
+        "per_stage": stages,
+        "simulate_l_gpus": {"stages": len(bounds), "iteration_time_us": round(sim.iteration_time, 1),
+                            "samples_per_s": round(b * 1e6 / sim.iteration_time, 1),
+                            "bubble_ratio": round(sim.bubble_ratio, 4)},
+        "one_gpu": {"model_samples_per_s": round(b * 1e6 / serial_us, 1),
+                    "measured_samples_per_s": round(measured, 1),
+                    "model_iteration_us": serial_us,
+                    "measured_iteration_us": round(rep.iteration_time, 1)},
+    }
+
+
+def planner_timing(model: str, b: int, stages: int, t_live: float) -> dict:
+    """Planner wall time: the live plan of this run, and this package's planner
+    vs the unmodified reference (dawnplan.plan_with_trace, timed in the dev
+    container by oracle/gen_golden_large.py) on the same committed B200
+    profile and configuration, with byte-identical plan_json."""
+    import gzip
+    import hashlib
+    from paper_2505_05856_b200 import planner as P
+    out = {"live_plan_s": round(t_live, 3)}
+    gold = ROOT / "tests" / "golden" / "planner_golden_large.json.gz"
+    if not gold.exists():
+        return out
+    cases = json.loads(gzip.decompress(gold.read_bytes()))["cases"]
+    rows = []
+    for rec in cases:
+        if "plan_json_sha256" not in rec:
+            continue
+        prof, bsz = rec["profile"].rsplit("_b", 1)
+        g = committed_profile(prof, int(bsz))
+        cfg = P.PlanConfig(stages=rec["stages"], schedule=rec["schedule"], capacity=rec["capacity"],
+                           bandwidth=rec["bandwidth"])
+        t0 = time.perf_counter()
+        p = P.plan(g, cfg)
+        dt = time.perf_counter() - t0
+        rows.append({"profile": rec["profile"], "stages": rec["stages"], "capacity": rec["capacity"],
+                     "memopt_actions": sum(len(s["memopt"]) for s in rec["plan_doc"]["stages"]),
+                     "ours_s": round(dt, 3), "reference_s": rec["reference_plan_s"],
+                     "identical": hashlib.sha256(P.plan_json(p).encode()).hexdigest() == rec["plan_json_sha256"]})
+    out["vs_reference"] = rows
+    out["reference_timing_host"] = "dev container, 8 cores (the reference is not shipped to the GPU box)"
+    return out
+
+
 def run_reference(args):
+    """The reference arm: the training step's CPU implementation (the oracle
+    port -- the reference `dawnplan` has a planner and an analytic simulator
+    but no executor) on all host cores, same model and same DawnPiper stage
+    cuts as our arm's workload, each step a bounded sample of it (CPU_SAMPLE).
+    The cuts come from planning the committed B200-measured profile of the
+    workload with the package planner (byte-identical to the reference's
+    plan); setup is outside the timed steps."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from paper_2505_05856_b200 import planner as P
+    from paper_2505_05856_b200.runtime.graph import profile_graph
     from paper_2505_05856_b200.runtime.model import PRESETS
-    stages = args.stages or (8 if world == 1 else world)
-    for _ in range(args.warmup):
-        cpu_port_sample(args.model, stages)
-    vals = []
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, cores, sample = cpu_port_sample(args.model, stages)
-        vals.append(v)
-    total = time.perf_counter() - t0
-    value = args.steps / total
     cfg = PRESETS[args.model]
+    stages = args.stages or (8 if world == 1 else world)
+    g = committed_profile(args.model, args.micro_batch)
+    src = "committed B200-measured profile" if g is not None else "analytic profile"
+    if g is None:
+        g = profile_graph(cfg, args.micro_batch)
+    plan = P.plan(g, P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC,
+                                  capacity=int(args.capacity_gib * (1 << 30)), bandwidth=64 << 30))
+    port = CpuPort(args.model, plan.cuts.positions)
+    for _ in range(args.warmup):
+        port.step()
+    total = sum(port.step() for _ in range(args.steps))
+    value = port.samples * args.steps / total
     out = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(total / args.steps * 1e3, 1),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic", "impl": "reference",
-           "config": {"workload": f"{args.model} s{cfg.seq}, {stages}-stage 1F1B, one sample per step "
-                                  f"(CPU port of the training step; the reference dawnplan has no executor)",
-                      "model": args.model, "seq_len": cfg.seq, "stages": stages},
-           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "port",
-                            "sample": sample},
+           "config": {"workload": f"{args.model} s{cfg.seq}, {stages}-stage DawnPiper 1F1B plan "
+                                  f"(cuts from the {src} at b={args.micro_batch}), CPU training step "
+                                  f"on a bounded sample per step",
+                      "model": args.model, "seq_len": cfg.seq, "stages": stages,
+                      "cuts": list(plan.cuts.positions), **CPU_SAMPLE},
+           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": port.cores, "kind": "port",
+                            "sample": port.sample},
            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)

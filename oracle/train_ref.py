@@ -287,61 +287,83 @@ def boundary(stage_nodes: List[List[str]], x: int, dims: dict) -> List[str]:
     return [u for u in before if any(u in _inputs(v, dims) for v in after)]
 
 
+class RefPipeline:
+    """The oracle's stages, built once (parameter copies, Adam state), so a
+    timed caller measures `train` alone."""
+
+    def __init__(self, dims: dict, init: Dict[str, torch.Tensor], stage_nodes: List[List[str]],
+                 opt: dict, schedule: str = "async_1f1b", micro_batches: int = 0):
+        self.l = len(stage_nodes)
+        self.sync = schedule == "sync"
+        self.stages = [RefStage(dims, init, nodes, opt, sync_m=micro_batches if self.sync else 0)
+                       for nodes in stage_nodes]
+        self.sends = [boundary(stage_nodes, x, dims) for x in range(self.l)]
+
+    def train(self, ids: torch.Tensor, labels: torch.Tensor, steps: int = 1) -> List[List[float]]:
+        """`steps` iterations of m micro-batches (ids/labels: int [m, b*s]) in
+        the schedule's per-stage op order; returns the losses [steps][m]."""
+        l, m, stages, sends = self.l, ids.shape[0], self.stages, self.sends
+        if self.sync:
+            assert all(st.sync_m == m for st in stages), "GPipe oracle built for another m"
+        all_losses = []
+        for _ in range(steps):
+            losses = [0.0] * m
+            if self.sync:
+                ops = [[("fwd", j) for j in range(1, m + 1)] + [("bwd", j) for j in range(m, 0, -1)]
+                       for _ in range(l)]
+            else:
+                ops = [one_f_one_b(l, m, x + 1) for x in range(l)]
+            ptr = [0] * l
+            acts: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
+            grads: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
+            left = sum(len(o) for o in ops)
+            while left:
+                moved = False
+                for x in range(l):
+                    while ptr[x] < len(ops[x]):
+                        kind, j = ops[x][ptr[x]]
+                        if kind == "fwd":
+                            if x > 0 and (x - 1, j) not in acts:
+                                break
+                            recv = acts.get((x - 1, j), {})
+                            env = stages[x].forward(j, recv, ids=ids[j - 1], labels=labels[j - 1])
+                            fwd_env = dict(recv)
+                            fwd_env.update(env)
+                            if x < l - 1:
+                                acts[(x, j)] = {u: fwd_env[u].detach() for u in sends[x]}
+                            else:
+                                losses[j - 1] = float(env["head"].detach())
+                        else:
+                            if x < l - 1 and (x, j) not in grads:
+                                break
+                            g_in = stages[x].backward(j, grads.pop((x, j), {}), sends[x])
+                            if x > 0:
+                                grads[(x - 1, j)] = g_in
+                        ptr[x] += 1
+                        left -= 1
+                        moved = True
+                if not moved:
+                    raise RuntimeError("oracle schedule deadlock")
+            for st in stages:
+                st.flush()
+            all_losses.append(losses)
+        return all_losses
+
+    def params(self) -> Dict[str, torch.Tensor]:
+        final = {}
+        for s in self.stages:
+            final.update({k: v.detach().clone() for k, v in s.params.items()})
+        return final
+
+
 def reference_train(dims: dict, init: Dict[str, torch.Tensor], ids: torch.Tensor,
                     labels: torch.Tensor, stage_nodes: List[List[str]], opt: dict,
                     steps: int = 1, schedule: str = "async_1f1b"):
     """Run `steps` iterations of m micro-batches (ids/labels: int [m, b*s]).
     Returns (losses [steps][m], final fp32 parameters)."""
-    l, m = len(stage_nodes), ids.shape[0]
-    sync = schedule == "sync"
-    stages = [RefStage(dims, init, nodes, opt, sync_m=m if sync else 0) for nodes in stage_nodes]
-    sends = [boundary(stage_nodes, x, dims) for x in range(l)]
-    all_losses = []
-    for _ in range(steps):
-        losses = [0.0] * m
-        if sync:
-            ops = [[("fwd", j) for j in range(1, m + 1)] + [("bwd", j) for j in range(m, 0, -1)]
-                   for _ in range(l)]
-        else:
-            ops = [one_f_one_b(l, m, x + 1) for x in range(l)]
-        ptr = [0] * l
-        acts: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
-        grads: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
-        left = sum(len(o) for o in ops)
-        while left:
-            moved = False
-            for x in range(l):
-                while ptr[x] < len(ops[x]):
-                    kind, j = ops[x][ptr[x]]
-                    if kind == "fwd":
-                        if x > 0 and (x - 1, j) not in acts:
-                            break
-                        recv = acts.get((x - 1, j), {})
-                        env = stages[x].forward(j, recv, ids=ids[j - 1], labels=labels[j - 1])
-                        fwd_env = dict(recv)
-                        fwd_env.update(env)
-                        if x < l - 1:
-                            acts[(x, j)] = {u: fwd_env[u].detach() for u in sends[x]}
-                        else:
-                            losses[j - 1] = float(env["head"].detach())
-                    else:
-                        if x < l - 1 and (x, j) not in grads:
-                            break
-                        g_in = stages[x].backward(j, grads.pop((x, j), {}), sends[x])
-                        if x > 0:
-                            grads[(x - 1, j)] = g_in
-                    ptr[x] += 1
-                    left -= 1
-                    moved = True
-            if not moved:
-                raise RuntimeError("oracle schedule deadlock")
-        for st in stages:
-            st.flush()
-        all_losses.append(losses)
-    final = {}
-    for s in stages:
-        final.update({k: v.detach().clone() for k, v in s.params.items()})
-    return all_losses, final
+    ref = RefPipeline(dims, init, stage_nodes, opt, schedule, micro_batches=ids.shape[0])
+    losses = ref.train(ids, labels, steps)
+    return losses, ref.params()
 
 
 def dims_from(cfg, nodes=None) -> dict:
