@@ -58,6 +58,11 @@ def parse():
     ap.add_argument("--capacity-gib", type=float, default=160.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=10)
+    ap.add_argument("--memopt-stage", action="store_true",
+                    help="instead of the throughput line: run the heaviest-memopt stage of a "
+                         "DawnPiper plan under --cap-gib on the GPU and report model vs measured")
+    ap.add_argument("--cap-gib", type=float, default=40.0)
+    ap.add_argument("--swap-gbs", type=float, default=48.0, help="host link the planner assumes")
     return ap.parse_args()
 
 
@@ -473,8 +478,46 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def run_memopt_stage(args):
+    """The memory plan executing: profile the model on the
+    B200 at micro-batch b, plan it for l stages under a per-GPU cap
+    (maxbatch.plan_for_cap: the planner gets the cap minus the optimizer state
+    its model does not see), then run the stage that evicts the most bytes
+    alone on the GPU under the cap with its real 1F1B op list
+    (runtime/memprobe.py) and report the planner's charge beside the measured
+    backward, swap-in stalls, recompute time, copy GB/s and device peak."""
+    from paper_2505_05856_b200.runtime.maxbatch import plan_for_cap
+    from paper_2505_05856_b200.runtime.memprobe import heaviest_stage, probe_stage
+    from paper_2505_05856_b200.runtime.model import PRESETS
+    from paper_2505_05856_b200.runtime.profiler import profile as b200_profile
+    cfg = PRESETS[args.model]
+    b, stages = args.micro_batch, args.stages or 8
+    cap = int(args.cap_gib * (1 << 30))
+    g = b200_profile(cfg, b, iters=args.profile_iters, warmup=3)
+    t0 = time.perf_counter()
+    plan, pcfg = plan_for_cap(cfg, g, stages, cap, int(args.swap_gbs * 1e9), b=b)
+    t_plan = time.perf_counter() - t0
+    x = heaviest_stage(plan)
+    # the executor's memory-faithful defaults, then the throughput knobs
+    # Pipeline runs with (RunConfig.d2h_budget / swap_prefetch)
+    res = probe_stage(cfg, g, plan, x, b, cap=cap)
+    from paper_2505_05856_b200.runtime.pipeline import RunConfig
+    rc = RunConfig(micro_batches=1, micro_batch_size=b)
+    res_overlap = probe_stage(cfg, g, plan, x, b, cap=cap,
+                              swap_knobs={"d2h_budget": rc.d2h_budget, "prefetch_budget": rc.swap_prefetch})
+    out = {"mode": "memopt_stage", "model": args.model, "micro_batch": b, "stages": stages,
+           "cap_bytes": cap, "planner_capacity": pcfg.capacity, "planner_bandwidth_Bps": pcfg.bandwidth,
+           "plan_s": round(t_plan, 3), "cuts": list(plan.cuts.positions),
+           "actions_per_stage": [len(m.actions) for m in plan.memopt],
+           "host_link_GBps_measured_r01": "57 D2H / 55 H2D (profiles/r01_swap_bw.jsonl)",
+           "probe": res, "probe_overlapped": res_overlap}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
+    if args.memopt_stage:
+        return run_memopt_stage(args)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -107,6 +107,8 @@ def _build_parser() -> _Parser:
     r.add_argument("--seed", type=int, default=0)
     r.add_argument("--trace")
     r.add_argument("--out")
+    r.add_argument("--static-peaks", action="store_true",
+                   help="report static buffer bytes instead of measuring each stage's peak")
 
     c = sub.add_parser("compare", help="compute-balanced vs memory-balanced vs full planner")
     planner_args(c)
@@ -203,7 +205,8 @@ def _cmd_run(args) -> int:
     m = _default_m(p.config.stages, p.schedule, args.micro_batches)
     devices = tuple(int(d) for d in args.devices.split(",") if d.strip())
     cfg = RunConfig(micro_batches=m, micro_batch_size=b, devices=devices, seed=args.seed,
-                    trace=True, capacity=p.config.capacity)
+                    trace=True, capacity=p.config.capacity,
+                    measure_stage_peaks=not args.static_peaks)
     try:
         rep = run(p, g, cfg, model=model, steps=max(1, args.steps))
     except Exception as e:  # OOM under the cap = the plan does not fit this device

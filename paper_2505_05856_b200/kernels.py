@@ -300,6 +300,26 @@ def memset(t, value=0, nbytes=None, stream=None):
     check(lib().dpn_memset_async(t.data_ptr(), value, n, _s(stream)), "dpn_memset_async")
 
 
+def swap_out(host_dst, dev_src, copy_stream, ready_event=None):
+    """Swap engine D2H (memopt `swap`): host_dst (pinned) <- dev_src on
+    copy_stream after ready_event (recorded on the compute stream)."""
+    n = dev_src.numel() * dev_src.element_size()
+    check(lib().dpn_swap_out(host_dst.data_ptr(), dev_src.data_ptr(), n, _s(copy_stream),
+                             ready_event.cuda_event if ready_event is not None else None, None),
+          "dpn_swap_out")
+    return n
+
+
+def swap_in(dev_dst, host_src, copy_stream, ready_event=None):
+    """Swap engine H2D prefetch: dev_dst <- host_src (pinned) on copy_stream
+    after ready_event."""
+    n = dev_dst.numel() * dev_dst.element_size()
+    check(lib().dpn_swap_in(dev_dst.data_ptr(), host_src.data_ptr(), n, _s(copy_stream),
+                            ready_event.cuda_event if ready_event is not None else None, None),
+          "dpn_swap_in")
+    return n
+
+
 def copy_d2d(dst, src, nbytes=None, dst_dev=0, src_dev=0, stream=None):
     n = nbytes if nbytes is not None else src.numel() * src.element_size()
     check(lib().dpn_p2p_copy(dst.data_ptr(), dst_dev, src.data_ptr(), src_dev, n, _s(stream)),

@@ -144,6 +144,28 @@ def host_bytes(plan, stages: int) -> List[int]:
             for x, m in enumerate(plan.memopt, start=1)]
 
 
+def plan_for_cap(model: TransformerConfig, g, stages: int, cap: int, bandwidth: int,
+                 margin: float = 0.0, b: int = 1):
+    """DawnPiper plan for a per-GPU byte cap: the planner gets the cap minus
+    what its memory model does not see (`stage_overhead`), re-planned with the
+    reserve of the plan's own stages until every stage's overhead is covered.
+    Raises InfeasibleModelError."""
+    reserve = optimizer_reserve(model, g, stages, b=b)
+    cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC,
+                       capacity=max(1, int((cap - reserve) * (1.0 - margin))), bandwidth=bandwidth)
+    for _ in range(4):
+        plan = P.plan(g, cfg)
+        need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b)
+        pcap = int((cap - need) * (1.0 - margin))
+        if pcap >= cfg.capacity:
+            break
+        if pcap <= 0:
+            raise P.InfeasibleModelError("stage overhead alone exceeds the cap")
+        cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=pcap,
+                           bandwidth=bandwidth)
+    return plan, cfg
+
+
 def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth: int,
               strategy: str, device: int = 0, times=None, run_gpu: bool = True,
               host_cap: int = 96 * GIB, margin: float = 0.0) -> dict:
@@ -161,24 +183,12 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
         rec.update(feasible=False, reason="optimizer state alone exceeds the cap")
         return rec
     if strategy == "dawnpiper":
-        # plan, then re-plan with the reserve of the plan's own stages until the
-        # capacity handed to the planner covers every stage's overhead
-        for _ in range(4):
-            try:
-                plan = P.plan(g, cfg)
-            except P.InfeasibleModelError as e:
-                rec.update(feasible=False, reason=f"planner: {e}")
-                return rec
-            need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b)
-            if int((cap - need) * (1.0 - margin)) >= cfg.capacity:
-                break
-            pcap = int((cap - need) * (1.0 - margin))
-            if pcap <= 0:
-                rec.update(feasible=False, reason="stage overhead alone exceeds the cap")
-                return rec
-            cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=pcap,
-                               bandwidth=bandwidth)
-            rec["planner_capacity"] = pcap
+        try:
+            plan, cfg = plan_for_cap(model, g, stages, cap, bandwidth, margin, b)
+        except P.InfeasibleModelError as e:
+            rec.update(feasible=False, reason=f"planner: {e}")
+            return rec
+        rec["planner_capacity"] = cfg.capacity
     elif strategy == "even_compute_memopt":
         # even-compute cuts + the same per-stage memopt policy (cli.py:276-300 "compute_balanced")
         cb = P.compute_balanced(g, 0, len(g) - 1, [1] * stages)

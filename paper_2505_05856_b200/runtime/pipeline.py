@@ -53,6 +53,19 @@ class RunConfig:
     # dependencies through events), so independent work of different stages
     # -- what separate GPUs would run in parallel -- can overlap on the device
     concurrent_stages: bool = True
+    # `run` only: after the timed steps, run every stage alone on its GPU with
+    # its real op list (runtime/memprobe.py) and report those measured device
+    # peaks as per_stage_peak (otherwise: the stage's static buffer bytes)
+    measure_stage_peaks: bool = False
+    # swap engine knobs for throughput runs (StageExecutor defaults hold
+    # memory to the planner's model: 256 MiB of D2H in flight, no early
+    # prefetch): offloads may queue up to d2h_budget bytes behind the forward
+    # and the next micro-batch's swap-ins start at the end of a backward, up
+    # to swap_prefetch bytes -- both held that much longer than the model
+    # assumes (tools/memopt_knobs.py: GPT-2 XL stage 1, b=16, 40 GiB cap:
+    # 80 -> 44 ms per micro-batch, peak +1.3 GB)
+    d2h_budget: int = 1 << 30
+    swap_prefetch: int = 2 << 30
 
     def __post_init__(self):
         if self.micro_batches < 1:
@@ -76,6 +89,7 @@ class RunReport:
     samples_per_s: float = 0.0
     step_time_us: float = 0.0
     device_peak_bytes: int = 0
+    per_stage_peak_source: str = "static"
 
     def to_doc(self) -> dict:
         return {
@@ -90,6 +104,7 @@ class RunReport:
             "samples_per_s": self.samples_per_s,
             "step_time_us": self.step_time_us,
             "device_peak_bytes": self.device_peak_bytes,
+            "per_stage_peak_source": self.per_stage_peak_source,
         }
 
 
@@ -181,6 +196,8 @@ class Pipeline:
                     micro_batch=cfg.micro_batch_size, memopt=plan.memopt[x - 1], init=init,
                     device=torch.device("cuda", d), stream=self.stage_streams[x - 1], opt=cfg.opt,
                     schedule=plan.schedule, micro_batches=self.m))
+                self.stages[-1].d2h_budget = cfg.d2h_budget
+                self.stages[-1].prefetch_budget = cfg.swap_prefetch
         self.order = sync_order(self.l, self.m) if self.sync else colocated_order(self.l, self.m)
         first_dev = self.stage_dev[0]
         self.loss = torch.zeros(self.m, dtype=torch.float32, device=torch.device("cuda", self.stage_dev[-1]))
@@ -464,7 +481,10 @@ def run(plan: PartitionPlan, g: ComputationGraph, cfg: RunConfig,
         model = PRESETS[base]
     pipe = Pipeline(model, g, plan, cfg)
     try:
-        return _run(pipe, model, cfg, ids, labels, steps)
+        rep = _run(pipe, model, cfg, ids, labels, steps)
+        if rep is not None and cfg.measure_stage_peaks:
+            rep = _with_measured_peaks(rep, pipe, model, g, plan, cfg)
+        return rep
     finally:
         if cfg.capacity is not None:  # the cap does not outlive the run
             for d in set(pipe.stage_dev):
@@ -490,3 +510,25 @@ def _run(pipe: Pipeline, model, cfg: RunConfig, ids, labels, steps: int) -> RunR
         wall = (time.perf_counter() - w0) * 1e6
         rep = pipe.report(events, t0, losses, wall) if cfg.trace else None
     return rep
+
+
+def _with_measured_peaks(rep: RunReport, pipe: Pipeline, model, g: ComputationGraph,
+                         plan: PartitionPlan, cfg: RunConfig) -> RunReport:
+    """per_stage_peak := each stage's measured device peak when it runs alone
+    on its GPU (its 1F1B op list, w + 1 micro-batches, memopt executed) --
+    what the planner's _async_peaks model (simulate.py:298-323) predicts for
+    the one-stage-per-GPU deployment; waste_ratio and capacity_exceeded follow."""
+    import dataclasses
+    from .memprobe import probe_stage
+    init = init_params(model, cfg.seed)
+    peaks = []
+    for x in range(1, pipe.l + 1):
+        r = probe_stage(model, g, plan, x, cfg.micro_batch_size, device=pipe.stage_dev[x - 1],
+                        micro_batches=pipe.l - x + 2, init=init)
+        peaks.append(r["peak_bytes"]["measured"])
+    top = max(peaks)
+    waste = sum(top - p for p in peaks) / (pipe.l * top) if top > 0 else 0.0
+    exceeded = tuple(x + 1 for x, p in enumerate(peaks) if cfg.capacity is not None and p > cfg.capacity)
+    return dataclasses.replace(rep, per_stage_peak=tuple(peaks), waste_ratio=waste,
+                               capacity_exceeded=exceeded,
+                               per_stage_peak_source="measured: each stage alone on its GPU")

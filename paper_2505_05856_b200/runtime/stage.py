@@ -169,7 +169,12 @@ class StageExecutor:
         self.id_offset = {"embed": 0, "dembed": self.M}
         self.device = device
         self.stream = stream
-        self.copy_stream = torch.cuda.Stream(device=device)
+        # swap engine: one copy stream per direction, so a micro-batch's D2H
+        # offloads and an earlier micro-batch's H2D prefetches use both
+        # directions of the host link at once (1F1B interleaves them)
+        self.copy_stream = torch.cuda.Stream(device=device)      # D2H
+        self.h2d_stream = torch.cuda.Stream(device=device)       # H2D
+        self.d2h_done: Dict[Tuple[str, int], torch.cuda.Event] = {}
         self.opt = opt
         if schedule not in (SCHEDULE_ASYNC, SCHEDULE_SYNC):
             raise ValueError(f"unknown schedule {schedule!r}")
@@ -336,10 +341,21 @@ class StageExecutor:
                 self.bwd_last[t] = min(self.bwd_last.get(t, pos[n.id]), pos[n.id])
                 self.bwd_first[t] = max(self.bwd_first.get(t, pos[n.id]), pos[n.id])
         self.swap_lookahead = 2
+        # early prefetch: at the end of micro-batch mb's backward, H2D of up to
+        # this many bytes of mb+1's swapped tensors starts, so it overlaps the
+        # next forward's D2H offloads (1F1B runs F(mb+w) between B(mb) and
+        # B(mb+1)); the bytes are held that much earlier than just-in-time
+        self.prefetch_budget = 0
+        self.prefetched: Dict[str, Tuple[torch.Tensor, torch.cuda.Event]] = {}
         self._recv_mb = 0  # micro-batch whose boundary inputs are being delivered
         # profiler hook: when a list, every node forward / backward is bracketed
         # with CUDA events on the compute stream -> (node id, "fwd"|"bwd", e0, e1)
         self.node_timer: Optional[list] = None
+        # memory-plan instrumentation: when a dict of lists, the swap engine and
+        # recompute replay record timing events -- "d2h" / "h2d": (bytes, start,
+        # end) on the copy stream; "stall": compute-stream waits on a swap-in;
+        # "recompute": replayed producer chains (runtime/memprobe.py)
+        self.memstats: Optional[Dict[str, list]] = None
 
     # ---- helpers -------------------------------------------------------------------
 
@@ -496,36 +512,62 @@ class StageExecutor:
         return outs
 
     def _swap_out(self, tid: str, slot: int) -> None:
-        """D2H of an evicted tensor on the copy stream (swap engine, memopt swap)."""
+        """D2H of an evicted tensor on the copy stream (swap engine, memopt swap),
+        through the C-ABI's dpn_swap_out: the copy stream waits on an event of
+        the compute stream, so the copy reads the finished tensor."""
         ev = torch.cuda.Event()
         ev.record(self.stream)
         cs = self.copy_stream
-        cs.wait_event(ev)
         src = self.live[tid]
-        with torch.cuda.stream(cs):
-            self.host[tid][slot].copy_(src, non_blocking=True)
+        t0 = self._stat_event(cs, ev)
+        nbytes = K.swap_out(self.host[tid][slot], src, cs, ready_event=ev)
         src.record_stream(cs)  # memory is recycled only after the D2H completes
-        done = torch.cuda.Event()
+        done = torch.cuda.Event(enable_timing=self.memstats is not None)
         done.record(cs)
-        self.d2h_pending.append((done, src.numel() * src.element_size()))
+        if self.memstats is not None:
+            self.memstats["d2h"].append((nbytes, t0, done))
+        self.d2h_pending.append((done, nbytes))
+        self.d2h_done[(tid, slot)] = done  # the H2D of this slot reads after it
+
+    def _stat_event(self, stream, after=None):
+        """A timing event on `stream` (after `after`) when memstats is on."""
+        if self.memstats is None:
+            return None
+        if after is not None:
+            stream.wait_event(after)
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
 
     def _d2h_backpressure(self) -> None:
         while self.d2h_pending and sum(b for _, b in self.d2h_pending) > self.d2h_budget:
             ev, _ = self.d2h_pending.pop(0)
             self.stream.wait_event(ev)
 
-    def _swap_in(self, tid: str, slot: int) -> None:
-        """H2D prefetch of a swapped tensor into a fresh device buffer."""
-        dst = self._alloc_live(tid)
+    def _swap_in(self, tid: str, slot: int, early: bool = False) -> None:
+        """H2D prefetch of a swapped tensor into a fresh device buffer (early:
+        held in `prefetched` until its micro-batch's backward starts)."""
+        if early:
+            shape, dt = self._spec(tid)
+            dst = torch.empty(shape, dtype=dt, device=self.device)
+        else:
+            dst = self._alloc_live(tid)
         ev = torch.cuda.Event()
         ev.record(self.stream)  # the buffer's memory is free in compute-stream order
-        cs = self.copy_stream
-        cs.wait_event(ev)
-        with torch.cuda.stream(cs):
-            dst.copy_(self.host[tid][slot], non_blocking=True)
-        done = torch.cuda.Event()
+        cs = self.h2d_stream
+        written = self.d2h_done.pop((tid, slot), None)
+        if written is not None:  # the host slot holds this micro-batch's copy
+            cs.wait_event(written)
+        t0 = self._stat_event(cs, ev)
+        nbytes = K.swap_in(dst, self.host[tid][slot], cs, ready_event=ev)
+        done = torch.cuda.Event(enable_timing=self.memstats is not None)
         done.record(cs)
-        self.swap_in_done[tid] = done
+        if self.memstats is not None:
+            self.memstats["h2d"].append((nbytes, t0, done))
+        if early:
+            self.prefetched[tid] = (dst, done)
+        else:
+            self.swap_in_done[tid] = done
 
     def _node_fwd(self, n: NodeDef, slot: int, ver: int, phase: str,
                   loss_out: Optional[torch.Tensor] = None) -> None:
@@ -833,6 +875,12 @@ class StageExecutor:
             # `swap_lookahead` tensors ahead of the node that needs them
             queue = sorted(self.swap_ids, key=lambda t: (-self.bwd_first.get(t, -1), t))
             issued: Set[str] = set()
+            for t, (buf, done) in self.prefetched.items():  # started by the last backward
+                self.live[t] = buf
+                self.swap_in_done[t] = done
+                issued.add(t)
+                queue.remove(t)
+            self.prefetched = {}
 
             def issue_next() -> None:
                 t = queue.pop(0)
@@ -856,13 +904,19 @@ class StageExecutor:
                                 raise RuntimeError(f"stage {self.stage}: swap-in of {t} never issued")
                             issue_next()
                         if t in self.swap_in_done:
+                            s0 = self._stat_event(st)
                             st.wait_event(self.swap_in_done.pop(t))
+                            if s0 is not None:  # compute-stream time spent waiting on the H2D
+                                self.memstats["stall"].append((s0, self._stat_event(st)))
                     elif t not in self.live:  # recompute: replay its producer chain now
+                        r0 = self._stat_event(st)
                         self._alloc_live(t)
                         for i in self.chains[t]:
                             self._node_fwd_replay(self.all_nodes[i], slot, ver)
                         for e in [e for e in self.live if e in self.ephemeral]:
                             del self.live[e]  # chain intermediates
+                        if r0 is not None:
+                            self.memstats["recompute"].append((r0, self._stat_event(st)))
                 if self.node_timer is not None:
                     e0 = torch.cuda.Event(enable_timing=True)
                     e0.record(st)
@@ -879,7 +933,26 @@ class StageExecutor:
                 self.grads.pop(out_tid(n.id), None)
                 prefetch(self.swap_lookahead)
             out = {t: self.grads[t] for t in self.recv_ids if t in self.grads}
+            self._prefetch_next(mb)
         return out
+
+    def _prefetch_next(self, mb: int) -> None:
+        """Start the H2D of micro-batch mb+1's first swapped tensors (up to
+        prefetch_budget bytes) if its forward has run (1F1B: it has, whenever
+        mb+1 <= mb + w - 1)."""
+        if not self.prefetch_budget or self.sync or not self.swap_ids:
+            return
+        nxt = mb + 1
+        slot = self.slot_of(nxt)
+        if self.slot_mb[slot] != nxt:
+            return
+        budget = self.prefetch_budget
+        for t in sorted(self.swap_ids, key=lambda t: (-self.bwd_first.get(t, -1), t)):
+            size = self.host[t][slot].numel() * self.host[t][slot].element_size()
+            if size > budget:
+                break
+            self._swap_in(t, slot, early=True)
+            budget -= size
 
     def finish_backward(self, mb: int) -> None:
         """Optimizer step after micro-batch mb's backward (PipeDream per-micro-batch
