@@ -471,6 +471,12 @@ class StageExecutor:
             return self._alloc_live(tid)
         return self.buf(tid, self.slot_of(mb), "fwd")
 
+    def recv_like(self, tid: str) -> torch.Tensor:
+        """A fresh device buffer shaped like boundary input tid (an early-posted
+        receive lands in it; `adopt_recv` then takes it over)."""
+        shape, dt = self._spec(tid)
+        return torch.empty(shape, dtype=dt, device=self.device)
+
     def adopt_recv(self, tid: str, mb: int, msg: torch.Tensor) -> None:
         """Zero-copy receive (co-located stages): the message buffer becomes this
         stage's buffer of tid for micro-batch mb.  The sender hands over a

@@ -74,6 +74,24 @@ class FakeStage:
         self.synced.append(self.wgrad[0].item())
 
 
+class OverlappedFakeStage(FakeStage):
+    """FakeStage with the executor's zero-copy receive / send hooks, so the
+    scheduler takes its overlapped protocol (early-posted receives adopted by
+    the stage, sends from released buffers)."""
+
+    def recv_like(self, tid):
+        return torch.zeros(4)
+
+    def adopt_recv(self, tid, j, t):
+        self.inbox[j] = t
+
+    def release_send_buffer(self, tid, j):
+        return self.outbox.pop(j)
+
+    def slot_of(self, j):
+        return (j - 1) % (self.world - self.x + 1)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -82,7 +100,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, m, q, schedule="async_1f1b", stages=None):
+def _worker(rank, world, port, m, q, schedule="async_1f1b", stages=None, overlapped=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -90,7 +108,7 @@ def _worker(rank, world, port, m, q, schedule="async_1f1b", stages=None):
     from paper_2505_05856_b200.planner.schedule import async_ops, sync_ops
     chans = BoundaryChannels(world, stages)
     l = chans.stages
-    st = FakeStage(rank, world, stages)
+    st = (OverlappedFakeStage if overlapped else FakeStage)(rank, world, stages)
     st.sync = schedule == "sync"
     # replica k's ids are offset by 1000 k: a message crossing replicas shows up
     ids = (torch.arange(m * 4, dtype=torch.int32).reshape(m, 4) + 1000 * st.replica
@@ -113,13 +131,16 @@ def _worker(rank, world, port, m, q, schedule="async_1f1b", stages=None):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m,schedule", [(2, 5, "async_1f1b"), (3, 7, "async_1f1b"),
-                                               (2, 4, "sync"), (3, 5, "sync")])
-def test_gloo_pipeline_order_and_matching(world, m, schedule):
+@pytest.mark.parametrize("world,m,schedule,overlapped",
+                         [(2, 5, "async_1f1b", False), (3, 7, "async_1f1b", False),
+                          (2, 4, "sync", False), (3, 5, "sync", False),
+                          (3, 7, "async_1f1b", True), (3, 5, "sync", True)])
+def test_gloo_pipeline_order_and_matching(world, m, schedule, overlapped):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, m, q, schedule)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, q, schedule, None, overlapped))
+             for r in range(world)]
     for p in procs:
         p.start()
     out = {}
