@@ -113,6 +113,13 @@ int dpn_layernorm_bwd(const void* dy, const void* x, const void* gamma, const fl
                       const float* rstd, void* dx, const void* dx_add, float* dgamma, float* dbeta,
                       int64_t rows, int64_t cols, float* workspace, int64_t workspace_floats,
                       void* stream);
+/* LayerNorm backward in one pass: dx (+= dx_add when given), dgamma += sum dy * xhat,
+ * dbeta += sum dy and, when dbias is given, dbias += column sums of the final dx (the
+ * bias gradient of the linear node whose output gradient dx is).  Replaces the
+ * ln_dx + column-reduction pair of dpn_layernorm_bwd for the fused executor path. */
+int dpn_layernorm_bwd_fused(const void* dy, const void* x, const void* gamma, const float* mean,
+                            const float* rstd, void* dx, const void* dx_add, float* dgamma,
+                            float* dbeta, float* dbias, int64_t rows, int64_t cols, void* stream);
 /* score: P = softmax(alpha * S) per row; causal masks key > (row % q_len). */
 int dpn_softmax_fwd(const void* s, void* p, int64_t rows, int64_t cols, int64_t q_len, float alpha,
                     int causal, void* stream);

@@ -55,6 +55,7 @@ SIGNATURES = {
                            _f32, _vp],
     "dpn_layernorm_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp],
     "dpn_layernorm_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp],
+    "dpn_layernorm_bwd_fused": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _vp],
     "dpn_softmax_fwd": [_vp, _vp, _i64, _i64, _i64, _f32, C.c_int, _vp],
     "dpn_softmax_bwd": [_vp, _vp, _vp, _i64, _i64, _f32, _vp],
     "dpn_gelu_fwd": [_vp, _vp, _i64, _vp],

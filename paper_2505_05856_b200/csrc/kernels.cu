@@ -185,6 +185,151 @@ __device__ __forceinline__ void red_add_v4(float* addr, const float* v) {
                : "memory");
 }
 
+// Fused LayerNorm backward: dx (+ dx_add), dgamma, dbeta and, optionally, the
+// column sum of the final dx (the bias gradient of the linear node whose
+// output gradient this is) in ONE pass over dy / x / dx_add.
+//
+// Layout: a row is owned by a group of G = ceil(cols / 256) warps, one 16-byte
+// column chunk (8 columns) per lane, so every thread keeps the SAME 8 columns
+// for every row its CTA visits: the three column accumulators cost 24
+// registers (a warp-per-row kernel needs 32 * 3 * cols / 256 of them, which is
+// what capped the earlier fused attempt at 16 warps per SM).  Row statistics
+// (sum dy*gamma, sum dy*gamma*xhat) combine the group's warps through shared
+// memory behind a per-group named barrier; kLnRows rows per group are in
+// flight per iteration.  The CTA's column partials combine across groups in
+// shared memory and go out with one vector red per 4 columns.
+//   bytes: read dy, x (, dx_add), write dx  (+ 8 B of stats per row)
+constexpr int kLnThreads = 512;
+constexpr int kLnRows = 3;
+__global__ void __launch_bounds__(kLnThreads, 1) ln_bwd_fused_kernel(
+    const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+    const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
+    const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
+    long long rows, int cols, long long rows_per_cta, float* __restrict__ dgamma,
+    float* __restrict__ dbeta, float* __restrict__ dbias) {
+  pdl_wait();
+  extern __shared__ float ln_smem[];
+  const int nvec = cols >> 3;
+  const int G = (nvec + 31) >> 5;              // warps per row group
+  const int groups = (kLnThreads >> 5) / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = warp / G, wi = warp % G;
+  const int chunk = wi * 32 + lane;
+  const bool in_grp = grp < groups;
+  const bool col = in_grp && chunk < nvec;
+  float* stat = ln_smem;                       // [2 parity][16 warps][kLnRows][2]
+  float* part = ln_smem + 2 * 16 * kLnRows * 2; // [groups][cols]
+  float gm[8], ag[8], ab[8], ad[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ag[i] = ab[i] = ad[i] = 0.f;
+  if (col) load8(gamma + chunk * 8, gm);
+  const float inv_cols = 1.f / (float)cols;
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  int parity = 0;
+  if (in_grp) {
+    for (long long base = r0 + (long long)grp * kLnRows; base < r1;
+         base += (long long)groups * kLnRows, parity ^= 1) {
+      uint4 xr[kLnRows], dr[kLnRows], ar[kLnRows];
+      float mu[kLnRows], rs[kLnRows];
+#pragma unroll
+      for (int u = 0; u < kLnRows; ++u) {
+        const long long r = base + u;
+        const bool ok = col && r < r1;
+        xr[u] = ok ? *reinterpret_cast<const uint4*>(x + r * cols + chunk * 8) : make_uint4(0, 0, 0, 0);
+        dr[u] = ok ? *reinterpret_cast<const uint4*>(dy + r * cols + chunk * 8) : make_uint4(0, 0, 0, 0);
+        ar[u] = ok && dx_add ? *reinterpret_cast<const uint4*>(dx_add + r * cols + chunk * 8)
+                             : make_uint4(0, 0, 0, 0);
+        mu[u] = r < r1 ? mean[r] : 0.f;
+        rs[u] = r < r1 ? rstd[r] : 0.f;
+      }
+      float* st = stat + parity * 16 * kLnRows * 2;
+#pragma unroll
+      for (int u = 0; u < kLnRows; ++u) {
+        float xv[8], dv[8], s1 = 0.f, s2 = 0.f;
+        load8(reinterpret_cast<const __nv_bfloat16*>(&xr[u]), xv);
+        load8(reinterpret_cast<const __nv_bfloat16*>(&dr[u]), dv);
+        if (col) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float g = dv[i] * gm[i];
+            s1 += g;
+            s2 += g * (xv[i] - mu[u]) * rs[u];
+          }
+        }
+        s1 = warp_sum(s1);
+        s2 = warp_sum(s2);
+        if (lane == 0) {
+          st[(warp * kLnRows + u) * 2] = s1;
+          st[(warp * kLnRows + u) * 2 + 1] = s2;
+        }
+      }
+      // the group's G warps (parity double-buffers `stat`, so one barrier per
+      // iteration orders both the writes and the next iteration's reuse)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(G * 32) : "memory");
+#pragma unroll
+      for (int u = 0; u < kLnRows; ++u) {
+        const long long r = base + u;
+        float s1 = 0.f, s2 = 0.f;
+        for (int w = 0; w < G; ++w) {
+          s1 += st[((grp * G + w) * kLnRows + u) * 2];
+          s2 += st[((grp * G + w) * kLnRows + u) * 2 + 1];
+        }
+        s1 *= inv_cols;
+        s2 *= inv_cols;
+        if (!col || r >= r1) continue;
+        float xv[8], dv[8], o[8];
+        load8(reinterpret_cast<const __nv_bfloat16*>(&xr[u]), xv);
+        load8(reinterpret_cast<const __nv_bfloat16*>(&dr[u]), dv);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float xh = (xv[i] - mu[u]) * rs[u];
+          ab[i] += dv[i];
+          ag[i] += dv[i] * xh;
+          o[i] = rs[u] * (dv[i] * gm[i] - s1 - xh * s2);
+        }
+        if (dx_add) {
+          float a[8];
+          load8(reinterpret_cast<const __nv_bfloat16*>(&ar[u]), a);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[i] += a[i];
+        }
+        uint4 packed;
+        packed.x = pack_bf16(o[0], o[1]);
+        packed.y = pack_bf16(o[2], o[3]);
+        packed.z = pack_bf16(o[4], o[5]);
+        packed.w = pack_bf16(o[6], o[7]);
+        *reinterpret_cast<uint4*>(dx + r * cols + chunk * 8) = packed;
+        if (dbias) {  // the bias gradient sums the stored (bf16) dx, as a colsum pass would
+          float q[8];
+          load8(reinterpret_cast<const __nv_bfloat16*>(&packed), q);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) ad[i] += q[i];
+        }
+      }
+    }
+  }
+  // column partials: combine the groups in shared memory, one red per 4 columns
+  auto flush = [&](float* out, const float(&acc)[8]) {
+    __syncthreads();
+    if (col) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) part[grp * cols + chunk * 8 + i] = acc[i];
+    }
+    __syncthreads();
+    for (int c4 = threadIdx.x; c4 < (cols >> 2); c4 += kLnThreads) {
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int g = 0; g < groups; ++g)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] += part[g * cols + c4 * 4 + i];
+      red_add_v4(out + c4 * 4, v);
+    }
+  };
+  flush(dgamma, ag);
+  flush(dbeta, ab);
+  if (dbias) flush(dbias, ad);
+}
+
 // Column reductions over a row-major [rows, cols] bf16 matrix (bias and
 // LayerNorm parameter gradients).  CTA (band, group) owns 8*cw columns and a
 // band of rows; its 512 threads are cw column chunks x L row lanes, each lane
@@ -676,6 +821,36 @@ extern "C" int dpn_layernorm_fwd(const void* x, const void* gamma, const void* b
   LN_DISPATCH(ln_fwd_kernel, grid_for(rows, 8), 0, (const __nv_bfloat16*)x,
               (const __nv_bfloat16*)gamma, (const __nv_bfloat16*)beta, (__nv_bfloat16*)y, mean, rstd,
               rows, (int)cols, eps);
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int dpn_layernorm_bwd_fused(const void* dy, const void* x, const void* gamma,
+                                       const float* mean, const float* rstd, void* dx,
+                                       const void* dx_add, float* dgamma, float* dbeta,
+                                       float* dbias, int64_t rows, int64_t cols, void* stream) {
+  DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * 16, "cols must be a multiple of 8, <= 4096");
+  DPN_REQUIRE(dgamma && dbeta, "the fused LayerNorm backward produces dgamma and dbeta");
+  if (rows == 0) return 0;
+  const int nvec = (int)(cols / 8);
+  const int G = (nvec + 31) / 32;
+  const int groups = (kLnThreads / 32) / G;
+  // one CTA per SM (persistent over a band of rows), at least kLnRows * groups rows each
+  const long long per_iter = (long long)groups * kLnRows;
+  long long per = (rows + 147) / 148;
+  per = std::max<long long>(per_iter, (per + per_iter - 1) / per_iter * per_iter);
+  const unsigned grid = (unsigned)((rows + per - 1) / per);
+  const size_t smem = (2 * 16 * kLnRows * 2 + (size_t)groups * cols) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_fused_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  DPN_CHECK_CUDA(launch_pdl(ln_bwd_fused_kernel, dim3(grid), kLnThreads, smem, (cudaStream_t)stream,
+                            (const __nv_bfloat16*)dy, (const __nv_bfloat16*)x,
+                            (const __nv_bfloat16*)gamma, mean, rstd, (__nv_bfloat16*)dx,
+                            (const __nv_bfloat16*)dx_add, rows, (int)cols, per, dgamma, dbeta, dbias));
   DPN_LAUNCH_CHECK();
   return 0;
 }

@@ -222,6 +222,18 @@ def layernorm_bwd(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, stre
           "dpn_layernorm_bwd")
 
 
+def layernorm_bwd_fused(dy, x, gamma, mean, rstd, dx, dgamma, dbeta, dx_add=None, dbias=None,
+                        stream=None):
+    """One-pass LayerNorm backward (dx, dgamma, dbeta and optionally the next
+    linear's bias gradient = column sums of the final dx)."""
+    rows, cols = x.shape
+    INSTR.launches += 1
+    check(lib().dpn_layernorm_bwd_fused(dy.data_ptr(), x.data_ptr(), gamma.data_ptr(),
+                                        mean.data_ptr(), rstd.data_ptr(), dx.data_ptr(), _p(dx_add),
+                                        dgamma.data_ptr(), dbeta.data_ptr(), _p(dbias), rows, cols,
+                                        _s(stream)), "dpn_layernorm_bwd_fused")
+
+
 def softmax_fwd(s, p, q_len, alpha, causal, stream=None):
     cols = s.shape[-1]
     rows = s.numel() // cols

@@ -52,24 +52,81 @@ class StageCheck:
     error: str = ""
 
 
-def stage_overhead(model: TransformerConfig, g, lo: int, hi: int, b: int) -> int:
-    """Device bytes of a stage the planner's model (w x (micro_peak - saved),
-    memopt.py:156-158) does not see: fp32 master / Adam m / Adam v / grad
-    (16 B per parameter; the bf16 versions are the model's m_p), backward
-    gradient buffers (~2 of the stage's largest activation), the D2H
-    back-pressure window and workspace / allocator slack.  Calibrated against
-    measured per-stage peaks (tools/max_batch.py, profiles/r01_maxbatch_*)."""
-    params = g.segment_params(lo, hi) // 2  # m_p = 2 B / param (one bf16 version)
-    largest = max(g.nodes[k].m_a for k in range(lo, hi + 1))
-    return 16 * params + 2 * largest + 3 * GIB // 2
+@dataclass(frozen=True)
+class Overhead:
+    """Device bytes of a stage the planner's memory model (w x (micro_peak -
+    saved), memopt.py:156-158) does not see, as a linear function of the
+    stage: per_param x (bytes of one bf16 weight version, the profile's m_p)
+    + per_act x (the stage's largest activation) + const.  What it stands for:
+    fp32 master / Adam m / Adam v / grad (8 bytes per m_p byte), backward
+    gradient buffers, the D2H back-pressure window, workspaces and allocator
+    slack."""
+
+    per_param: float = 8.0
+    per_act: float = 2.0
+    const: int = 3 * GIB // 2
+    source: str = "hand-calibrated (round 1: 16 B/param + 2 x largest activation + 1.5 GiB)"
+
+    def to_doc(self) -> dict:
+        return {"per_param": self.per_param, "per_act": self.per_act, "const": self.const,
+                "source": self.source}
 
 
-def optimizer_reserve(model: TransformerConfig, g, stages: int, cuts=None, b: int = 1) -> int:
+DEFAULT_OVERHEAD = Overhead()
+
+
+def _stage_features(g, lo: int, hi: int) -> Tuple[int, int]:
+    return g.segment_params(lo, hi), max(g.nodes[k].m_a for k in range(lo, hi + 1))
+
+
+def stage_overhead(model: TransformerConfig, g, lo: int, hi: int, b: int,
+                   overhead: Overhead = DEFAULT_OVERHEAD) -> int:
+    params, largest = _stage_features(g, lo, hi)
+    return int(overhead.per_param * params + overhead.per_act * largest + overhead.const)
+
+
+def optimizer_reserve(model: TransformerConfig, g, stages: int, cuts=None, b: int = 1,
+                      overhead: Overhead = DEFAULT_OVERHEAD) -> int:
     """Max stage_overhead over the stages of `cuts` (default: compute-balanced)."""
     if cuts is None:
         cuts = P.compute_balanced(g, 0, len(g) - 1, [1] * stages).positions
     bounds = P.stage_bounds(P.Cut(tuple(cuts)), len(g))
-    return max(stage_overhead(model, g, lo, hi, b) for lo, hi in bounds)
+    return max(stage_overhead(model, g, lo, hi, b, overhead) for lo, hi in bounds)
+
+
+def calibrate_overhead(model: TransformerConfig, stages: int, device: int = 0,
+                       sizes: Tuple[int, ...] = (1, 2), times=None) -> Tuple[Overhead, List[dict]]:
+    """Fit `Overhead` to measured stage peaks: every stage of the
+    compute-balanced split (no memopt) runs alone on the GPU at each micro-batch
+    size in `sizes` (runtime/memprobe.py); the unmodelled bytes (measured peak
+    - the planner's sched_peak) are least-squares fitted on (m_p bytes,
+    largest activation, 1), and the constant is raised by the largest
+    under-prediction so the fit bounds every measurement from above."""
+    import numpy as np
+    from .memprobe import probe_stage
+    rows, ys, pts = [], [], []
+    init = init_params(model, 0)
+    for b in sizes:
+        g = profile_graph(model, b, times=times)
+        ample = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=1 << 62,
+                             bandwidth=1 << 40)
+        plan = P.plan_from_cuts(g, ample, P.compute_balanced(g, 0, len(g) - 1, [1] * stages).positions)
+        for x, (lo, hi) in enumerate(P.stage_bounds(plan.cuts, len(g)), start=1):
+            r = probe_stage(model, g, plan, x, b, device=device, micro_batches=stages - x + 2, init=init)
+            extra = r["peak_bytes"]["measured"] - plan.stages[x - 1].sched_peak
+            params, largest = _stage_features(g, lo, hi)
+            rows.append([params, largest, 1.0])
+            ys.append(extra)
+            pts.append({"b": b, "stage": x, "measured_peak": r["peak_bytes"]["measured"],
+                        "sched_peak": plan.stages[x - 1].sched_peak, "unmodelled": extra})
+    A, y = np.array(rows, dtype=np.float64), np.array(ys, dtype=np.float64)
+    coef, *_ = np.linalg.lstsq(A, y, rcond=None)
+    per_param, per_act = max(0.0, float(coef[0])), max(0.0, float(coef[1]))
+    const = y - (per_param * A[:, 0] + per_act * A[:, 1])
+    oh = Overhead(per_param=round(per_param, 3), per_act=round(per_act, 3), const=int(const.max()),
+                  source=f"measured: {len(ys)} stage peaks at b in {list(sizes)}, least squares, "
+                         f"constant raised to bound every point")
+    return oh, pts
 
 
 def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, device: int = 0,
@@ -145,17 +202,17 @@ def host_bytes(plan, stages: int) -> List[int]:
 
 
 def plan_for_cap(model: TransformerConfig, g, stages: int, cap: int, bandwidth: int,
-                 margin: float = 0.0, b: int = 1):
+                 margin: float = 0.0, b: int = 1, overhead: Overhead = DEFAULT_OVERHEAD):
     """DawnPiper plan for a per-GPU byte cap: the planner gets the cap minus
     what its memory model does not see (`stage_overhead`), re-planned with the
     reserve of the plan's own stages until every stage's overhead is covered.
     Raises InfeasibleModelError."""
-    reserve = optimizer_reserve(model, g, stages, b=b)
+    reserve = optimizer_reserve(model, g, stages, b=b, overhead=overhead)
     cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC,
                        capacity=max(1, int((cap - reserve) * (1.0 - margin))), bandwidth=bandwidth)
     for _ in range(4):
         plan = P.plan(g, cfg)
-        need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b)
+        need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b, overhead=overhead)
         pcap = int((cap - need) * (1.0 - margin))
         if pcap >= cfg.capacity:
             break
@@ -168,11 +225,12 @@ def plan_for_cap(model: TransformerConfig, g, stages: int, cap: int, bandwidth: 
 
 def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth: int,
               strategy: str, device: int = 0, times=None, run_gpu: bool = True,
-              host_cap: int = 96 * GIB, margin: float = 0.0) -> dict:
+              host_cap: int = 96 * GIB, margin: float = 0.0,
+              overhead: Overhead = DEFAULT_OVERHEAD, timing: bool = False) -> dict:
     """One trial; `margin` shrinks the capacity handed to the planner by that
     fraction (the measured-memory feedback of `max_batch`)."""
     g = profile_graph(model, b, times=times)
-    reserve = optimizer_reserve(model, g, stages, b=b)
+    reserve = optimizer_reserve(model, g, stages, b=b, overhead=overhead)
     pcap = int((cap - reserve) * (1.0 - margin))
     rec = {"b": b, "strategy": strategy, "planner_capacity": pcap, "reserve": reserve}
     if margin:
@@ -184,7 +242,7 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
         return rec
     if strategy == "dawnpiper":
         try:
-            plan, cfg = plan_for_cap(model, g, stages, cap, bandwidth, margin, b)
+            plan, cfg = plan_for_cap(model, g, stages, cap, bandwidth, margin, b, overhead)
         except P.InfeasibleModelError as e:
             rec.update(feasible=False, reason=f"planner: {e}")
             return rec
@@ -224,6 +282,8 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
         rec["feasible"] = True
         return rec
     init = init_params(model, 0)
+    if timing:
+        return _timed_stages(rec, model, g, plan, b, cap, device, init)
     checks = [check_stage(model, g, plan, x, b, cap, device, init=init) for x in range(1, stages + 1)]
     rec["stage_peak_gib"] = [round(c.peak_bytes / GIB, 2) for c in checks]
     bad = [c for c in checks if not c.ok]
@@ -233,9 +293,38 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
     return rec
 
 
+def _timed_stages(rec: dict, model, g, plan, b: int, cap: int, device: int, init) -> dict:
+    """Every stage alone on the GPU under the cap with timing (memprobe), and
+    the 1F1B steady-state throughput those stage times give on l GPUs: one
+    micro-batch per bottleneck-stage period (forward + backward + the
+    per-micro-batch AdamW of the slowest stage; boundary transfers over
+    NVLink are overlapped and not charged)."""
+    from .memprobe import probe_stage
+    per = []
+    for x in range(1, len(plan.stages) + 1):
+        try:
+            r = probe_stage(model, g, plan, x, b, cap=cap, device=device, init=init)
+        except torch.OutOfMemoryError as e:
+            rec.update(feasible=False, reason=f"stage {x} OOM on GPU: {str(e).splitlines()[0][:160]}")
+            return rec
+        per.append({"stage": x, "fwd_us": r["fwd_us"]["measured"], "bwd_us": r["bwd_us"]["measured"],
+                    "opt_us": r["optimizer_us"], "model_us": r["fwd_us"]["model"] + r["bwd_us"]["model"],
+                    "stall_us": r["added_time_us"]["measured_stall_per_mb"],
+                    "recompute_us": r["added_time_us"]["measured_recompute_per_mb"],
+                    "peak_gib": round(r["peak_bytes"]["measured"] / GIB, 2)})
+    period = max(p["fwd_us"] + p["bwd_us"] + p["opt_us"] for p in per)
+    model_period = max(p["model_us"] for p in per)
+    rec.update(feasible=True, stage_times=per, bottleneck_us=round(period, 1),
+               samples_per_s_l_gpus=round(b * 1e6 / period, 1),
+               samples_per_s_l_gpus_model=round(b * 1e6 / model_period, 1),
+               stage_peak_gib=[p["peak_gib"] for p in per])
+    return rec
+
+
 def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, strategy: str,
               b_max: int = 64, device: int = 0, log=None, host_cap: int = 96 * GIB,
-              run_gpu: bool = True, margins: Tuple[float, ...] = (0.1, 0.2)) -> Tuple[int, List[dict]]:
+              run_gpu: bool = True, margins: Tuple[float, ...] = (0.1, 0.2),
+              overhead: Overhead = DEFAULT_OVERHEAD) -> Tuple[int, List[dict]]:
     """Largest feasible b (0 if none) by doubling then bisection.
 
     Measured-memory feedback for the planned strategies: the planner's memory
@@ -248,7 +337,7 @@ def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, s
     def ok(b: int) -> bool:
         for margin in (0.0,) + (tuple(margins) if strategy != "even_compute" else ()):
             r = try_batch(model, b, stages, cap, bandwidth, strategy, device, host_cap=host_cap,
-                          run_gpu=run_gpu, margin=margin)
+                          run_gpu=run_gpu, margin=margin, overhead=overhead)
             hist.append(r)
             if log:
                 log(r)

@@ -307,6 +307,31 @@ class StageExecutor:
                 if len(users) == 1 and users[0].kind == "linear":
                     self.bwd_gelu_of[users[0].id] = n.id
         self._skip_bwd: Set[str] = set()
+        # bias gradient of a linear node folded into the one-pass LayerNorm
+        # backward of the LN reading that node's output (or, through the
+        # residual `add`, fc2's): the LN's final dx IS the linear's output
+        # gradient when the LN is the lowest-index in-stage consumer (every
+        # other contribution has landed), so its column sums are the bias
+        # gradient and the separate colsum pass over dy is skipped
+        self.ln_bias_of: Dict[str, str] = {}
+        self._bias_done: Set[str] = set()
+        spos = {n.id: i for i, n in enumerate(self.nodes)}
+        for n in self.nodes:
+            if n.kind != "ln" or n.inputs[0] not in in_stage:
+                continue
+            u = self.node_by_id[n.inputs[0]]
+            lin = u
+            if u.kind == "add" and u.inputs[0] in in_stage:
+                lin = self.node_by_id[u.inputs[0]]
+                if lin.kind != "linear":
+                    continue
+            elif u.kind not in ("linear", "linear_res"):
+                continue
+            if not any(pn == "bias" for pn, _ in lin.params):
+                continue
+            first = min(spos[c.id] for c in self.nodes if u.id in c.inputs)
+            if first == spos[n.id]:
+                self.ln_bias_of[n.id] = lin.id
         # residual add fused into fc2's epilogue when both live in this stage:
         # fc2's forward writes z + y straight into the add node's output
         # (fc2's own output z is never materialised: nothing reads it later)
@@ -975,6 +1000,7 @@ class StageExecutor:
         self.grads = {}
         self.grad_init = set()
         self._skip_bwd = set()
+        self._bias_done = set()
         self.shared_grads = set()
 
     def dp_grads(self) -> List[torch.Tensor]:
@@ -1031,15 +1057,19 @@ class StageExecutor:
             x_t = out_tid(n.inputs[0])
             x = self.buf(x_t, slot, "bwd")
             stats = self.buf(stats_tid(n.id), slot, "bwd")
+            lin = self.ln_bias_of.get(n.id)
+            dbias = P.gradv(f"{lin}.bias") if lin is not None else None
             if x_t in self.grad_init:
                 dx = self.grads[x_t]
-                K.layernorm_bwd(dy, x, W("gamma"), stats[0], stats[1], dx, G("gamma"), G("beta"),
-                                dx_add=dx, stream=st)
+                K.layernorm_bwd_fused(dy, x, W("gamma"), stats[0], stats[1], dx, G("gamma"),
+                                      G("beta"), dx_add=dx, dbias=dbias, stream=st)
             else:
                 dx = self.grad_buffer(x_t)
-                K.layernorm_bwd(dy, x, W("gamma"), stats[0], stats[1], dx, G("gamma"), G("beta"),
-                                stream=st)
+                K.layernorm_bwd_fused(dy, x, W("gamma"), stats[0], stats[1], dx, G("gamma"),
+                                      G("beta"), dbias=dbias, stream=st)
                 self.grad_init.add(x_t)
+            if lin is not None:
+                self._bias_done.add(lin)
         elif k in ("linear", "linear_res"):
             x_t = out_tid(n.inputs[0])
             x = self.buf(x_t, slot, "bwd")
@@ -1060,7 +1090,8 @@ class StageExecutor:
                 K.linear_dgrad(dy, W("weight"), dx, stream=st)
                 self.grad_init.add(x_t)
             K.linear_wgrad(dy, x, G("weight"), accumulate=self._wgrad_acc, stream=st)
-            K.colsum(dy, G("bias"), stream=st)
+            if n.id not in self._bias_done:
+                K.colsum(dy, G("bias"), stream=st)
             if k == "linear_res":
                 self._contribute_identity(out_tid(n.inputs[1]), dy)
         elif k == "gelu":

@@ -71,3 +71,29 @@ def test_two_replicas_match_one_double_batch(name):
     assert cos > 0.98 and rel < 0.2, (cos, rel)
     # the mean of the replicas' per-token losses is the double batch's loss
     torch.testing.assert_close((lossr[0] + lossr[1]) / 2, loss1, rtol=2e-2, atol=1e-3)
+    # ... and to the CPU fp32 oracle trained on the concatenated micro-batches
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    from oracle.train_ref import dims_from, reference_train
+    from paper_2505_05856_b200.runtime.model import build_nodes
+    ids_cat = torch.stack([torch.cat([halves[0][0][j], halves[1][0][j]]) for j in range(m)])
+    lab_cat = torch.stack([torch.cat([halves[0][1][j], halves[1][1][j]]) for j in range(m)])
+    nodes = [n.id for n in build_nodes(cfg)]
+    opt = reps[0].opt
+    want_losses, want = reference_train(
+        dims_from(cfg, build_nodes(cfg)), init, ids_cat, lab_cat, [nodes],
+        dict(lr=opt.lr, beta1=opt.beta1, beta2=opt.beta2, eps=opt.eps, weight_decay=opt.weight_decay))
+    got_losses = ((lossr[0] + lossr[1]) / 2).tolist()
+    for a, r in zip(got_losses, want_losses[0]):
+        assert abs(a - r) <= 2e-2 * abs(r), (got_losses, want_losses)
+    for n in reps[0].params.slots:
+        if n.endswith("qkv.bias"):
+            continue  # zero-gradient key bias (test_pipeline_gpu._compare)
+        got = reps[0].params.master_view(n).float().cpu()
+        w0n = init[n]
+        if w0n.norm() > 0:
+            assert float((got - want[n]).norm() / want[n].norm()) <= 2e-2, n
+        dg, dw = (got - w0n).flatten(), (want[n] - w0n).flatten()
+        if dw.norm() > 0:
+            assert float(torch.dot(dg, dw) / (dg.norm() * dw.norm())) >= 0.95, n

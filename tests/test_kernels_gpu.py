@@ -204,6 +204,40 @@ def test_layernorm(cols):
     close(db, br.grad, rel=5e-3)
 
 
+@pytest.mark.parametrize("rows,cols", [(333, 128), (16384, 1024), (1000, 768), (2048, 1600),
+                                       (7, 1024), (8192, 2048)])
+@pytest.mark.parametrize("add", [False, True])
+def test_layernorm_bwd_fused(rows, cols, add):
+    """One-pass LayerNorm backward (dx, dgamma, dbeta, + the bias gradient of
+    the linear producing the LN input = column sums of the final dx) against
+    the fp32 torch reference."""
+    k = K()
+    x = rnd(rows, cols, scale=2.0)
+    g, b = rnd(cols), rnd(cols)
+    y = torch.empty_like(x)
+    mean = torch.empty(rows, device="cuda")
+    rstd = torch.empty(rows, device="cuda")
+    k.layernorm_fwd(x, g, b, y, mean, rstd)
+    xr = x.float().requires_grad_()
+    gr = g.float().requires_grad_()
+    br = b.float().requires_grad_()
+    yr = torch.nn.functional.layer_norm(xr, (cols,), gr, br, 1e-5)
+    dy = rnd(rows, cols)
+    yr.backward(dy.float())
+    dxa = rnd(rows, cols) if add else None
+    dx = dxa.clone() if add else torch.empty_like(x)   # in place over dx_add, as the executor does
+    dg = torch.full((cols,), 0.5, device="cuda")       # accumulates into what is there
+    db = torch.zeros(cols, device="cuda")
+    dbias = torch.full((cols,), -1.0, device="cuda")
+    k.layernorm_bwd_fused(dy, x, g, mean, rstd, dx, dg, db, dx_add=dx if add else None, dbias=dbias)
+    torch.cuda.synchronize()
+    want_dx = xr.grad + (dxa.float() if add else 0)
+    close(dx, want_dx)
+    close(dg, gr.grad + 0.5, rel=5e-3)
+    close(db, br.grad, rel=5e-3)
+    close(dbias, dx.float().sum(0) - 1.0, rel=5e-3)
+
+
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("cols", [128, 512, 1024])
 def test_softmax(causal, cols):
