@@ -21,6 +21,7 @@
 #ifndef DAWNPIPER_H_
 #define DAWNPIPER_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -37,6 +38,21 @@ int dpn_init(int device);
 int dpn_host_alloc(int64_t bytes, void** out);   /* pinned, portable */
 int dpn_host_free(void* host_ptr);
 int dpn_memset_async(void* dst, int value, int64_t bytes, void* stream);
+
+/* Per-stage device arenas (runtime/arena.py).  One cudaMalloc of cap_bytes per arena; torch's
+ * caching allocator draws its segments from it through a MemPool whose pluggable allocator is
+ * dpn_arena_malloc / dpn_arena_free, so the arena is the stage's device-memory cap and its
+ * high-water mark the stage's measured peak.  The arena serving a malloc is the calling thread's
+ * current one (dpn_arena_select; -1 = none, mallocs then fail). */
+int dpn_arena_create(int device, int64_t cap_bytes, int* handle);
+int dpn_arena_destroy(int handle);
+int dpn_arena_select(int handle);
+int dpn_arena_stats(int handle, int64_t* in_use, int64_t* peak, int64_t* cap);
+int dpn_arena_reset_peak(int handle);
+void* dpn_arena_malloc(size_t size, int device, void* stream);    /* torch pluggable (cudaStream_t) */
+void dpn_arena_free(void* ptr, size_t size, int device, void* stream);
+/* Free every arena the library created (device synchronize first). */
+int dpn_destroy(void);
 
 /* Swap engine (memopt swap actions).  The copy is issued on copy_stream after
  * it waits for ready_event (if non-NULL); done_event (if non-NULL) is recorded

@@ -43,6 +43,12 @@ SIGNATURES = {
     "dpn_host_alloc": [_i64, C.POINTER(_vp)],
     "dpn_host_free": [_vp],
     "dpn_memset_async": [_vp, C.c_int, _i64, _vp],
+    "dpn_arena_create": [C.c_int, _i64, C.POINTER(C.c_int)],
+    "dpn_arena_destroy": [C.c_int],
+    "dpn_arena_select": [C.c_int],
+    "dpn_arena_stats": [C.c_int, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64)],
+    "dpn_arena_reset_peak": [C.c_int],
+    "dpn_destroy": [],
     "dpn_swap_out": [_vp, _vp, _i64, _vp, _vp, _vp],
     "dpn_swap_in": [_vp, _vp, _i64, _vp, _vp, _vp],
     "dpn_p2p_copy": [_vp, C.c_int, _vp, C.c_int, _i64, _vp],
@@ -104,6 +110,11 @@ def load_library() -> C.CDLL:
                 fn.restype = C.c_int
             lib.dpn_last_error.argtypes = []
             lib.dpn_last_error.restype = C.c_char_p
+            # torch's pluggable-allocator entry points (called by torch, typed for completeness)
+            lib.dpn_arena_malloc.argtypes = [C.c_size_t, C.c_int, _vp]
+            lib.dpn_arena_malloc.restype = _vp
+            lib.dpn_arena_free.argtypes = [_vp, C.c_size_t, C.c_int, _vp]
+            lib.dpn_arena_free.restype = None
             _lib = lib
     return _lib
 

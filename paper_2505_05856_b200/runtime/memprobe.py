@@ -37,7 +37,7 @@ from .stage import StageExecutor
 
 def probe_stage(model: TransformerConfig, g, plan, x: int, b: int, *, cap: Optional[int] = None,
                 micro_batches: Optional[int] = None, device: int = 0, init=None,
-                swap_knobs: Optional[dict] = None) -> dict:
+                swap_knobs: Optional[dict] = None, use_arena: bool = False) -> dict:
     dev = torch.device("cuda", device)
     init_device(device)
     l = len(plan.stages)
@@ -50,9 +50,17 @@ def probe_stage(model: TransformerConfig, g, plan, x: int, b: int, *, cap: Optio
     torch.cuda.empty_cache()
     base = torch.cuda.memory_allocated(device)
     torch.cuda.reset_peak_memory_stats(device)
-    if cap is not None:
+    arena = None
+    if cap is not None and use_arena:  # the stage's own cap-sized arena (runtime/arena.py)
+        from .arena import StageArena
+        arena = StageArena(device, cap)
+    elif cap is not None:
         torch.cuda.set_per_process_memory_fraction(min(1.0, (cap + base) / total), device)
     ex = None
+    import contextlib
+    scope = contextlib.ExitStack()
+    if arena is not None:
+        scope.enter_context(arena.active())
     try:
         stream = torch.cuda.Stream(device=dev)
         ex = StageExecutor(cfg=model, g=g, nodes=build_nodes(model), lo=lo, hi=hi, stage=x, stages=l,
@@ -102,6 +110,8 @@ def probe_stage(model: TransformerConfig, g, plan, x: int, b: int, *, cap: Optio
                     ops.append(("opt", j, e1, e2))
         torch.cuda.synchronize(device)
         peak = torch.cuda.max_memory_allocated(device) - base
+        if arena is not None:  # the arena's high-water mark (allocator segments)
+            peak = arena.stats()[1]
         st = ex.memstats
 
         def span_us(pairs):
@@ -144,6 +154,10 @@ def probe_stage(model: TransformerConfig, g, plan, x: int, b: int, *, cap: Optio
     finally:
         del ex
         release_workspaces()
+        gc.collect()
+        scope.close()
+        if arena is not None:
+            arena.close()
         gc.collect()
         torch.cuda.synchronize(device)
         torch.cuda.empty_cache()

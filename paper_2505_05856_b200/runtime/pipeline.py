@@ -66,6 +66,10 @@ class RunConfig:
     # 80 -> 44 ms per micro-batch, peak +1.3 GB)
     d2h_budget: int = 1 << 30
     swap_prefetch: int = 2 << 30
+    # one device arena per stage (runtime/arena.py) of `capacity` bytes: the
+    # stage's own cap (as on its own GPU) and its measured peak; the arenas
+    # are reserved up front, so the stages sharing a device must fit it
+    arenas: bool = False
 
     def __post_init__(self):
         if self.micro_batches < 1:
@@ -171,7 +175,13 @@ class Pipeline:
                 if a != b:
                     from .._lib import check, lib
                     check(lib().dpn_enable_peer(a, b), "dpn_enable_peer")
-        if cfg.capacity is not None:
+        self.arenas = None
+        if cfg.arenas:
+            if cfg.capacity is None:
+                raise ValueError("per-stage arenas need a capacity")
+            from .arena import StageArena
+            self.arenas = [StageArena(d, cfg.capacity) for d in self.stage_dev]
+        elif cfg.capacity is not None:
             # the plan's capacity is per stage; stages sharing a GPU share its cap
             for d in set(self.stage_dev):
                 total = torch.cuda.get_device_properties(d).total_memory
@@ -190,7 +200,7 @@ class Pipeline:
         self.stages: List[StageExecutor] = []
         for x, (lo, hi) in enumerate(bounds, start=1):
             d = self.stage_dev[x - 1]
-            with torch.cuda.device(d):
+            with torch.cuda.device(d), self._arena(x - 1):
                 self.stages.append(StageExecutor(
                     cfg=model, g=g, nodes=nodes, lo=lo, hi=hi, stage=x, stages=self.l,
                     micro_batch=cfg.micro_batch_size, memopt=plan.memopt[x - 1], init=init,
@@ -204,6 +214,16 @@ class Pipeline:
         self.static_bytes = [self._stage_bytes(s) for s in self.stages]
         for d in set(self.stage_dev):
             torch.cuda.synchronize(d)  # parameter init (default stream) before the run streams
+
+    def _arena(self, x: int):
+        """Allocation context of stage index x (0-based)."""
+        if self.arenas is None:
+            import contextlib
+            return contextlib.nullcontext()
+        return self.arenas[x].active()
+
+    def arena_peaks(self) -> Optional[List[int]]:
+        return None if self.arenas is None else [a.stats()[1] for a in self.arenas]
 
     @staticmethod
     def _stage_bytes(s: StageExecutor) -> int:
@@ -344,35 +364,39 @@ class Pipeline:
         pending: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
         mailbox: Dict[Tuple[int, int], Dict[str, torch.Tensor]] = {}
         for x, kind, j in self.order:
-            s = self.stages[x - 1]
-            st = self.streams[self.stage_dev[x - 1]]
-            if events is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record(st)
-            if kind == "fwd":
-                if x > 1:
-                    self._deliver_fwd(x, j, mailbox.pop((x, j)))
-                s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
-                          labels=labels[j - 1] if s.is_last else None,
-                          loss_out=self.loss[j - 1:j] if s.is_last else None)
-                if x < self.l:
-                    mailbox[(x + 1, j)] = self._send_fwd(x, j)
-            else:
-                for tid, gt in pending.pop((x, j), {}).items():
-                    s.set_recv_grad(tid, gt)
-                grads = s.backward(j)
-                if x > 1:
-                    pending[(x - 1, j)] = self._send_bwd(x, grads)
-                s.finish_backward(j)
-            if events is not None:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record(st)
-                events.append((x, j, kind, e0, e1))
+            with self._arena(x - 1):
+                self._op_serial(x, kind, j, ids, labels, events, pending, mailbox)
         if self.sync:  # GPipe: one update per stage after the last backward
             for x, s in enumerate(self.stages):
-                with torch.cuda.stream(self.streams[self.stage_dev[x]]):
+                with torch.cuda.stream(self.streams[self.stage_dev[x]]), self._arena(x):
                     s.optimizer_step()
         return self.loss
+
+    def _op_serial(self, x, kind, j, ids, labels, events, pending, mailbox) -> None:
+        s = self.stages[x - 1]
+        st = self.streams[self.stage_dev[x - 1]]
+        if events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+        if kind == "fwd":
+            if x > 1:
+                self._deliver_fwd(x, j, mailbox.pop((x, j)))
+            s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
+                      labels=labels[j - 1] if s.is_last else None,
+                      loss_out=self.loss[j - 1:j] if s.is_last else None)
+            if x < self.l:
+                mailbox[(x + 1, j)] = self._send_fwd(x, j)
+        else:
+            for tid, gt in pending.pop((x, j), {}).items():
+                s.set_recv_grad(tid, gt)
+            grads = s.backward(j)
+            if x > 1:
+                pending[(x - 1, j)] = self._send_bwd(x, grads)
+            s.finish_backward(j)
+        if events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(st)
+            events.append((x, j, kind, e0, e1))
 
     def _step_streams(self, ids, labels, events=None) -> torch.Tensor:
         """Co-located stages on their own streams: fork from the device's main
@@ -389,50 +413,56 @@ class Pipeline:
         mailbox: Dict[Tuple[int, int], tuple] = {}
         last = None
         for x, kind, j in self.order:
-            s = self.stages[x - 1]
-            st = self.stage_streams[x - 1]
-            if self.serialize and last is not None:
-                st.wait_event(last)
-            if events is not None:
-                e0 = torch.cuda.Event(enable_timing=True)
-                e0.record(st)
-            if kind == "fwd":
-                if x > 1:
-                    msgs, ev = mailbox.pop((x, j))
-                    st.wait_event(ev)
-                    with torch.cuda.stream(st):
-                        for tid, msg in msgs.items():
-                            s.adopt_recv(tid, j, msg)
-                s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
-                          labels=labels[j - 1] if s.is_last else None,
-                          loss_out=self.loss[j - 1:j] if s.is_last else None)
-                if x < self.l:
-                    mailbox[(x + 1, j)] = self._send_fwd_streams(x, j)
-            else:
-                if (x, j) in pending:
-                    gts, ev = pending.pop((x, j))
-                    st.wait_event(ev)
-                    for tid, gt in gts.items():
-                        s.set_recv_grad(tid, gt)
-                grads = s.backward(j)
-                if x > 1:
-                    pending[(x - 1, j)] = self._send_bwd_streams(x, grads)
-                s.finish_backward(j)
-            if events is not None:
-                e1 = torch.cuda.Event(enable_timing=True)
-                e1.record(st)
-                events.append((x, j, kind, e0, e1))
-            if self.serialize:
-                last = torch.cuda.Event()
-                last.record(st)
+            with self._arena(x - 1):
+                last = self._op_streams(x, kind, j, ids, labels, events, pending, mailbox, last)
         if self.sync:
-            for s in self.stages:
-                s.optimizer_step()
+            for x, s in enumerate(self.stages):
+                with self._arena(x):
+                    s.optimizer_step()
         for st in self.stage_streams:
             join = torch.cuda.Event()
             join.record(st)
             main.wait_event(join)
         return self.loss
+
+    def _op_streams(self, x, kind, j, ids, labels, events, pending, mailbox, last):
+        s = self.stages[x - 1]
+        st = self.stage_streams[x - 1]
+        if self.serialize and last is not None:
+            st.wait_event(last)
+        if events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+        if kind == "fwd":
+            if x > 1:
+                msgs, ev = mailbox.pop((x, j))
+                st.wait_event(ev)
+                with torch.cuda.stream(st):
+                    for tid, msg in msgs.items():
+                        s.adopt_recv(tid, j, msg)
+            s.forward(j, ids=ids[j - 1] if s.needs_ids else None,
+                      labels=labels[j - 1] if s.is_last else None,
+                      loss_out=self.loss[j - 1:j] if s.is_last else None)
+            if x < self.l:
+                mailbox[(x + 1, j)] = self._send_fwd_streams(x, j)
+        else:
+            if (x, j) in pending:
+                gts, ev = pending.pop((x, j))
+                st.wait_event(ev)
+                for tid, gt in gts.items():
+                    s.set_recv_grad(tid, gt)
+            grads = s.backward(j)
+            if x > 1:
+                pending[(x - 1, j)] = self._send_bwd_streams(x, grads)
+            s.finish_backward(j)
+        if events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(st)
+            events.append((x, j, kind, e0, e1))
+        if self.serialize:
+            last = torch.cuda.Event()
+            last.record(st)
+        return last
 
     def report(self, events: list, t_origin: torch.cuda.Event, losses: torch.Tensor,
                wall_us: float) -> RunReport:
@@ -452,7 +482,8 @@ class Pipeline:
         iteration = float(makespan) if self.sync else async_iteration(done, self.l, self.m, makespan)
         busy = [sum(e.end - e.start for e in ev if e.stage == x + 1) for x in range(self.l)]
         bubble = 1.0 - sum(busy) / (self.l * makespan) if makespan > 0 else 0.0
-        peaks = list(self.static_bytes)
+        measured = self.arena_peaks()
+        peaks = measured if measured is not None else list(self.static_bytes)
         top = max(peaks) if peaks else 0
         waste = sum(top - p for p in peaks) / (self.l * top) if top > 0 else 0.0
         cap = self.cfg.capacity
@@ -465,7 +496,9 @@ class Pipeline:
             losses=tuple(float(v) for v in losses.tolist()),
             samples_per_s=((b * (self.m if self.sync else 1)) * 1e6 / iteration) if iteration > 0 else 0.0,
             step_time_us=wall_us,
-            device_peak_bytes=max(torch.cuda.max_memory_allocated(d) for d in set(self.stage_dev)))
+            device_peak_bytes=max(torch.cuda.max_memory_allocated(d) for d in set(self.stage_dev)),
+            per_stage_peak_source="measured: stage arena high-water mark" if measured is not None
+            else "static")
 
 
 def run(plan: PartitionPlan, g: ComputationGraph, cfg: RunConfig,
@@ -482,11 +515,16 @@ def run(plan: PartitionPlan, g: ComputationGraph, cfg: RunConfig,
     pipe = Pipeline(model, g, plan, cfg)
     try:
         rep = _run(pipe, model, cfg, ids, labels, steps)
-        if rep is not None and cfg.measure_stage_peaks:
+        if rep is not None and cfg.measure_stage_peaks and pipe.arenas is None:
             rep = _with_measured_peaks(rep, pipe, model, g, plan, cfg)
         return rep
     finally:
-        if cfg.capacity is not None:  # the cap does not outlive the run
+        if pipe.arenas is not None:  # the stages' arenas do not outlive the run
+            arenas = pipe.arenas
+            del pipe
+            for a in arenas:
+                a.close()
+        elif cfg.capacity is not None:  # the cap does not outlive the run
             for d in set(pipe.stage_dev):
                 torch.cuda.set_per_process_memory_fraction(1.0, d)
 

@@ -29,7 +29,8 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert lib.dpn_version() == 1
     # every declared symbol is typed by the binding
-    assert set(_declared()) <= set(_lib.SIGNATURES) | {"dpn_last_error"}
+    assert set(_declared()) <= set(_lib.SIGNATURES) | {"dpn_last_error", "dpn_arena_malloc",
+                                                      "dpn_arena_free"}
 
 
 def test_bad_arguments_fail_with_a_message():
