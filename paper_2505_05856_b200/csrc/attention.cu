@@ -447,7 +447,7 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t* r) 
       : "r"(taddr));
 }
 
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(96)
     attn_fwd2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                      const AttnParams p) {
   extern __shared__ uint8_t smem_raw[];

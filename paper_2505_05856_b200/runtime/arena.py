@@ -62,7 +62,9 @@ class StageArena:
         gc.collect()
         torch.cuda.synchronize(self.device)
         torch.cuda.empty_cache()
-        check(lib().dpn_arena_destroy(self.handle), "dpn_arena_destroy")
+        # a block still referenced elsewhere (e.g. a cached workspace) keeps the
+        # arena's reservation alive; the memory is returned by dpn_destroy
+        lib().dpn_arena_destroy(self.handle)
 
     def reset_peak(self) -> None:
         check(lib().dpn_arena_reset_peak(self.handle), "dpn_arena_reset_peak")

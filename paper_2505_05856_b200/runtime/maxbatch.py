@@ -151,14 +151,20 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
         w = l - x + 1
         m = micro_batches or (w + 1)
         gen = torch.Generator(device=dev).manual_seed(x)
+        # harness inputs: two micro-batches, cycled, and only on the stages that
+        # read them (the stage itself keeps its w input slots, like in a run)
         ishape, idt = model.input_spec(b)
-        if idt == torch.int32:
-            ids = torch.randint(0, model.vocab, (m,) + tuple(ishape), device=dev, dtype=idt,
-                                generator=gen)
-        else:  # CNN images
-            ids = torch.randn((m,) + tuple(ishape), device=dev, generator=gen).to(idt)
-        labels = torch.randint(0, model.vocab, (m, b * model.out_tokens), device=dev,
-                               dtype=torch.int32, generator=gen)
+        n_in = min(m, 2)
+        ids = labels = None
+        if ex.needs_ids:
+            if idt == torch.int32:
+                ids = torch.randint(0, model.vocab, (n_in,) + tuple(ishape), device=dev, dtype=idt,
+                                    generator=gen)
+            else:  # CNN images
+                ids = torch.randn((n_in,) + tuple(ishape), device=dev, generator=gen).to(idt)
+        if ex.is_last:
+            labels = torch.randint(0, model.vocab, (n_in, b * model.out_tokens), device=dev,
+                                   dtype=torch.int32, generator=gen)
         loss = torch.zeros(m, device=dev)
         with torch.cuda.stream(stream):
             for kind, j, _ in async_ops(l, m, x):
@@ -166,8 +172,8 @@ def check_stage(model: TransformerConfig, g, plan, x: int, b: int, cap: int, dev
                     for tid in ex.recv_ids:
                         buf = ex.recv_buffer(tid, j)
                         buf.normal_(0, 1, generator=gen) if buf.is_floating_point() else None
-                    ex.forward(j, ids=ids[j - 1] if ex.needs_ids else None,
-                               labels=labels[j - 1] if ex.is_last else None,
+                    ex.forward(j, ids=ids[(j - 1) % n_in] if ex.needs_ids else None,
+                               labels=labels[(j - 1) % n_in] if ex.is_last else None,
                                loss_out=loss[j - 1:j] if ex.is_last else None)
                 else:
                     for tid in ex.send_ids:
@@ -324,7 +330,7 @@ def _timed_stages(rec: dict, model, g, plan, b: int, cap: int, device: int, init
 def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, strategy: str,
               b_max: int = 64, device: int = 0, log=None, host_cap: int = 96 * GIB,
               run_gpu: bool = True, margins: Tuple[float, ...] = (0.1, 0.2),
-              overhead: Overhead = DEFAULT_OVERHEAD) -> Tuple[int, List[dict]]:
+              overhead: Overhead = DEFAULT_OVERHEAD, b_start: int = 1) -> Tuple[int, List[dict]]:
     """Largest feasible b (0 if none) by doubling then bisection.
 
     Measured-memory feedback for the planned strategies: the planner's memory
@@ -347,10 +353,12 @@ def max_batch(model: TransformerConfig, stages: int, cap: int, bandwidth: int, s
                 return False  # planner / host-memory infeasibility: a margin cannot help
         return False
 
-    if not ok(1):
-        return 0, hist
-    lo, hi = 1, None
-    b = 2
+    if b_start > 1 and ok(b_start):  # resume from a size known to fit
+        lo, hi, b = b_start, None, 2 * b_start
+    else:
+        if not ok(1):
+            return 0, hist
+        lo, hi, b = 1, None, 2
     while b <= b_max:
         if ok(b):
             lo = b

@@ -71,13 +71,20 @@ def probe_stage(model: TransformerConfig, g, plan, x: int, b: int, *, cap: Optio
         for k, v in (swap_knobs or {}).items():  # d2h_budget, prefetch_budget, swap_lookahead
             setattr(ex, k, v)
         gen = torch.Generator(device=dev).manual_seed(x)
+        # harness inputs: two micro-batches, cycled, and only on the stages that
+        # read them (the stage itself keeps its w input slots, like in a run)
         ishape, idt = model.input_spec(b)
-        if idt == torch.int32:
-            ids = torch.randint(0, model.vocab, (m,) + tuple(ishape), device=dev, dtype=idt, generator=gen)
-        else:
-            ids = torch.randn((m,) + tuple(ishape), device=dev, generator=gen).to(idt)
-        labels = torch.randint(0, model.vocab, (m, b * model.out_tokens), device=dev,
-                               dtype=torch.int32, generator=gen)
+        n_in = min(m, 2)
+        ids = labels = None
+        if ex.needs_ids:
+            if idt == torch.int32:
+                ids = torch.randint(0, model.vocab, (n_in,) + tuple(ishape), device=dev, dtype=idt,
+                                    generator=gen)
+            else:  # CNN images
+                ids = torch.randn((n_in,) + tuple(ishape), device=dev, generator=gen).to(idt)
+        if ex.is_last:
+            labels = torch.randint(0, model.vocab, (n_in, b * model.out_tokens), device=dev,
+                                   dtype=torch.int32, generator=gen)
         loss = torch.zeros(m, device=dev)
         ops = []
         with torch.cuda.stream(stream):
@@ -95,8 +102,8 @@ def probe_stage(model: TransformerConfig, g, plan, x: int, b: int, *, cap: Optio
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
                 if kind == "fwd":
-                    ex.forward(j, ids=ids[j - 1] if ex.needs_ids else None,
-                               labels=labels[j - 1] if ex.is_last else None,
+                    ex.forward(j, ids=ids[(j - 1) % n_in] if ex.needs_ids else None,
+                               labels=labels[(j - 1) % n_in] if ex.is_last else None,
                                loss_out=loss[j - 1:j] if ex.is_last else None)
                 else:
                     ex.backward(j)

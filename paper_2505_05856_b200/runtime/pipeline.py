@@ -522,6 +522,7 @@ def run(plan: PartitionPlan, g: ComputationGraph, cfg: RunConfig,
         if pipe.arenas is not None:  # the stages' arenas do not outlive the run
             arenas = pipe.arenas
             del pipe
+            K.release_workspaces()  # scratch buffers cached per stage stream live in the arenas
             for a in arenas:
                 a.close()
         elif cfg.capacity is not None:  # the cap does not outlive the run

@@ -25,6 +25,7 @@ ap.add_argument("--stages", type=int, default=8)
 ap.add_argument("--cap-gib", type=float, default=40.0)
 ap.add_argument("--bandwidth-gbs", type=float, default=48.0, help="host link for swaps (GB/s)")
 ap.add_argument("--b-max", type=int, default=64)
+ap.add_argument("--b-start", type=int, default=1, help="a micro-batch known to fit (resume)")
 ap.add_argument("--out", default=None)
 ap.add_argument("--host-cap-gib", type=float, default=64.0)
 ap.add_argument("--calibrate", action="store_true")
@@ -49,7 +50,7 @@ for strat in args.strategies.split(","):
     t0 = time.time()
     best, hist = max_batch(cfg, args.stages, cap, bw, strat, b_max=args.b_max,
                            log=lambda r: print(json.dumps(r), flush=True), host_cap=host_cap,
-                           run_gpu=not args.no_gpu, overhead=overhead)
+                           run_gpu=not args.no_gpu, overhead=overhead, b_start=args.b_start)
     res[strat] = {"max_micro_batch": best, "search_s": round(time.time() - t0, 1), "trials": hist}
     if best and not args.no_gpu and not args.no_timing:
         ok = [r for r in hist if r["b"] == best and r.get("feasible")][0]

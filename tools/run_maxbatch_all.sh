@@ -1,12 +1,15 @@
 #!/bin/bash
-# Max-batch sweep of the BASELINE models at 8 and 4 stages under a 40 GiB
-# per-GPU cap (Table 2 of the paper); one JSON result per (model, stages).
-# usage: tools/run_maxbatch_all.sh "gpt2-xl:8:64 t5-large:8:512" [outdir]
+# Max-batch sweep of the BASELINE models under a 40 GiB per-GPU cap (Table 2
+# of the paper); one JSON result per spec.
+# usage: tools/run_maxbatch_all.sh "gpt2-xl:8:64 t5-large:8:512[:strategies[:b_start]]" [outdir]
 out=${2:-gpurun_out/maxbatch}
 mkdir -p "$out"
 for spec in $1; do
-  IFS=: read model stages bmax <<< "$spec"
+  IFS=: read model stages bmax strats bstart <<< "$spec"
+  strats=${strats:-even_compute,even_compute_memopt,dawnpiper}
+  tag=${model}_l${stages}${bstart:+_from$bstart}
   timeout 3000 python tools/max_batch.py --model "$model" --stages "$stages" --b-max "$bmax" \
-     --calibrate --out "$out/${model}_l${stages}.json" > "$out/${model}_l${stages}.log" 2>&1
-  echo "$model l=$stages rc=$? $(tail -1 "$out/${model}_l${stages}.log" | cut -c1-600)"
+     --strategies "$strats" --b-start "${bstart:-1}" \
+     --calibrate --out "$out/$tag.json" > "$out/$tag.log" 2>&1
+  echo "$model l=$stages rc=$? $(tail -1 "$out/$tag.log" | cut -c1-600)"
 done
