@@ -199,9 +199,9 @@ __device__ __forceinline__ void red_add_v4(float* addr, const float* v) {
 // flight per iteration.  The CTA's column partials combine across groups in
 // shared memory and go out with one vector red per 4 columns.
 //   bytes: read dy, x (, dx_add), write dx  (+ 8 B of stats per row)
-constexpr int kLnThreads = 512;
+constexpr int kLnThreads = 256;  // two CTAs per SM: their load / reduce / store phases interleave
 constexpr int kLnRows = 3;
-__global__ void __launch_bounds__(kLnThreads, 1) ln_bwd_fused_kernel(
+__global__ void __launch_bounds__(kLnThreads, 2) ln_bwd_fused_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(kLnThreads, 1) ln_bwd_fused_kernel(
   const int chunk = wi * 32 + lane;
   const bool in_grp = grp < groups;
   const bool col = in_grp && chunk < nvec;
-  float* stat = ln_smem;                       // [2 parity][16 warps][kLnRows][2]
-  float* part = ln_smem + 2 * 16 * kLnRows * 2; // [groups][cols]
+  float* stat = ln_smem;                       // [2 parity][warps][kLnRows][2]
+  float* part = ln_smem + 2 * (kLnThreads / 32) * kLnRows * 2; // [groups][cols]
   float gm[8], ag[8], ab[8], ad[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) ag[i] = ab[i] = ad[i] = 0.f;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kLnThreads, 1) ln_bwd_fused_kernel(
         mu[u] = r < r1 ? mean[r] : 0.f;
         rs[u] = r < r1 ? rstd[r] : 0.f;
       }
-      float* st = stat + parity * 16 * kLnRows * 2;
+      float* st = stat + parity * (kLnThreads / 32) * kLnRows * 2;
 #pragma unroll
       for (int u = 0; u < kLnRows; ++u) {
         float xv[8], dv[8], s1 = 0.f, s2 = 0.f;
@@ -829,18 +829,18 @@ extern "C" int dpn_layernorm_bwd_fused(const void* dy, const void* x, const void
                                        const float* mean, const float* rstd, void* dx,
                                        const void* dx_add, float* dgamma, float* dbeta,
                                        float* dbias, int64_t rows, int64_t cols, void* stream) {
-  DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * 32 * 16, "cols must be a multiple of 8, <= 4096");
+  DPN_REQUIRE(cols % 8 == 0 && cols <= 8 * kLnThreads, "cols must be a multiple of 8, <= 2048");
   DPN_REQUIRE(dgamma && dbeta, "the fused LayerNorm backward produces dgamma and dbeta");
   if (rows == 0) return 0;
   const int nvec = (int)(cols / 8);
   const int G = (nvec + 31) / 32;
   const int groups = (kLnThreads / 32) / G;
-  // one CTA per SM (persistent over a band of rows), at least kLnRows * groups rows each
+  // two CTAs per SM (persistent over bands of rows), at least kLnRows * groups rows each
   const long long per_iter = (long long)groups * kLnRows;
-  long long per = (rows + 147) / 148;
+  long long per = (rows + 295) / 296;
   per = std::max<long long>(per_iter, (per + per_iter - 1) / per_iter * per_iter);
   const unsigned grid = (unsigned)((rows + per - 1) / per);
-  const size_t smem = (2 * 16 * kLnRows * 2 + (size_t)groups * cols) * sizeof(float);
+  const size_t smem = (2 * (kLnThreads / 32) * kLnRows * 2 + (size_t)groups * cols) * sizeof(float);
   static bool attr = false;
   if (!attr) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(ln_bwd_fused_kernel,
