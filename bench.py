@@ -181,8 +181,11 @@ def gemm_traffic():
     of the bench step (profiles/, cold-cache replay), else None."""
     import gzip
     import csv as _csv
-    p = ROOT / "profiles" / "r01_launches_step_b32.csv.gz"
-    if not p.exists():
+    for name in ("r02_launches_step.csv.gz", "r01_launches_step_b32.csv.gz"):
+        p = ROOT / "profiles" / name
+        if p.exists():
+            break
+    else:
         return None
     try:
         rows = list(_csv.reader(gzip.open(p, "rt")))
@@ -197,7 +200,7 @@ def gemm_traffic():
                 tot += float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
                 ids.add(r[0])
         return {"bytes_per_launch": round(tot / len(ids)), "launches": len(ids),
-                "source": "profiles/r01_launches_step_b32.csv.gz (ncu dram__bytes_read+write, cold cache)"} if ids else None
+                "source": f"profiles/{p.name} (ncu dram__bytes_read+write, cold cache)"} if ids else None
     except Exception:
         return None
 

@@ -309,7 +309,9 @@ def _timed_stages(rec: dict, model, g, plan, b: int, cap: int, device: int, init
     per = []
     for x in range(1, len(plan.stages) + 1):
         try:
-            r = probe_stage(model, g, plan, x, b, cap=cap, device=device, init=init)
+            # the same op list length as the feasibility check (w + 1 micro-batches)
+            r = probe_stage(model, g, plan, x, b, cap=cap, device=device, init=init,
+                            micro_batches=len(plan.stages) - x + 2)
         except torch.OutOfMemoryError as e:
             rec.update(feasible=False, reason=f"stage {x} OOM on GPU: {str(e).splitlines()[0][:160]}")
             return rec

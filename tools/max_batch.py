@@ -32,6 +32,8 @@ ap.add_argument("--calibrate", action="store_true")
 ap.add_argument("--no-gpu", action="store_true")
 ap.add_argument("--no-timing", action="store_true")
 ap.add_argument("--strategies", default="even_compute,even_compute_memopt,dawnpiper")
+ap.add_argument("--time-at", default="", help="STRAT:B[,STRAT:B]: only time those max batches "
+                "(margins 0 / 0.1 / 0.2 as the search)")
 args = ap.parse_args()
 cfg = PRESETS[args.model]
 cap = int(args.cap_gib * (1 << 30))
@@ -46,6 +48,21 @@ if args.calibrate and not args.no_gpu:
     res["overhead_calibration"] = {"points": pts, "seconds": round(time.time() - t0, 1)}
     print(json.dumps({"overhead": overhead.to_doc()}), flush=True)
 res["overhead"] = overhead.to_doc()
+if args.time_at:
+    for item in args.time_at.split(","):
+        strat, b = item.split(":")
+        for margin in (0.0, 0.1, 0.2):
+            timed = try_batch(cfg, int(b), args.stages, cap, bw, strat, host_cap=host_cap,
+                              margin=margin, overhead=overhead, timing=True)
+            if timed.get("feasible"):
+                break
+        res[strat] = {"max_micro_batch": int(b), "at_max": timed}
+        print(json.dumps({"strategy": strat, "at_max": {k: timed.get(k) for k in (
+            "b", "margin", "feasible", "samples_per_s_l_gpus", "samples_per_s_l_gpus_model",
+            "bottleneck_us", "stage_peak_gib", "reason")}}), flush=True)
+    if args.out:
+        open(args.out, "w").write(json.dumps(res, indent=1))
+    sys.exit(0)
 for strat in args.strategies.split(","):
     t0 = time.time()
     best, hist = max_batch(cfg, args.stages, cap, bw, strat, b_max=args.b_max,

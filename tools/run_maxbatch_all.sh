@@ -13,3 +13,11 @@ for spec in $1; do
      --calibrate --out "$out/$tag.json" > "$out/$tag.log" 2>&1
   echo "$model l=$stages rc=$? $(tail -1 "$out/$tag.log" | cut -c1-600)"
 done
+# timing-only specs: TIME="model:stages:STRAT:B,STRAT:B ..." tools/run_maxbatch_all.sh ""
+for spec in $TIME; do
+  IFS=: read model stages rest <<< "$spec"
+  tag=${model}_l${stages}_timing
+  timeout 3000 python tools/max_batch.py --model "$model" --stages "$stages" --calibrate \
+     --time-at "$rest" --out "$out/$tag.json" > "$out/$tag.log" 2>&1
+  echo "$model l=$stages timing rc=$? $(grep at_max "$out/$tag.log" | cut -c1-300)"
+done
