@@ -63,6 +63,8 @@ def parse():
                          "DawnPiper plan under --cap-gib on the GPU and report model vs measured")
     ap.add_argument("--cap-gib", type=float, default=40.0)
     ap.add_argument("--swap-gbs", type=float, default=48.0, help="host link the planner assumes")
+    ap.add_argument("--link-aware", action="store_true",
+                    help="--memopt-stage: plan with the link-aware eviction costs (beyond the reference)")
     return ap.parse_args()
 
 
@@ -498,7 +500,8 @@ def run_memopt_stage(args):
     cap = int(args.cap_gib * (1 << 30))
     g = b200_profile(cfg, b, iters=args.profile_iters, warmup=3)
     t0 = time.perf_counter()
-    plan, pcfg = plan_for_cap(cfg, g, stages, cap, int(args.swap_gbs * 1e9), b=b)
+    plan, pcfg = plan_for_cap(cfg, g, stages, cap, int(args.swap_gbs * 1e9), b=b,
+                              link_aware=args.link_aware)
     t_plan = time.perf_counter() - t0
     x = heaviest_stage(plan)
     # the executor's memory-faithful defaults, then the throughput knobs
@@ -509,6 +512,7 @@ def run_memopt_stage(args):
     res_overlap = probe_stage(cfg, g, plan, x, b, cap=cap,
                               swap_knobs={"d2h_budget": rc.d2h_budget, "prefetch_budget": rc.swap_prefetch})
     out = {"mode": "memopt_stage", "model": args.model, "micro_batch": b, "stages": stages,
+           "link_aware": args.link_aware,
            "cap_bytes": cap, "planner_capacity": pcfg.capacity, "planner_bandwidth_Bps": pcfg.bandwidth,
            "plan_s": round(t_plan, 3), "cuts": list(plan.cuts.positions),
            "actions_per_stage": [len(m.actions) for m in plan.memopt],

@@ -208,14 +208,16 @@ def host_bytes(plan, stages: int) -> List[int]:
 
 
 def plan_for_cap(model: TransformerConfig, g, stages: int, cap: int, bandwidth: int,
-                 margin: float = 0.0, b: int = 1, overhead: Overhead = DEFAULT_OVERHEAD):
+                 margin: float = 0.0, b: int = 1, overhead: Overhead = DEFAULT_OVERHEAD,
+                 link_aware: bool = False):
     """DawnPiper plan for a per-GPU byte cap: the planner gets the cap minus
     what its memory model does not see (`stage_overhead`), re-planned with the
     reserve of the plan's own stages until every stage's overhead is covered.
     Raises InfeasibleModelError."""
     reserve = optimizer_reserve(model, g, stages, b=b, overhead=overhead)
     cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC,
-                       capacity=max(1, int((cap - reserve) * (1.0 - margin))), bandwidth=bandwidth)
+                       capacity=max(1, int((cap - reserve) * (1.0 - margin))), bandwidth=bandwidth,
+                       link_aware=link_aware)
     for _ in range(4):
         plan = P.plan(g, cfg)
         need = optimizer_reserve(model, g, stages, plan.cuts.positions, b=b, overhead=overhead)
@@ -225,7 +227,7 @@ def plan_for_cap(model: TransformerConfig, g, stages: int, cap: int, bandwidth: 
         if pcap <= 0:
             raise P.InfeasibleModelError("stage overhead alone exceeds the cap")
         cfg = P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=pcap,
-                           bandwidth=bandwidth)
+                           bandwidth=bandwidth, link_aware=link_aware)
     return plan, cfg
 
 
@@ -246,9 +248,10 @@ def try_batch(model: TransformerConfig, b: int, stages: int, cap: int, bandwidth
     if pcap <= 0:
         rec.update(feasible=False, reason="optimizer state alone exceeds the cap")
         return rec
-    if strategy == "dawnpiper":
+    if strategy in ("dawnpiper", "dawnpiper_link"):
         try:
-            plan, cfg = plan_for_cap(model, g, stages, cap, bandwidth, margin, b, overhead)
+            plan, cfg = plan_for_cap(model, g, stages, cap, bandwidth, margin, b, overhead,
+                                     link_aware=strategy == "dawnpiper_link")
         except P.InfeasibleModelError as e:
             rec.update(feasible=False, reason=f"planner: {e}")
             return rec
