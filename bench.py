@@ -5,12 +5,13 @@
 
 Workload (BASELINE.json configs[1]): BERT-large (24 x 1024, 16 heads, FFN 4096,
 vocab 30522), seq 512, partitioned by this package's planner into an 8-stage
-async-1F1B DawnPiper plan, micro-batch b=32, m=32 micro-batches per step
+async-1F1B DawnPiper plan, micro-batch b=48, m=32 micro-batches per step
 (m = 4l, cli.py:226-228), bf16 compute with fp32 master weights, PipeDream
 weight stashing and a per-micro-batch AdamW update.  BASELINE.json leaves b
-open ("b swept"); b=32 is the largest swept size (8, 16, 32 ->
-533 / 612 / 663 samples/s, profiles/r01_bench_*) -- larger micro-batches fill
-the tensor cores better and amortise the per-micro-batch optimizer step.  At N=1 all 8 stages are
+open ("b swept"); swept sizes 8 / 16 / 32 / 48 gave 533 / 612 /
+705 / 726 samples/s (profiles/r01_bench_*, profiles/r02_bench_*) -- larger
+micro-batches fill the tensor cores better and amortise the per-micro-batch
+optimizer step.  At N=1 all 8 stages are
 co-located on one GPU; at N>1 (torchrun) the plan has l=N stages, one per GPU.
 
 A step = one pipeline iteration (m micro-batches, b*m samples, every forward,
@@ -51,7 +52,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="bert-large")
-    ap.add_argument("--micro-batch", type=int, default=32)
+    ap.add_argument("--micro-batch", type=int, default=48)
     ap.add_argument("--stages", type=int, default=0, help="default: 8 at N=1, N otherwise; "
                     "l < N at N>1 runs N/l data-parallel replicas of an l-stage pipeline")
     ap.add_argument("--micro-batches", type=int, default=32)
@@ -136,10 +137,23 @@ def committed_profile(model: str, b: int):
     inputs of the reference-generated large goldens), or None."""
     import gzip
     from paper_2505_05856_b200 import planner as P
-    f = ROOT / "tests" / "golden" / "profiles" / f"{model}_b{b}.json.gz"
+    d = ROOT / "tests" / "golden" / "profiles"
+    f = d / f"{model}_b{b}.json.gz"
     if not f.exists():
         return None
     return P.graph_from_doc(json.loads(gzip.decompress(f.read_bytes())))
+
+
+def committed_cuts_profile(model: str, b: int):
+    """The committed measured profile of `model` at the micro-batch closest to
+    b (relative node times barely move with b), or None: what the reference
+    arm plans its stage cuts on."""
+    d = ROOT / "tests" / "golden" / "profiles"
+    sizes = sorted(int(f.name.split("_b")[1].split(".")[0]) for f in d.glob(f"{model}_b*.json.gz"))
+    if not sizes:
+        return None, None
+    bb = min(sizes, key=lambda x: (abs(x - b), x))
+    return committed_profile(model, bb), bb
 
 
 class CpuPort:
@@ -456,8 +470,8 @@ def run_reference(args):
     from paper_2505_05856_b200.runtime.model import PRESETS
     cfg = PRESETS[args.model]
     stages = args.stages or (8 if world == 1 else world)
-    g = committed_profile(args.model, args.micro_batch)
-    src = "committed B200-measured profile" if g is not None else "analytic profile"
+    g, bb = committed_cuts_profile(args.model, args.micro_batch)
+    src = f"committed B200-measured profile at b={bb}" if g is not None else "analytic profile"
     if g is None:
         g = profile_graph(cfg, args.micro_batch)
     plan = P.plan(g, P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC,
@@ -472,7 +486,7 @@ def run_reference(args):
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
            "data": "synthetic", "impl": "reference",
            "config": {"workload": f"{args.model} s{cfg.seq}, {stages}-stage DawnPiper 1F1B plan "
-                                  f"(cuts from the {src} at b={args.micro_batch}), CPU training step "
+                                  f"(cuts from the {src}), CPU training step "
                                   f"on a bounded sample per step",
                       "model": args.model, "seq_len": cfg.seq, "stages": stages,
                       "cuts": list(plan.cuts.positions), **CPU_SAMPLE},
