@@ -112,16 +112,6 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// spin until the shared PV-completion counter reaches `n` (acquire: the MMA
-// results it stands for are visible to the tcgen05.ld that follows)
-__device__ __forceinline__ void pv_wait(uint32_t* counter, uint32_t n) {
-  const uint32_t a = smem_u32(counter);
-  uint32_t v;
-  do {
-    asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-  } while (v < n);
-}
-
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                     const AttnParams p) {
@@ -188,7 +178,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       mbar_init(&o_empty[i], 8);
     }
     mbar_init(pv_done, 1);
-    tmem_slot[1] = 0;  // PV tiles completed, published by warp 3
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<512>(tmem_slot);
@@ -282,23 +271,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       }
     }
     if (g >= 1) issue_pv(g - 1, prev_first, prev_ub, prev_uc);
-  } else if (warp == 3) {
-    // PV completion counter: waits every pv_done phase in order (so no waiter
-    // ever lags the barrier by two phases) and publishes the count in shared
-    // memory; the softmax warps consult it only when they must rescale O, and
-    // otherwise release P(j) without waiting for PV(j-1).
-    if (lane == 0) {
-      const uint32_t cnt = smem_u32(tmem_slot + 1);
-      uint32_t t = 0;
-      for (long long u = blockIdx.x; u < units; u += gridDim.x) {
-        int qt, h, bb;
-        decode(u, qt, h, bb);
-        for (int j = kv_tiles(qt); j > 0; --j, ++t) {
-          mbar_wait(pv_done, t & 1);
-          asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(cnt), "r"(t + 1) : "memory");
-        }
-      }
-    }
   } else if (warp >= 4) {
     // ---------------- softmax ----------------
     const int quarter = warp & 3, half = (warp - 4) >> 2;
@@ -374,10 +346,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
         l = l * alpha + (sum2.x + sum2.y);
         fence_async_smem();
-        if (j > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        if (j > 0) {
           // O_half holds tiles < j once PV(j-1) is done; rescale rows whose max grew
-          {
-            pv_wait(tmem_slot + 1, (uint32_t)gj);
+          mbar_wait(pv_done, (gj - 1) & 1);
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
             tc_fence_after();
             uint32_t ou[64];
             tmem_ld_32x32b_x32(o_half, ou);
@@ -395,7 +367,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         if (lane == 0) mbar_arrive(&p_full[i]);
       }
       // ---- unit epilogue: combine the key halves ----
-      pv_wait(tmem_slot + 1, (uint32_t)(g + n_kv));
+      mbar_wait(pv_done, (g + n_kv - 1) & 1);
       tc_fence_after();
       float* xm = xs + ub * 512 + r * 4;
       xm[half * 2] = ms;
