@@ -351,10 +351,25 @@ class Pipeline:
     def step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
         """One training iteration (m micro-batches).  ids/labels: int32 [m, b*s] on
         the first / last stage's device.  Returns the device loss vector [m]."""
+        last_dev = self.stage_dev[-1]
+        caller = torch.cuda.current_stream(last_dev)
+        # ... and the pipeline's streams wait for whatever the caller's streams
+        # did before (e.g. the H2D copy of ids / labels)
+        for d, st in self.streams.items():
+            ready = torch.cuda.Event()
+            ready.record(torch.cuda.current_stream(d))
+            st.wait_event(ready)
         if len(self.streams) == 1:  # co-located: everything on one stream
             with torch.cuda.stream(next(iter(self.streams.values()))):
-                return self._step(ids, labels, events)
-        return self._step(ids, labels, events)
+                loss = self._step(ids, labels, events)
+        else:
+            loss = self._step(ids, labels, events)
+        # the loss vector is written on the pipeline's streams: the caller's
+        # stream waits for it, so reading it there (e.g. .tolist()) is ordered
+        done = torch.cuda.Event()
+        done.record(self.streams[last_dev])
+        caller.wait_event(done)
+        return loss
 
     def _step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
         if self.multi:
