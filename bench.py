@@ -59,6 +59,8 @@ def parse():
     ap.add_argument("--capacity-gib", type=float, default=160.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=10)
+    ap.add_argument("--cuda-graph", action="store_true",
+                    help="replay each iteration as one captured CUDA graph (RunConfig.cuda_graph)")
     ap.add_argument("--memopt-stage", action="store_true",
                     help="instead of the throughput line: run the heaviest-memopt stage of a "
                          "DawnPiper plan under --cap-gib on the GPU and report model vs measured")
@@ -249,7 +251,8 @@ def run_ours(args):
     plan = P.plan(g, P.PlanConfig(stages=stages, schedule=P.SCHEDULE_ASYNC, capacity=cap,
                                   bandwidth=64 << 30))
     t_plan = time.perf_counter() - t_plan
-    pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, trace=False))
+    pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, trace=False,
+                                            cuda_graph=args.cuda_graph))
     ids, labels = synthetic_batch(cfg, m, b, seed=0)
     ids_d, lab_d = ids.cuda(), labels.cuda()
     st = pipe.streams[pipe.stage_dev[0]]
@@ -272,6 +275,8 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     launches = (K.INSTR.launches - l0) // args.steps
+    if args.cuda_graph:  # one graph launch per step; the kernels it replays
+        launches = pipe.graph_launches
     samples = args.steps * m * b
     value = samples / (ms / 1e3)
 
@@ -349,7 +354,8 @@ def run_ours(args):
                    "cuts": list(plan.cuts.positions), "parallelism": f"pp{stages} co-located",
                    "profile": f"measured B200 node times ({args.profile_iters} iters, {t_prof:.1f} s); "
                               f"plan {t_plan:.2f} s; graph hash {P.canonical_hash(g)}",
-                   "l2": "working set > L2 (no flush needed)"},
+                   "l2": "working set > L2 (no flush needed)",
+                   "issue": "one CUDA graph per iteration" if args.cuda_graph else "eager (ctypes launches)"},
         "model_tflops": round(value * cfg.flops_per_sample() / 1e12, 1),
         "e2e": e2e, "roofline": roofline, "gpu_launches": launches, "clocks": clk,
         "losses_last_step": [round(x, 4) for x in losses.tolist()[:4]],

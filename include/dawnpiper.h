@@ -163,6 +163,11 @@ int dpn_embed_bwd(const int32_t* ids, const void* dout, float* dtok, float* dpos
 /* AdamW over a stage's flat f32 buffers; writes the new bf16 weight version. */
 int dpn_adamw(float* w, float* m, float* v, const float* g, void* out_bf16, int64_t n, float lr,
               float beta1, float beta2, float eps, float weight_decay, int64_t step, void* stream);
+/* AdamW with the step count in device memory (incremented, then used for the
+ * bias corrections): replayable inside a CUDA graph. */
+int dpn_adamw_dstep(float* w, float* m, float* v, const float* g, void* out_bf16, int64_t n,
+                    float lr, float beta1, float beta2, float eps, float wd, int64_t* step_dev,
+                    void* stream);
 
 /* ---- CNN nodes (AmoebaNet-D; synth.py:123-135 conv / act / pool vocabulary) ----
  * Activations are NHWC bf16 viewed as [pixels, C], C % 8 == 0.  3x3 windows

@@ -73,6 +73,7 @@ SIGNATURES = {
     "dpn_embed_fwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_embed_bwd": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp],
     "dpn_adamw": [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _f32, _i64, _vp],
+    "dpn_adamw_dstep": [_vp, _vp, _vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _f32, _vp, _vp],
     "dpn_relu_fwd": [_vp, _vp, _i64, _vp],
     "dpn_relu_bwd": [_vp, _vp, _vp, _i64, _vp],
     "dpn_dwconv3_fwd": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _vp],

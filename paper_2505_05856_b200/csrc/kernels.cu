@@ -758,8 +758,13 @@ __global__ void embed_bwd_kernel(const int* __restrict__ ids, const __nv_bfloat1
 __global__ void adamw_kernel(float* __restrict__ w, float* __restrict__ m, float* __restrict__ v,
                              const float* __restrict__ g, __nv_bfloat16* __restrict__ out,
                              long long n4, float lr, float b1, float b2, float eps, float wd,
-                             float bc1, float bc2) {
+                             float bc1, float bc2, const long long* __restrict__ step_dev) {
   pdl_wait();
+  if (step_dev != nullptr) {  // device step counter (CUDA-graph replay): bias corrections here
+    const float t = (float)(*step_dev);
+    bc1 = 1.f - powf(b1, t);
+    bc2 = 1.f - powf(b2, t);
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     float4 wv = reinterpret_cast<float4*>(w)[i];
@@ -1016,7 +1021,27 @@ extern "C" int dpn_adamw(float* w, float* m, float* v, const float* g, void* out
   if (n == 0) return 0;
   const float bc1 = 1.f - powf(beta1, (float)step), bc2 = 1.f - powf(beta2, (float)step);
   DPN_CHECK_CUDA(launch_pdl(adamw_kernel, grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream, 
-      w, m, v, g, (__nv_bfloat16*)out_bf16, n / 4, lr, beta1, beta2, eps, wd, bc1, bc2));
+      w, m, v, g, (__nv_bfloat16*)out_bf16, n / 4, lr, beta1, beta2, eps, wd, bc1, bc2,
+      (const long long*)nullptr));
+  DPN_LAUNCH_CHECK();
+  return 0;
+}
+
+__global__ void step_increment_kernel(long long* step) { *step += 1; }
+
+// AdamW whose step count lives in device memory: `step_dev` is incremented and
+// then read by the update (so a CUDA graph replays with the right bias
+// corrections every time).
+extern "C" int dpn_adamw_dstep(float* w, float* m, float* v, const float* g, void* out_bf16,
+                               int64_t n, float lr, float beta1, float beta2, float eps, float wd,
+                               int64_t* step_dev, void* stream) {
+  DPN_REQUIRE(n % 4 == 0 && step_dev != nullptr, "n must be a multiple of 4; step_dev required");
+  if (n == 0) return 0;
+  step_increment_kernel<<<1, 1, 0, (cudaStream_t)stream>>>((long long*)step_dev);
+  DPN_LAUNCH_CHECK();
+  DPN_CHECK_CUDA(launch_pdl(adamw_kernel, grid_for(n / 4, 256), 256, 0, (cudaStream_t)stream,
+      w, m, v, g, (__nv_bfloat16*)out_bf16, n / 4, lr, beta1, beta2, eps, wd, 1.f, 1.f,
+      (const long long*)step_dev));
   DPN_LAUNCH_CHECK();
   return 0;
 }

@@ -307,6 +307,14 @@ def adamw(w, m, v, g, out_bf16, lr, beta1, beta2, eps, wd, step, stream=None):
                           _s(stream)), "dpn_adamw")
 
 
+def adamw_dstep(w, m, v, g, out_bf16, lr, beta1, beta2, eps, wd, step_dev, stream=None):
+    """AdamW with a device-resident step counter (CUDA-graph replayable)."""
+    INSTR.launches += 2
+    check(lib().dpn_adamw_dstep(w.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
+                                out_bf16.data_ptr(), w.numel(), lr, beta1, beta2, eps, wd,
+                                step_dev.data_ptr(), _s(stream)), "dpn_adamw_dstep")
+
+
 def memset(t, value=0, nbytes=None, stream=None):
     n = nbytes if nbytes is not None else t.numel() * t.element_size()
     check(lib().dpn_memset_async(t.data_ptr(), value, n, _s(stream)), "dpn_memset_async")

@@ -70,6 +70,12 @@ class RunConfig:
     # stage's own cap (as on its own GPU) and its measured peak; the arenas
     # are reserved up front, so the stages sharing a device must fit it
     arenas: bool = False
+    # replay each iteration as one captured CUDA graph (co-located async
+    # plans without memopt actions): the host issues one graph launch per step
+    # instead of every kernel -- what a small-b / small-model step needs when
+    # ~20k ctypes launches take longer than the GPU work (C1: 64 ms of host
+    # issue for 64 ms of GPU time, tools/host_profile.py)
+    cuda_graph: bool = False
 
     def __post_init__(self):
         if self.micro_batches < 1:
@@ -209,6 +215,7 @@ class Pipeline:
                 self.stages[-1].d2h_budget = cfg.d2h_budget
                 self.stages[-1].prefetch_budget = cfg.swap_prefetch
         self.order = sync_order(self.l, self.m) if self.sync else colocated_order(self.l, self.m)
+        self._graph = None
         first_dev = self.stage_dev[0]
         self.loss = torch.zeros(self.m, dtype=torch.float32, device=torch.device("cuda", self.stage_dev[-1]))
         self.static_bytes = [self._stage_bytes(s) for s in self.stages]
@@ -351,6 +358,94 @@ class Pipeline:
     def step(self, ids: torch.Tensor, labels: torch.Tensor, events: Optional[list] = None) -> torch.Tensor:
         """One training iteration (m micro-batches).  ids/labels: int32 [m, b*s] on
         the first / last stage's device.  Returns the device loss vector [m]."""
+        if self.cfg.cuda_graph and events is None and not self.serialize:
+            return self._graph_step(ids, labels)
+        loss = self._eager_step(ids, labels, events)
+        if self._graph is not None:  # keep the replay invariant: newest weights in the start slot
+            self._restore_ring()
+        return loss
+
+    def _restore_ring(self) -> None:
+        dev = self.stage_dev[0]
+        main = self.streams[dev]
+        for s, l0 in zip(self.stages, self._graph_start):
+            if s.params.latest != l0:
+                K.copy_d2d(s.params.ring[l0], s.params.ring[s.params.latest], dst_dev=dev,
+                           src_dev=dev, stream=main)
+                s.params.latest = l0
+
+    # ---- CUDA-graph mode --------------------------------------------------------
+
+    def _graph_step(self, ids: torch.Tensor, labels: torch.Tensor) -> torch.Tensor:
+        dev = self.stage_dev[0]
+        main = self.streams[dev]
+        if self._graph is None:
+            self._capture(ids, labels)
+        caller = torch.cuda.current_stream(dev)
+        ready = torch.cuda.Event()
+        ready.record(caller)
+        main.wait_event(ready)
+        with torch.cuda.stream(main):
+            self._gids.copy_(ids, non_blocking=True)
+            self._glabels.copy_(labels, non_blocking=True)
+            self._graph.replay()
+        done = torch.cuda.Event()
+        done.record(main)
+        caller.wait_event(done)
+        return self.loss
+
+    def _capture(self, ids: torch.Tensor, labels: torch.Tensor) -> None:
+        """Warm up eagerly on static input buffers, then capture one iteration.
+
+        A captured iteration replays with the addresses it was recorded with,
+        so (1) every tensor the stages hold when capture starts is kept alive
+        (buffers handed over during the step are replaced by graph-pool ones),
+        (2) each stage's newest weights are copied back into the ring slot they
+        occupied at capture start, so every replay starts from the same ring
+        state, and (3) AdamW reads its step count from device memory."""
+        if len(self.streams) != 1 or self.sync:
+            raise ValueError("CUDA-graph mode runs co-located async (1F1B) plans")
+        if any(m.actions for m in self.plan.memopt):
+            raise ValueError("CUDA-graph mode runs plans without swap / recompute actions")
+        dev = self.stage_dev[0]
+        main = self.streams[dev]
+        for s in self.stages:
+            s.params.device_step = True
+            s.params.step_dev.fill_(s.params.step)
+        self._gids = ids.clone()
+        self._glabels = labels.clone()
+        # the warm-up iterations must not train: snapshot and restore the state
+        saved = [(s.params.latest, s.params.step,
+                  [t.clone() for t in (s.params.master, s.params.m, s.params.v, s.params.ring,
+                                       s.params.step_dev)]) for s in self.stages]
+        for _ in range(2):  # lazy allocations, workspaces, kernel attributes
+            self._eager_step(self._gids, self._glabels, None)
+        torch.cuda.synchronize(dev)
+        for s, (latest, step, ts) in zip(self.stages, saved):
+            for dst, src in zip((s.params.master, s.params.m, s.params.v, s.params.ring,
+                                 s.params.step_dev), ts):
+                dst.copy_(src)
+            s.params.latest, s.params.step = latest, step
+        del saved
+        torch.cuda.synchronize(dev)
+        keep = []
+        for s in self.stages:
+            for d in s.slot_buf:
+                keep += list(d.values())
+            keep += list(s.live.values()) + list(s.grads.values())
+            keep += list(getattr(s, "ids", [])) + list(getattr(s, "labels", []))
+        self._keepalive = keep
+        self._graph_start = [s.params.latest for s in self.stages]
+        g = torch.cuda.CUDAGraph()
+        n0 = K.INSTR.launches
+        with torch.cuda.graph(g, stream=main):
+            self._step(self._gids, self._glabels, None)
+            self._restore_ring()
+        self.graph_launches = K.INSTR.launches - n0  # kernels one replay launches
+        self._graph = g
+
+    def _eager_step(self, ids: torch.Tensor, labels: torch.Tensor,
+                    events: Optional[list] = None) -> torch.Tensor:
         last_dev = self.stage_dev[-1]
         caller = torch.cuda.current_stream(last_dev)
         # ... and the pipeline's streams wait for whatever the caller's streams

@@ -94,6 +94,10 @@ class FlatParams:
         for k in range(versions):
             K.cast_f32_bf16(self.master, self.ring[k])
         self.step = 0
+        # device-resident step count (CUDA-graph mode: the update reads it on
+        # the GPU, so a replayed step applies the right bias corrections)
+        self.device_step = False
+        self.step_dev = torch.zeros(1, dtype=torch.int64, device=device)
         # weight-version ring bookkeeping (PipeDream stashing): the newest
         # version sits in `latest`; micro-batches in flight pin the slot their
         # forward read until their backward retires
@@ -144,8 +148,13 @@ class FlatParams:
 
     def adamw(self, out_slot: int, opt: AdamWConfig, stream=None) -> None:
         self.step += 1
-        K.adamw(self.master, self.m, self.v, self.grad, self.ring[out_slot], opt.lr, opt.beta1,
-                opt.beta2, opt.eps, opt.weight_decay, self.step, stream=stream)
+        if self.device_step:
+            K.adamw_dstep(self.master, self.m, self.v, self.grad, self.ring[out_slot], opt.lr,
+                          opt.beta1, opt.beta2, opt.eps, opt.weight_decay, self.step_dev,
+                          stream=stream)
+        else:
+            K.adamw(self.master, self.m, self.v, self.grad, self.ring[out_slot], opt.lr, opt.beta1,
+                    opt.beta2, opt.eps, opt.weight_decay, self.step, stream=stream)
         self.latest = out_slot
 
 

@@ -5,9 +5,13 @@ from paper_2505_05856_b200 import planner as P
 from paper_2505_05856_b200.runtime.graph import profile_graph
 from paper_2505_05856_b200.runtime.model import PRESETS, synthetic_batch
 from paper_2505_05856_b200.runtime.pipeline import Pipeline, RunConfig
-cfg = PRESETS["bert-large"]; b, m = 8, 32
+name = sys.argv[1] if len(sys.argv) > 1 else "bert-large"
+b = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+m = int(sys.argv[3]) if len(sys.argv) > 3 else 32
+stages = int(sys.argv[4]) if len(sys.argv) > 4 else 8
+cfg = PRESETS[name]
 g = profile_graph(cfg, b)
-plan = P.plan(g, P.PlanConfig(8, P.SCHEDULE_ASYNC, 160 << 30, 64 << 30))
+plan = P.plan(g, P.PlanConfig(stages, P.SCHEDULE_ASYNC, 160 << 30, 64 << 30))
 pipe = Pipeline(cfg, g, plan, RunConfig(micro_batches=m, micro_batch_size=b, trace=False))
 ids, lab = synthetic_batch(cfg, m, b); ids, lab = ids.cuda(), lab.cuda()
 for _ in range(3): pipe.step(ids, lab)
