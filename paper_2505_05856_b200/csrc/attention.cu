@@ -790,6 +790,345 @@ __global__ void __maxnreg__(96)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Forward, two softmax sets of whole rows (DPN_ATTN_FWD=3, experimental): set k
+// (4 warps, one per TMEM lane quarter, a thread owns a query row and all 128
+// keys of a tile) takes the KV tiles t with t % 2 == k, with its own S buffer,
+// P buffer, running max / sum and O accumulator; the tensor core runs one
+// set's S / PV while the other exponentiates.  10 warps leave 200 registers
+// per thread for the 128 scores a row holds.  TMEM: S[set] 128 columns each,
+// O[unit parity][set] 64 columns each.
+constexpr int kFwd3Threads = 320;  // warp 0 TMA + TMEM, warp 1 MMA, warps 2-9 softmax
+constexpr int kFwd3Bars = 2 + 2 * kKV2Stages + 4 * 2 + 2;
+constexpr int kFwd3Smem = 1024 + kTileBytes * (1 + 2 * kKV2Stages) + 2 * kPBytes + kFwd3Bars * 8 + 16 +
+                          2 * 128 * 2 * 2 * 4;
+
+__global__ void __maxnreg__(200)
+    attn_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
+                     const AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + kTileBytes;
+  uint8_t* sV = sK + kKV2Stages * kTileBytes;
+  uint8_t* sP = sV + kKV2Stages * kTileBytes;  // [set] 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* kv_full = bars + 2;
+  uint64_t* kv_empty = kv_full + kKV2Stages;
+  uint64_t* s_full = kv_empty + kKV2Stages;  // [set]
+  uint64_t* s_empty = s_full + 2;            // [set]
+  uint64_t* p_full = s_empty + 2;            // [set]
+  uint64_t* p_empty = p_full + 2;            // [set]
+  uint64_t* pv_done = p_empty + 2;           // [set]
+  uint64_t* o_empty = pv_done + 2;           // [unit parity]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kFwd3Bars);
+  float* xs = reinterpret_cast<float*>(tmem_slot + 4);  // [unit parity][128 rows][set][m, l]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_kv_all = (p.kv_seq + kTile - 1) / kTile;
+  const int n_qt = (p.seq + kTile - 1) / kTile;
+  const long long bh = (long long)p.batch * p.heads;
+  const long long units = bh * n_qt;
+  auto decode = [&](long long u, int& qt, int& h, int& bb) {
+    int qi;
+    long long r;
+    if (p.causal) {
+      qi = (int)(u / bh);
+      r = u - (long long)qi * bh;
+    } else {
+      qi = (int)(u % n_qt);
+      r = u / n_qt;
+    }
+    qt = p.causal ? n_qt - 1 - qi : qi;
+    h = (int)(r % p.heads);
+    bb = (int)(r / p.heads);
+  };
+  auto kv_tiles = [&](int qt) { return p.causal ? min(n_kv_all, qt + 1) : n_kv_all; };
+  auto set_count = [&](long long g0, int n_kv, int k) {
+    const int first = ((g0 & 1) == k) ? 0 : 1;
+    return first < n_kv ? (n_kv - first + 1) / 2 : 0;
+  };
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tm_q);
+    prefetch_tmap(&tm_kv);
+  }
+  if (warp == 1 && lane == 0) {
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < kKV2Stages; ++s) {
+      mbar_init(&kv_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);  // the set's 4 softmax warps
+      mbar_init(&p_full[i], 4);
+      mbar_init(&p_empty[i], 1);
+      mbar_init(&pv_done[i], 1);
+      mbar_init(&o_empty[i], 8);  // every softmax warp reads both sets' O of the unit
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      long long g = 0;
+      int uc = 0;
+      for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+        int qt, h, bb;
+        decode(u, qt, h, bb);
+        const int n_kv = kv_tiles(qt), row0 = bb * p.seq, krow0 = bb * p.kv_seq;
+        mbar_wait(q_empty, (uc & 1) ^ 1);
+        mbar_expect_tx(q_full, kTileBytes);
+        tma_load_2d(sQ, &tm_q, q_full, p.q_col + h * kD, row0 + qt * kTile);
+        for (int j = 0; j < n_kv; ++j, ++g) {
+          const int st = (int)(g % kKV2Stages);
+          mbar_wait(&kv_empty[st], (int)((g / kKV2Stages) & 1) ^ 1);
+          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
+          tma_load_2d(sK + st * kTileBytes, &tm_kv, &kv_full[st], p.k_col + h * kD, krow0 + j * kTile);
+          tma_load_2d(sV + st * kTileBytes, &tm_kv, &kv_full[st], p.v_col + h * kD, krow0 + j * kTile);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
+    constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);
+    struct Pending {
+      long long t;
+      int first, uc;
+    };
+    Pending pa{0, 0, 0}, pb{0, 0, 0};
+    int npend = 0;
+    auto issue_pv = [&](const Pending& d) {
+      const int i = (int)(d.t & 1), ub = d.uc & 1;
+      mbar_wait(&p_full[i], (int)((d.t >> 1) & 1));
+      if (d.first) mbar_wait(&o_empty[ub], ((d.uc >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (lane == 0) {
+        const int st = (int)(d.t % kKV2Stages);
+        const uint32_t pa_ = smem_u32(sP + i * kPBytes), vb = smem_u32(sV + st * kTileBytes);
+#pragma unroll
+        for (int k = 0; k < kTile / 16; ++k) {
+          const uint64_t ad = smem_desc_sw128(pa_ + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(vb + k * 2048, kD * 128, 1024);
+          umma_bf16(tmem + 256 + ub * 128 + i * 64, ad, bd, idesc_o, (d.first && k == 0) ? 0u : 1u);
+        }
+        umma_commit(&p_empty[i]);
+        umma_commit(&kv_empty[st]);
+        umma_commit(&pv_done[i]);
+      }
+      __syncwarp();
+    };
+    long long g = 0;
+    int uc = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+      int qt, h, bb;
+      decode(u, qt, h, bb);
+      const int n_kv = kv_tiles(qt);
+      mbar_wait(q_full, uc & 1);
+      for (int j = 0; j < n_kv; ++j) {
+        const long long t = g + j;
+        const int st = (int)(t % kKV2Stages), i = (int)(t & 1);
+        mbar_wait(&kv_full[st], (int)((t / kKV2Stages) & 1));
+        mbar_wait(&s_empty[i], (int)((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
+#pragma unroll
+          for (int k = 0; k < kD / 16; ++k) {
+            const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
+            const uint64_t bd = smem_desc_sw128(kb + k * 32, 16, 1024);
+            umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+          }
+          umma_commit(&s_full[i]);
+          if (j == n_kv - 1) umma_commit(q_empty);
+        }
+        __syncwarp();
+        const Pending d{t, j < 2 ? 1 : 0, uc};
+        if (npend == 2) {
+          issue_pv(pa);
+          pa = pb;
+          pb = d;
+        } else if (npend == 1) {
+          pb = d;
+          npend = 2;
+        } else {
+          pa = d;
+          npend = 1;
+        }
+      }
+      g += n_kv;
+    }
+    if (npend >= 1) issue_pv(pa);
+    if (npend == 2) issue_pv(pb);
+  } else {
+    // ---------------- softmax: warps 2-9, set = (warp - 2) / 4 ----------------
+    const int set = (warp - 2) >> 2;
+    const int quarter = warp & 3;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const float sl = p.scale_log2;
+    long long g = 0;
+    int uc = 0, tc_mine = 0, tc_other = 0;
+    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
+      int qt, h, bb;
+      decode(u, qt, h, bb);
+      const int n_kv = kv_tiles(qt), row0 = bb * p.seq, ub = uc & 1;
+      const int q = qt * kTile + r;
+      const int cnt0 = set_count(g, n_kv, 0), cnt1 = set_count(g, n_kv, 1);
+      const int cnt_other = set ? cnt0 : cnt1;
+      const uint32_t o_mine = tmem + 256 + ub * 128 + set * 64 + lane_off;
+      float ms = -INFINITY, l = 0.f;
+      const int j0 = ((g & 1) == set) ? 0 : 1;
+      for (int j = j0; j < n_kv; j += 2) {
+        const long long t = g + j;
+        const int i = set;
+        const int k0 = j * kTile;
+        const bool mask = (j + 1) * kTile > p.kv_seq || (p.causal && j == qt);
+        mbar_wait(&s_full[i], (int)((t >> 1) & 1));
+        tc_fence_after();
+        uint32_t sv[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tmem + i * 128 + c * 32 + lane_off, sv + c * 32);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[i]);
+        if (mask) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const int key = k0 + c;
+            if (!(key < p.kv_seq && (!p.causal || key <= q))) sv[c] = __float_as_uint(-INFINITY);
+          }
+        }
+        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < 128; c += 4) {
+          m4[0] = fmaxf(m4[0], __uint_as_float(sv[c]));
+          m4[1] = fmaxf(m4[1], __uint_as_float(sv[c + 1]));
+          m4[2] = fmaxf(m4[2], __uint_as_float(sv[c + 2]));
+          m4[3] = fmaxf(m4[3], __uint_as_float(sv[c + 3]));
+        }
+        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl;
+        float alpha = 1.f;
+        if (mx > ms + kRescaleLog2 || ms == -INFINITY) {
+          alpha = (ms == -INFINITY) ? 0.f : ex2(ms - mx);
+          ms = mx;
+        }
+        const float base = (ms == -INFINITY) ? 0.f : ms;
+        float2 sum2 = make_float2(0.f, 0.f);
+        mbar_wait(&p_empty[i], (int)((t >> 1) & 1) ^ 1);
+        uint8_t* pt = sP + i * kPBytes;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          float e8[8];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const float2 a = fma2(make_float2(__uint_as_float(sv[c * 8 + e]), __uint_as_float(sv[c * 8 + e + 1])),
+                                  make_float2(sl, sl), make_float2(-base, -base));
+            const float2 ev = make_float2(ex2(a.x), ex2(a.y));
+            e8[e] = ev.x;
+            e8[e + 1] = ev.y;
+            sum2 = fma2(make_float2(1.f, 1.f), ev, sum2);
+          }
+          uint4 w;
+          w.x = pack_bf16(e8[0], e8[1]);
+          w.y = pack_bf16(e8[2], e8[3]);
+          w.z = pack_bf16(e8[4], e8[5]);
+          w.w = pack_bf16(e8[6], e8[7]);
+          *reinterpret_cast<uint4*>(pt + (c >> 3) * (kPBytes / 2) + sw128(r, c & 7)) = w;
+        }
+        l = l * alpha + (sum2.x + sum2.y);
+        fence_async_smem();
+        if (j >= 2) {
+          mbar_wait(&pv_done[i], (tc_mine - 1) & 1);
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+            tc_fence_after();
+            uint32_t ou[64];
+            tmem_ld_32x32b_x32(o_mine, ou);
+            tmem_ld_32x32b_x32(o_mine + 32, ou + 32);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 64; ++e) ou[e] = __float_as_uint(__uint_as_float(ou[e]) * alpha);
+            tmem_st_32x32b_x32(o_mine, ou);
+            tmem_st_32x32b_x32(o_mine + 32, ou + 32);
+            tmem_st_wait();
+          }
+        }
+        tc_mine += 1;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[i]);
+      }
+      tc_other += cnt_other;
+      // ---- unit epilogue: combine the two sets ----
+      if (cnt0 > 0) mbar_wait(&pv_done[0], ((set ? tc_other : tc_mine) - 1) & 1);
+      if (cnt1 > 0) mbar_wait(&pv_done[1], ((set ? tc_mine : tc_other) - 1) & 1);
+      tc_fence_after();
+      float* xm = xs + (ub * 128 + r) * 4;
+      xm[set * 2] = ms;
+      xm[set * 2 + 1] = l;
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(64) : "memory");
+      const float m = fmaxf(xm[0], xm[2]);
+      const float a0 = xm[0] == -INFINITY ? 0.f : ex2(xm[0] - m);
+      const float a1 = xm[2] == -INFINITY ? 0.f : ex2(xm[2] - m);
+      const float lt = xm[1] * a0 + xm[3] * a1;
+      // this warp writes output columns 32 * set .. from both sets' accumulators
+      float o[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) o[e] = 0.f;
+      if (cnt0 > 0) {
+        uint32_t oo[32];
+        tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + 0 * 64 + set * 32 + lane_off, oo);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(oo[e]) * a0;
+      }
+      if (cnt1 > 0) {
+        uint32_t oo[32];
+        tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + 1 * 64 + set * 32 + lane_off, oo);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = fmaf(__uint_as_float(oo[e]), a1, o[e]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[ub]);
+      if (q < p.seq) {
+        const float inv = lt > 0.f ? 1.f / lt : 0.f;
+        __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + set * 32;
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) {
+          uint4 w;
+          w.x = pack_bf16(o[cc * 8 + 0] * inv, o[cc * 8 + 1] * inv);
+          w.y = pack_bf16(o[cc * 8 + 2] * inv, o[cc * 8 + 3] * inv);
+          w.z = pack_bf16(o[cc * 8 + 4] * inv, o[cc * 8 + 5] * inv);
+          w.w = pack_bf16(o[cc * 8 + 6] * inv, o[cc * 8 + 7] * inv);
+          reinterpret_cast<uint4*>(op)[cc] = w;
+        }
+        if (set == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (m + log2f(lt)) / kLog2e;
+      }
+      g += n_kv;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_free<512>(tmem);
+  }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -853,8 +1192,9 @@ struct FwdKernel {
 FwdKernel fwd_kernel() {
   static FwdKernel k = [] {
     const char* e = getenv("DPN_ATTN_FWD");
-    FwdKernel r = (e && e[0] == '2') ? FwdKernel{attn_fwd2_kernel, kFwd2Threads, kFwd2Smem}
-                                     : FwdKernel{attn_fwd_kernel, kFwdThreads, kFwdSmem};
+    FwdKernel r = (e && e[0] == '2')   ? FwdKernel{attn_fwd2_kernel, kFwd2Threads, kFwd2Smem}
+                  : (e && e[0] == '3') ? FwdKernel{attn_fwd3_kernel, kFwd3Threads, kFwd3Smem}
+                                       : FwdKernel{attn_fwd_kernel, kFwdThreads, kFwdSmem};
     cudaFuncSetAttribute(r.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, r.smem);
     return r;
   }();
