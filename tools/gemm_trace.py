@@ -30,6 +30,11 @@ cases = [  # name, M, N, K, a_mn, b_mn, f32, epilogue kwargs
     ("fc2dg resadd", 16384, 4096, 1024, 0, 1, 0, "res"),
     ("fc2dg gg-ldg", 16384, 4096, 1024, 0, 1, 0, "gelu_grad_direct"),
     ("fc1 b32 ldg", 16384, 4096, 1024, 0, 0, 0, "gelu_aux_direct"),
+    ("qkv b48", 24576, 3072, 1024, 0, 0, 0, "bias"),
+    ("proj b48", 24576, 1024, 1024, 0, 0, 0, "bias_res"),
+    ("fc2 b48", 24576, 1024, 4096, 0, 0, 0, "bias_res"),
+    ("fc1dg b48", 24576, 1024, 4096, 0, 1, 0, "acc"),
+    ("big plain", 8192, 8192, 8192, 0, 1, 0, ""),
 ]
 for name, m, n, kk, amn, bmn, f32, epi in cases:
     A = torch.randn(kk, m, device="cuda").to(bf) if amn else torch.randn(m, kk, device="cuda").to(bf)
