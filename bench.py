@@ -5,13 +5,15 @@
 
 Workload (BASELINE.json configs[1]): BERT-large (24 x 1024, 16 heads, FFN 4096,
 vocab 30522), seq 512, partitioned by this package's planner into an 8-stage
-async-1F1B DawnPiper plan, micro-batch b=48, m=32 micro-batches per step
+async-1F1B DawnPiper plan, micro-batch b=64, m=32 micro-batches per step
 (m = 4l, cli.py:226-228), bf16 compute with fp32 master weights, PipeDream
 weight stashing and a per-micro-batch AdamW update.  BASELINE.json leaves b
-open ("b swept"); swept sizes 8 / 16 / 32 / 48 gave 533 / 612 /
-705 / 726 samples/s (profiles/r01_bench_*, profiles/r02_bench_*) -- larger
-micro-batches fill the tensor cores better and amortise the per-micro-batch
-optimizer step.  At N=1 all 8 stages are
+open ("b swept"); swept sizes 8 / 16 / 32 / 48 / 64 / 74 gave
+533 / 612 / 705 / 725 / 734 / 605 samples/s (profiles/r01_bench_*,
+profiles/r02_bench_*, profiles/r02_s3/) -- larger micro-batches fill the
+tensor cores better (b=64: 128 x 4 pair tiles for the N=1024 GEMMs, 6.9 full
+waves on 74 CTA pairs vs 5.2 at b=48) and amortise the per-micro-batch
+optimizer step; b=74 runs out of headroom for the allocator.  At N=1 all 8 stages are
 co-located on one GPU; at N>1 (torchrun) the plan has l=N stages, one per GPU.
 
 A step = one pipeline iteration (m micro-batches, b*m samples, every forward,
@@ -52,7 +54,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="bert-large")
-    ap.add_argument("--micro-batch", type=int, default=48)
+    ap.add_argument("--micro-batch", type=int, default=64)
     ap.add_argument("--stages", type=int, default=0, help="default: 8 at N=1, N otherwise; "
                     "l < N at N>1 runs N/l data-parallel replicas of an l-stage pipeline")
     ap.add_argument("--micro-batches", type=int, default=32)

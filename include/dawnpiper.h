@@ -91,6 +91,9 @@ typedef struct {
   int32_t split_k; /* f32 output without bias/residual/GELU only: 0 = heuristic, 1 = off, n = n splits */
   int32_t cta_group; /* 0 = heuristic, 1 = one CTA per tile, 2 = CTA pair (tcgen05 cta_group::2, 256-row tile), 4 = two pairs sharing A by TMA multicast (block_n 256) */
   int32_t epilogue; /* 0 = TMA-staged stores when unbatched (default), 1 = direct per-thread stores */
+  float* colsum; /* optional (bf16 C, TMA-staged epilogue): colsum[n] += sum_m C[m, n] of the stored
+                    values -- the bias gradient of the linear whose output gradient C is, fused
+                    into the GEMM that produces it (replaces a dpn_colsum pass over C) */
 } dpn_gemm_args;
 int dpn_gemm(const dpn_gemm_args* args, void* stream);
 

@@ -33,6 +33,7 @@ class GemmArgs(C.Structure):
         ("split_k", _i32),
         ("cta_group", _i32),
         ("epilogue", _i32),
+        ("colsum", _vp),
     ]
 
 

@@ -11,8 +11,11 @@
 // unit's Q / K / V loads and S MMAs overlap the current unit's tail (the
 // per-unit prologue / epilogue of a one-CTA-per-unit grid dominated at
 // s = 512).  384 threads:
-//   warp 0   TMA: Q per unit (single buffer, released after the unit's last
-//            S MMA), K_j / V_j tiles into a 3-deep ring
+//   warp 0   TMA: Q per unit, double-buffered by unit parity (with one buffer
+//            the next Q could only load after the unit's last S MMA, and the
+//            MMA warp -- which issues PV(j-1) after S(j) -- held the unit's
+//            last PV, and the softmax warps' unit epilogue, for a TMA round
+//            trip), K_j / V_j tiles into a 3-deep ring
 //   warp 1   MMA issuer: S_j = Q K_j^T (M=128,N=128,K=64) into TMEM S[j%2];
 //            O_j = P_j V_j (M=128,N=64,K=128) into TMEM O[j%2]
 //   warp 2   TMEM allocator
@@ -118,13 +121,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kTileBytes;                  // [stage] 16 KB
+  uint8_t* sQ = smem;                             // [2] by unit parity: the next
+                                                  // unit's Q loads during this one
+  uint8_t* sK = sQ + 2 * kTileBytes;              // [stage] 16 KB
   uint8_t* sV = sK + kKVStages * kTileBytes;      // [stage] 16 KB
   uint8_t* sP = sV + kKVStages * kTileBytes;      // [2] 32 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
-  uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;
+  uint64_t* q_full = bars;                  // [2]
+  uint64_t* kv_full = bars + 2;
   uint64_t* kv_empty = kv_full + kKVStages;
   uint64_t* s_full = kv_empty + kKVStages;  // [2]
   uint64_t* s_empty = s_full + 2;           // [2]
@@ -132,8 +136,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint64_t* p_empty = p_full + 2;           // [2]
   uint64_t* pv_done = p_empty + 2;          // one phase per KV tile
   uint64_t* o_empty = pv_done + 1;          // [2] by unit parity
-  uint64_t* q_empty = o_empty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 1);
+  uint64_t* q_empty = o_empty + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_kv_all = (p.kv_seq + kTile - 1) / kTile;
@@ -164,8 +168,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     prefetch_tmap(&tm_kv);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
+    }
     for (int s = 0; s < kKVStages; ++s) {
       mbar_init(&kv_full[s], 1);
       mbar_init(&kv_empty[s], 1);
@@ -199,9 +205,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         int qt, h, bb;
         decode(u, qt, h, bb);
         const int n_kv = kv_tiles(qt), row0 = bb * p.seq, krow0 = bb * p.kv_seq;
-        mbar_wait(q_empty, (uc & 1) ^ 1);
-        mbar_expect_tx(q_full, kTileBytes);
-        tma_load_2d(sQ, &tm_q, q_full, p.q_col + h * kD, row0 + qt * kTile);
+        const int qb = uc & 1;
+        mbar_wait(&q_empty[qb], ((uc >> 1) & 1) ^ 1);
+        mbar_expect_tx(&q_full[qb], kTileBytes);
+        tma_load_2d(sQ + qb * kTileBytes, &tm_q, &q_full[qb], p.q_col + h * kD, row0 + qt * kTile);
         for (int j = 0; j < n_kv; ++j, ++g) {
           const int st = g % kKVStages;
           mbar_wait(&kv_empty[st], ((g / kKVStages) & 1) ^ 1);
@@ -246,14 +253,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int qt, h, bb;
       decode(u, qt, h, bb);
       const int n_kv = kv_tiles(qt);
-      mbar_wait(q_full, uc & 1);
+      const int qb = uc & 1;
+      mbar_wait(&q_full[qb], (uc >> 1) & 1);
       for (int j = 0; j < n_kv; ++j, ++g) {
         const int st = g % kKVStages, i = g & 1;
         mbar_wait(&kv_full[st], (g / kKVStages) & 1);
         mbar_wait(&s_empty[i], ((g >> 1) & 1) ^ 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
+          const uint32_t qa = smem_u32(sQ + qb * kTileBytes), kb = smem_u32(sK + st * kTileBytes);
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k) {
             const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
@@ -261,7 +269,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
           }
           umma_commit(&s_full[i]);
-          if (j == n_kv - 1) umma_commit(q_empty);  // Q is free once the unit's S MMAs ran
+          if (j == n_kv - 1) umma_commit(&q_empty[qb]);  // Q is free once the unit's S MMAs ran
         }
         __syncwarp();
         if (g >= 1) issue_pv(g - 1, prev_first, prev_ub, prev_uc);
@@ -795,15 +803,16 @@ __global__ void __maxnreg__(96)
 // (4 warps, one per TMEM lane quarter, a thread owns a query row and all 128
 // keys of a tile) takes the KV tiles t with t % 2 == k, with its own S buffer,
 // P buffer, running max / sum and O accumulator; the tensor core runs one
-// set's S / PV while the other exponentiates.  10 warps leave 200 registers
-// per thread for the 128 scores a row holds.  TMEM: S[set] 128 columns each,
-// O[unit parity][set] 64 columns each.
-constexpr int kFwd3Threads = 320;  // warp 0 TMA + TMEM, warp 1 MMA, warps 2-9 softmax
+// set's S / PV while the other exponentiates.  Three warpgroups: WG0 (warp 0
+// TMA + TMEM, warp 1 MMA) gives its registers to the two softmax warpgroups
+// (setmaxnreg 56 / 224), which hold the 128 scores of a row without spills.
+// TMEM: S[set] 128 columns each, O[unit parity][set] 64 columns each.
+constexpr int kFwd3Threads = 384;  // WG0: warp 0 TMA + TMEM, warp 1 MMA; WG1 / WG2: softmax sets
 constexpr int kFwd3Bars = 2 + 2 * kKV2Stages + 4 * 2 + 2;
 constexpr int kFwd3Smem = 1024 + kTileBytes * (1 + 2 * kKV2Stages) + 2 * kPBytes + kFwd3Bars * 8 + 16 +
                           2 * 128 * 2 * 2 * 4;
 
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kFwd3Threads, 1)
     attn_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                      const AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -881,6 +890,7 @@ __global__ void __maxnreg__(200)
   pdl_wait();
 
   if (warp == 0) {
+    regs_dec<56>();
     if (lane == 0) {
       long long g = 0;
       int uc = 0;
@@ -901,6 +911,7 @@ __global__ void __maxnreg__(200)
       }
     }
   } else if (warp == 1) {
+    regs_dec<56>();
     constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
     constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);
     struct Pending {
@@ -971,9 +982,10 @@ __global__ void __maxnreg__(200)
     }
     if (npend >= 1) issue_pv(pa);
     if (npend == 2) issue_pv(pb);
-  } else {
-    // ---------------- softmax: warps 2-9, set = (warp - 2) / 4 ----------------
-    const int set = (warp - 2) >> 2;
+  } else if (warp >= 4) {
+    // ---------------- softmax: warps 4-11, set = (warp - 4) / 4 ----------------
+    regs_inc<224>();
+    const int set = (warp - 4) >> 2;
     const int quarter = warp & 3;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
@@ -1120,6 +1132,8 @@ __global__ void __maxnreg__(200)
       }
       g += n_kv;
     }
+  } else {
+    regs_dec<56>();
   }
   tc_fence_before();
   __syncthreads();
@@ -1181,7 +1195,7 @@ int map_2d_f32(CUtensorMap* map, const void* ptr, long long rows, long long cols
 }
 
 // + 256 B of barriers / TMEM slot, then the per-unit (m, l) exchange [2][128][2][2] f32
-constexpr int kFwdSmem = 1024 + kTileBytes * (1 + 2 * kKVStages) + 2 * kPBytes + 256 + 1024 * 4;
+constexpr int kFwdSmem = 1024 + kTileBytes * (2 + 2 * kKVStages) + 2 * kPBytes + 256 + 1024 * 4;
 
 // Forward kernel choice: the single-set kernel unless DPN_ATTN_FWD=2 (the
 // two-set kernel, under validation; tools/attn_micro.py A/B).

@@ -61,6 +61,7 @@ struct GemmParams {
   float alpha;
   int gelu;
   long long* trace;  // debug: per-CTA wait cycles by role (dpn_gemm_debug_trace), else null
+  float* colsum;     // optional: colsum[n] += sum over rows of the stored bf16 C (bias gradient)
 };
 
 // timed mbarrier wait (debug tracing only)
@@ -79,6 +80,16 @@ __device__ __forceinline__ void mbar_wait_t(uint64_t* bar, uint32_t parity, long
 constexpr int kEpiStage = 4096;
 constexpr int kEpiBytes = kEpiWarps * 2 * kEpiStage;
 constexpr int kMaxSmem = 232448;  // 227 KB per CTA on sm_100
+// build-time knobs for same-box A/B experiments (tools/build_variant.sh)
+#ifndef DPN_GEMM_MAX_STAGES
+#define DPN_GEMM_MAX_STAGES 8
+#endif
+#ifndef DPN_GEMM_GROUP
+#define DPN_GEMM_GROUP 8
+#endif
+#ifndef DPN_GEMM_L2_PROMO
+#define DPN_GEMM_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
 
 // CG: CTAs per cluster. 1 = one CTA per tile; 2 = a CTA pair on one 256-row
 // tile (tcgen05 cta_group::2); 4 = two pairs on N-adjacent tiles sharing their
@@ -91,7 +102,7 @@ struct Cfg {
   static constexpr int kBBytes = kBRows * BK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kFit = (kMaxSmem - kEpiBytes - 2048) / kStageBytes;
-  static constexpr int kStages = kFit < 8 ? kFit : 8;
+  static constexpr int kStages = kFit < DPN_GEMM_MAX_STAGES ? kFit : DPN_GEMM_MAX_STAGES;
   static constexpr int kTmemCols = 2 * BN;  // two accumulator buffers
   static constexpr int kSmem = kStages * kStageBytes + kEpiBytes + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(kSmem <= kMaxSmem, "shared memory budget");
@@ -147,7 +158,7 @@ __device__ __forceinline__ Unit decode(const GemmParams& p, long long u, int nk)
   const int z = (int)(t / per_z);
   const int r = (int)(t - (long long)z * per_z);
   // grouped raster: 8 m-blocks sweep all n-blocks together (L2 reuse of B)
-  const int G = 8;
+  const int G = DPN_GEMM_GROUP;
   const int per_group = G * p.tiles_n;
   const int g = r / per_group;
   const int first_m = g * G;
@@ -160,6 +171,10 @@ __device__ __forceinline__ Unit decode(const GemmParams& p, long long u, int nk)
   w.kb0 = split * p.kb_per_split;
   w.kb1 = min(nk, w.kb0 + p.kb_per_split);
   return w;
+}
+
+__device__ __forceinline__ void red_add_v2(float* addr, float a, float b) {
+  asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(addr), "f"(a), "f"(b) : "memory");
 }
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -434,6 +449,26 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       tma_store_2d(tmC, s_out, col0, row_base);
       if (aux) tma_store_2d(tmX, s_side, col0, row_base);
       bulk_commit();
+    }
+    if (p.colsum) {
+      // column sums of the stored tile (the bias gradient of the linear whose
+      // output gradient C is): lane l adds columns 2l, 2l+1 over the warp's 32
+      // rows, read back from the swizzled staging tile (one 128-byte row per
+      // load: conflict-free); the next chunk's writes wait on the __syncwarp above
+      const int nr = min(32, p.M - row_base);
+      float2 cs = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        if (r < nr) {
+          const uint32_t u = *reinterpret_cast<const uint32_t*>(s_out + swz128(r, lane >> 2) + (lane & 3) * 4);
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
+          cs.x += f.x;
+          cs.y += f.y;
+        }
+      }
+      const int cc = col0 + 2 * lane;
+      if (cc + 1 < p.N) red_add_v2(p.colsum + cc, cs.x, cs.y);
+      else if (cc < p.N) atomicAdd(p.colsum + cc, cs.x);
     }
   }
 }
@@ -823,7 +858,7 @@ int encode_map(CUtensorMap* map, const void* ptr, long long inner, long long out
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                   DPN_GEMM_L2_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   DPN_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
   return 0;
 }
@@ -862,6 +897,8 @@ int launch(const dpn_gemm_args* g, const GemmParams& p0, cudaStream_t stream) {
   // the side staging tile holds either the residual or the aux output, not both
   p.tma_epi = g->batch1 * g->batch2 == 1 && (!p.res || (al16(p.res) && p.ldr % 8 == 0)) &&
               (!p.aux || al16(p.aux)) && !(p.res && p.aux && p.gelu) && g->epilogue != 1;
+  DPN_REQUIRE(!p.colsum || (p.tma_epi && !p.c_f32),
+              "colsum needs a bf16 output on the TMA-staged epilogue (unbatched, aligned operands)");
   if (p.tma_epi) {
     rc = make_epi_map(&tc, g->C, g->M, g->N, g->ldc, p.c_f32 != 0);
     if (!rc && p.res) rc = make_epi_map(&tr, p.res, g->M, g->N, p.ldr, false);
@@ -1030,6 +1067,8 @@ extern "C" int dpn_gemm(const dpn_gemm_args* g, void* stream_) {
   p.alpha = g->alpha;
   p.gelu = g->gelu;
   p.trace = g_gemm_trace;
+  p.colsum = g->colsum;
+  DPN_REQUIRE(!g->colsum || (reinterpret_cast<uintptr_t>(g->colsum) & 7) == 0, "colsum must be 8-byte aligned");
   cudaStream_t s = static_cast<cudaStream_t>(stream_);
   int bn = 0, cg = 1;
   pick_config(g->M, g->N, g->K, p.Z, bn, cg);

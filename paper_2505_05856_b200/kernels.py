@@ -97,8 +97,10 @@ def _s(stream) -> Optional[int]:
 def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batch1=1, batch2=1,
              a_s=(0, 0), b_s=(0, 0), c_s=(0, 0), bias=None, residual=None, ldr=None, r_s=None,
              aux=None, alpha=1.0, gelu=False, accumulate=False, block_n=0, split_k=0,
-             cta_group=0, residual_mode=0, epilogue=0, stream=None) -> None:
-    """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules."""
+             cta_group=0, residual_mode=0, epilogue=0, colsum=None, stream=None) -> None:
+    """C[z] = epi(alpha * A[z] B[z]^T); see include/dawnpiper.h for the layout rules.
+    colsum: optional f32 [N]: += the column sums of the stored bf16 C (fused bias gradient)."""
+    assert colsum is None or colsum.dtype == F32
     rs = (r_s if r_s is not None else c_s) if residual is not None else (0, 0)
     g = GemmArgs(M, N, K, batch1, batch2,
                  A.data_ptr(), lda, a_s[0], a_s[1], a_mn,
@@ -108,7 +110,7 @@ def gemm_raw(*, M, N, K, A, lda, B, ldb, Cout, ldc, a_mn=False, b_mn=False, batc
                  None if residual is None else residual.data_ptr(),
                  (ldr if ldr is not None else ldc) if residual is not None else 0, rs[0], rs[1],
                  residual_mode, None if aux is None else aux.data_ptr(), alpha, gelu, block_n,
-                 split_k, cta_group, epilogue)
+                 split_k, cta_group, epilogue, None if colsum is None else colsum.data_ptr())
     INSTR.launches += 1
     INSTR.gemm_flops += 2 * int(M) * int(N) * int(K) * int(batch1) * int(batch2)
     ev = INSTR.gemm_events
@@ -137,17 +139,19 @@ def linear_fwd(x, w, out, bias=None, residual=None, gelu=False, aux=None, stream
              stream=stream)
 
 
-def linear_dgrad(dy, w, dx, accumulate_into=None, gelu_of=None, stream=None):
+def linear_dgrad(dy, w, dx, accumulate_into=None, gelu_of=None, dbias=None, stream=None):
     """dx[M, K] = dy[M, N] @ w[N, K]  (w used MN-major: no transpose copy).
     accumulate_into: a bf16 [M, K] tensor added to the result (may be dx);
-    gelu_of: pre-activation f [M, K]: dx *= gelu'(f) (fused GELU backward)."""
+    gelu_of: pre-activation f [M, K]: dx *= gelu'(f) (fused GELU backward);
+    dbias: f32 [K]: += column sums of the stored dx (the bias gradient of the
+    linear that produced f, fused into this epilogue)."""
     M, N = dy.shape
     K = w.shape[1]
     assert accumulate_into is None or gelu_of is None
     res = accumulate_into if gelu_of is None else gelu_of
     gemm_raw(M=M, N=K, K=N, A=dy, lda=dy.stride(0), B=w, ldb=w.stride(0), b_mn=True, Cout=dx,
              ldc=dx.stride(0), residual=res, ldr=None if res is None else res.stride(0),
-             residual_mode=0 if gelu_of is None else 1, stream=stream)
+             residual_mode=0 if gelu_of is None else 1, colsum=dbias, stream=stream)
 
 
 def linear_wgrad(dy, x, dw, accumulate=False, stream=None):

@@ -315,6 +315,15 @@ class StageExecutor:
                 users = [c for c in self.nodes if n.id in c.inputs]
                 if len(users) == 1 and users[0].kind == "linear":
                     self.bwd_gelu_of[users[0].id] = n.id
+        # fc1's bias gradient folded into fc2's dgrad epilogue (dpn_gemm colsum):
+        # df written there is fc1's complete output gradient when the GELU is the
+        # only reader of fc1's output anywhere in the graph
+        self.gelu_bias_of: Dict[str, str] = {}  # fc2 id -> fc1 id
+        for fc2_id, g_id in self.bwd_gelu_of.items():
+            src = self.node_by_id[g_id].inputs[0]
+            if (src in in_stage and self.node_by_id[src].kind == "linear"
+                    and [c.id for c in self.all_nodes if src in c.inputs] == [g_id]):
+                self.gelu_bias_of[fc2_id] = src
         self._skip_bwd: Set[str] = set()
         # bias gradient of a linear node folded into the one-pass LayerNorm
         # backward of the LN reading that node's output (or, through the
@@ -1088,7 +1097,14 @@ class StageExecutor:
                 # lands in f's gradient; the gelu node's own backward is skipped
                 f_t = out_tid(self.node_by_id[g_id].inputs[0])
                 df = self.grad_buffer(f_t)
-                K.linear_dgrad(dy, W("weight"), df, gelu_of=self.buf(f_t, slot, "bwd"), stream=st)
+                fc1 = self.gelu_bias_of.get(n.id)
+                dbias = P.gradv(f"{fc1}.bias") if fc1 is not None else None
+                if dbias is not None and dbias.data_ptr() % 8:
+                    dbias = None  # the fused column sums need an 8-byte aligned f32 target
+                K.linear_dgrad(dy, W("weight"), df, gelu_of=self.buf(f_t, slot, "bwd"), dbias=dbias,
+                               stream=st)
+                if dbias is not None:
+                    self._bias_done.add(fc1)
                 self.grad_init.add(f_t)
                 self._skip_bwd.add(g_id)
             elif x_t in self.grad_init:

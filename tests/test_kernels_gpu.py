@@ -385,6 +385,30 @@ def test_gemm_fused_gelu_backward():
     close(dx, fr.grad)
 
 
+@pytest.mark.parametrize("M,N,Kd", [(512, 768, 256), (300, 520, 200), (4096, 4096, 1024)])
+def test_gemm_fused_colsum(M, N, Kd):
+    """colsum epilogue: the column sums of the stored bf16 dx are added to an f32
+    accumulator (fc1's bias gradient fused into fc2's dgrad), with ragged M / N."""
+    k = K()
+    dy, w, f = rnd(M, Kd), rnd(Kd, N, scale=0.05), rnd(M, N)
+    dx = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    db = torch.randn(N, device="cuda")
+    db0 = db.clone()
+    k.linear_dgrad(dy, w, dx, gelu_of=f, dbias=db)
+    torch.cuda.synchronize()
+    close(db - db0, dx.float().sum(0), rel=5e-3)  # sums of the stored values
+    fr = f.float().requires_grad_()
+    torch.nn.functional.gelu(fr, approximate="tanh").backward(dy.float() @ w.float())
+    close(db - db0, fr.grad.sum(0))
+    # plain bf16 GEMM with bias + colsum (no residual)
+    x, wt, b = rnd(M, Kd), rnd(N, Kd, scale=0.05), rnd(N)
+    y = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    cs = torch.zeros(N, device="cuda")
+    k.gemm_raw(M=M, N=N, K=Kd, A=x, lda=Kd, B=wt, ldb=Kd, Cout=y, ldc=N, bias=b, colsum=cs)
+    torch.cuda.synchronize()
+    close(cs, y.float().sum(0), rel=5e-3)
+
+
 def _attn_ref(qkv, b, s, A, causal):
     H = A * 64
     q = qkv[:, :H].float().reshape(b, s, A, 64).transpose(1, 2)

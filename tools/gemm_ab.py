@@ -28,9 +28,9 @@ def graph_time(fn, reps=20):
     return e0.elapsed_time(e1) / reps * 1e-3
 
 
-M = 16384
+M = int(__import__("os").environ.get("GEMM_AB_M", "24576"))
 row = {"so": str(_lib.SO_PATH.name)}
-for name, N, K in (("qkv", 3072, 1024), ("fc1", 4096, 1024), ("fc2", 1024, 4096), ("big", 8192, 8192)):
+for name, N, K in (("qkv", 3072, 1024), ("proj", 1024, 1024), ("fc1", 4096, 1024), ("fc2", 1024, 4096), ("big", 8192, 8192)):
     m = M if name != "big" else 8192
     x = torch.randn(m, K, device="cuda").bfloat16()
     w = torch.randn(N, K, device="cuda").bfloat16()
@@ -46,6 +46,8 @@ for name, N, K in (("qkv", 3072, 1024), ("fc1", 4096, 1024), ("fc2", 1024, 4096)
         row[f"{name}_gelu_aux"] = round(fl / graph_time(lambda: k.linear_fwd(x, w, y, bias=bias, gelu=True, aux=aux)) / 1e12)
     if name == "fc2":
         row[f"{name}_res"] = round(fl / graph_time(lambda: k.linear_fwd(x, w, y, bias=bias, residual=res)) / 1e12)
-    row[f"{name}_wgrad"] = round(fl / graph_time(lambda: k.linear_wgrad(dy, x, dw)) / 1e12)
-    row[f"{name}_cublas"] = round(fl / graph_time(lambda: torch.matmul(x, w.t(), out=y)) / 1e12)
+    if name in ("fc1", "qkv"):
+        row[f"{name}_wgrad"] = round(fl / graph_time(lambda: k.linear_wgrad(dy, x, dw)) / 1e12)
+    if name in ("fc2", "big"):
+        row[f"{name}_cublas"] = round(fl / graph_time(lambda: torch.matmul(x, w.t(), out=y)) / 1e12)
 print(json.dumps(row), flush=True)
