@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           w.y = pack_bf16(e8[2], e8[3]);
           w.z = pack_bf16(e8[4], e8[5]);
           w.w = pack_bf16(e8[6], e8[7]);
-          *reinterpret_cast<uint4*>(pt + sw128(r, c)) = w;
+          sts128(smem_u32(pt) + sw128(r, c), w);
         }
         l = l * alpha + (sum2.x + sum2.y);
         fence_async_smem();
@@ -710,7 +710,7 @@ __global__ void __maxnreg__(96)
           w.y = pack_bf16(e8[2], e8[3]);
           w.z = pack_bf16(e8[4], e8[5]);
           w.w = pack_bf16(e8[6], e8[7]);
-          *reinterpret_cast<uint4*>(pt + sw128(r, c)) = w;
+          sts128(smem_u32(pt) + sw128(r, c), w);
         }
         l = l * alpha + (sum2.x + sum2.y);
         fence_async_smem();
@@ -1058,7 +1058,7 @@ __global__ void __launch_bounds__(kFwd3Threads, 1)
           w.y = pack_bf16(e8[2], e8[3]);
           w.z = pack_bf16(e8[4], e8[5]);
           w.w = pack_bf16(e8[6], e8[7]);
-          *reinterpret_cast<uint4*>(pt + (c >> 3) * (kPBytes / 2) + sw128(r, c & 7)) = w;
+          sts128(smem_u32(pt) + (c >> 3) * (kPBytes / 2) + sw128(r, c & 7), w);
         }
         l = l * alpha + (sum2.x + sum2.y);
         fence_async_smem();
@@ -1533,7 +1533,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             b2.y = pack_bf16(dsv[2], dsv[3]);
             b2.z = pack_bf16(dsv[4], dsv[5]);
             b2.w = pack_bf16(dsv[6], dsv[7]);
-            *reinterpret_cast<uint4*>(tdS + half * (kPBytes / 2) + sw128(r, c)) = b2;
+            sts128(smem_u32(tdS) + half * (kPBytes / 2) + sw128(r, c), b2);
           }
         };
         if (mask) tile(std::true_type{});
@@ -1541,7 +1541,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(p_empty, (G & 1) ^ 1);
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(sP + half * (kPBytes / 2) + sw128(r, c)) = pk[c];
+          sts128(smem_u32(sP) + half * (kPBytes / 2) + sw128(r, c), pk[c]);
         fence_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&ds_full[pb]);
@@ -1578,9 +1578,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            *reinterpret_cast<uint4*>(sdQ + hh * (kPBytes / 2) + sw128(r, c)) =
-                make_uint4(uq[hh * 32 + c * 4], uq[hh * 32 + c * 4 + 1], uq[hh * 32 + c * 4 + 2],
-                           uq[hh * 32 + c * 4 + 3]);
+            sts128(smem_u32(sdQ) + hh * (kPBytes / 2) + sw128(r, c),
+                   make_uint4(uq[hh * 32 + c * 4], uq[hh * 32 + c * 4 + 1], uq[hh * 32 + c * 4 + 2],
+                           uq[hh * 32 + c * 4 + 3]));
         fence_async_smem();
         asm volatile("bar.sync 6, 128;" ::: "memory");
         if (issuer) {

@@ -336,7 +336,8 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       for (int q = 0; q < 8; ++q) {
         float4 o = make_float4(__uint_as_float(r[4 * q]) * p.alpha, __uint_as_float(r[4 * q + 1]) * p.alpha,
                                __uint_as_float(r[4 * q + 2]) * p.alpha, __uint_as_float(r[4 * q + 3]) * p.alpha);
-        *reinterpret_cast<float4*>(s_out + swz128(lane, q)) = o;
+        sts128(smem_u32(s_out) + swz128(lane, q),
+               make_uint4(__float_as_uint(o.x), __float_as_uint(o.y), __float_as_uint(o.z), __float_as_uint(o.w)));
       }
       epi_fence_async();
       __syncwarp();
@@ -394,7 +395,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       rphase ^= 1;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const uint4 u = *reinterpret_cast<const uint4*>(s_side + swz128(lane, q));
+        const uint4 u = lds128(smem_u32(s_side) + swz128(lane, q));
         const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -423,7 +424,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
         u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
         u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-        *reinterpret_cast<uint4*>(s_side + swz128(lane, q)) = u;
+        sts128(smem_u32(s_side) + swz128(lane, q), u);
       }
     }
     if (p.gelu) {
@@ -441,7 +442,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
       u.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
       u.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
       u.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-      *reinterpret_cast<uint4*>(s_out + swz128(lane, q)) = u;
+      sts128(smem_u32(s_out) + swz128(lane, q), u);
     }
     epi_fence_async();
     __syncwarp();
@@ -460,7 +461,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         if (r < nr) {
-          const uint32_t u = *reinterpret_cast<const uint32_t*>(s_out + swz128(r, lane >> 2) + (lane & 3) * 4);
+          const uint32_t u = lds32(smem_u32(s_out) + swz128(r, lane >> 2) + (lane & 3) * 4);
           const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u));
           cs.x += f.x;
           cs.y += f.y;

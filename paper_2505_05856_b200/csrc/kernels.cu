@@ -64,19 +64,36 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
-  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
-       r += (long long)gridDim.x * warps) {
-    const __nv_bfloat16* xr = x + r * cols;
+  const long long stride = (long long)gridDim.x * warps;
+  // the next row's x is in flight while this one is normalised (one row of
+  // loads per warp did not cover HBM latency); gamma / beta come from L1
+  uint4 xr[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) xr[j] = make_uint4(0, 0, 0, 0);
+  long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5);
+  if (r < rows) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) xr[j] = *reinterpret_cast<const uint4*>(x + r * cols + c * 8);
+    }
+  }
+  for (; r < rows; r += stride) {
+    const long long rn = r + stride;
+    uint4 xn[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int c = lane + 32 * j;
+      xn[j] = make_uint4(0, 0, 0, 0);
+      if (c < nvec && rn < rows) xn[j] = *reinterpret_cast<const uint4*>(x + rn * cols + c * 8);
+    }
     float v[NV][8];
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int c = lane + 32 * j;
-      if (c < nvec) {
-        load8(xr + c * 8, v[j]);
+      load8(reinterpret_cast<const __nv_bfloat16*>(&xr[j]), v[j]);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) s += v[j][i];
-      }
+      for (int i = 0; i < 8; ++i) s += v[j][i];  // zero-filled past cols
     }
     const float mu = warp_sum(s) / cols;
     float q = 0.f;
@@ -108,6 +125,8 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
       mean_out[r] = mu;
       rstd_out[r] = rs;
     }
+#pragma unroll
+    for (int j = 0; j < NV; ++j) xr[j] = xn[j];
   }
 }
 
@@ -199,9 +218,15 @@ __device__ __forceinline__ void red_add_v4(float* addr, const float* v) {
 // flight per iteration.  The CTA's column partials combine across groups in
 // shared memory and go out with one vector red per 4 columns.
 //   bytes: read dy, x (, dx_add), write dx  (+ 8 B of stats per row)
-constexpr int kLnThreads = 256;  // two CTAs per SM: their load / reduce / store phases interleave
-constexpr int kLnRows = 3;
-__global__ void __launch_bounds__(kLnThreads, 2) ln_bwd_fused_kernel(
+#ifndef DPN_LN_ROWS
+#define DPN_LN_ROWS 3
+#endif
+#ifndef DPN_LN_CTAS
+#define DPN_LN_CTAS 2
+#endif
+constexpr int kLnThreads = 256;  // DPN_LN_CTAS CTAs per SM: their load / reduce / store phases interleave
+constexpr int kLnRows = DPN_LN_ROWS;
+__global__ void __launch_bounds__(kLnThreads, DPN_LN_CTAS) ln_bwd_fused_kernel(
     const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
     const __nv_bfloat16* __restrict__ gamma, const float* __restrict__ mean,
     const float* __restrict__ rstd, __nv_bfloat16* dx, const __nv_bfloat16* dx_add,
@@ -840,9 +865,10 @@ extern "C" int dpn_layernorm_bwd_fused(const void* dy, const void* x, const void
   const int nvec = (int)(cols / 8);
   const int G = (nvec + 31) / 32;
   const int groups = (kLnThreads / 32) / G;
-  // two CTAs per SM (persistent over bands of rows), at least kLnRows * groups rows each
+  // DPN_LN_CTAS CTAs per SM (persistent over bands of rows), at least kLnRows * groups rows each
   const long long per_iter = (long long)groups * kLnRows;
-  long long per = (rows + 295) / 296;
+  const long long ctas = 148LL * DPN_LN_CTAS;
+  long long per = (rows + ctas - 1) / ctas;
   per = std::max<long long>(per_iter, (per + per_iter - 1) / per_iter * per_iter);
   const unsigned grid = (unsigned)((rows + per - 1) / per);
   const size_t smem = (2 * (kLnThreads / 32) * kLnRows * 2 + (size_t)groups * cols) * sizeof(float);
