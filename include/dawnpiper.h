@@ -107,7 +107,10 @@ int dpn_attn_fwd(const void* qkv, void* out, float* lse, int64_t batch, int64_t 
  * the forward's lse.  workspace: >= batch*seq*heads*64 + batch*heads*seq floats. */
 int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
                  float* workspace, int64_t workspace_floats, int64_t batch, int64_t seq,
-                 int64_t heads, int64_t head_dim, float scale, int causal, void* stream);
+                 int64_t heads, int64_t head_dim, float scale, int causal, float* dbias, void* stream);
+/* dbias (optional, 16-byte aligned f32 [3H]): += the column sums of dQ | dK | dV --
+ * the fused QKV projection's bias gradient, accumulated by the dQ store and the
+ * dK / dV drain (replaces a dpn_colsum pass over dqkv). */
 
 /* Cross-attention (T5 decoder): q [batch*q_seq, heads*64], kv [batch*kv_seq,
  * 2*heads*64] (K | V column blocks), out [batch*q_seq, heads*64], lse [batch,

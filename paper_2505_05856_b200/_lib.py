@@ -56,7 +56,7 @@ SIGNATURES = {
     "dpn_enable_peer": [C.c_int, C.c_int],
     "dpn_gemm": [C.POINTER(GemmArgs), _vp],
     "dpn_attn_fwd": [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _f32, C.c_int, _vp],
-    "dpn_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, C.c_int, _vp],
+    "dpn_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, C.c_int, _vp, _vp],
     "dpn_attn_fwd_cross": [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _f32, _vp],
     "dpn_attn_bwd_cross": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64,
                            _f32, _vp],

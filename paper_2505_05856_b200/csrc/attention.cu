@@ -1219,7 +1219,9 @@ FwdKernel fwd_kernel() {
 
 // ---------------------------------------------------------------------------
 // Backward: persistent, one CTA per SM walking units (batch, head, 128-key
-// tile) -- K_j, V_j stay in smem while the CTA walks the query tiles i
+// tile) -- K_j, V_j stay in smem while the CTA walks the query tiles i (K
+// double-buffered by unit parity and V released after the unit's last dP MMA,
+// so the next unit's K / V load under this one instead of after it)
 // (causal: i >= j); barrier phases run on CTA-global counters, the dV / dK
 // drain of a unit runs on the dQ warpgroup while the softmax warps start the
 // next unit:
@@ -1258,6 +1260,8 @@ struct AttnBwdParams {
   const float* D;    // [b, heads, s]
   float* dq;         // [b*s, H] f32 accumulator (zeroed)
   __nv_bfloat16* dqkv;  // [b*s, 3H]
+  float* dbias_k;       // optional: += column sums of dK / dV (head 0's column 0), the
+  float* dbias_v;       // fused QKV projection's bias gradient
 };
 
 
@@ -1269,16 +1273,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sK = smem;
-  uint8_t* sV = sK + kTileBytes;
+  uint8_t* sK = smem;                     // [2] by unit parity: the next unit's K loads
+                                          // during this one
+  uint8_t* sV = sK + 2 * kTileBytes;      // released after the unit's last dP MMA
   uint8_t* sQ = sV + kTileBytes;          // [2]
   uint8_t* sdO = sQ + 2 * kTileBytes;     // [2]
   uint8_t* sP = sdO + 2 * kTileBytes;     // 32 KB
   uint8_t* sdS = sP + kPBytes;            // [2] 32 KB
-  uint8_t* sdQ = sdS + 2 * kPBytes;       // 32 KB f32 staging: two [128][32] SW128 boxes
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sdQ + kPBytes);
-  uint64_t* kv_full = bars;
-  uint64_t* q_full = bars + 1;    // [2]
+  uint8_t* sdQ = sdS + 2 * kPBytes;       // 16 KB f32 staging: one [128][32] SW128 box
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sdQ + kPBytes / 2);
+  uint64_t* k_full = bars;        // [2]
+  uint64_t* v_full = bars + 2;
+  uint64_t* q_full = bars + 3;    // [2]
   uint64_t* q_empty = q_full + 2; // [2]
   uint64_t* sp_full = q_empty + 2;
   uint64_t* sp_loaded = sp_full + 1;
@@ -1288,8 +1294,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint64_t* dq_full = ds_empty + 2;  // [2] (dQ is double-buffered in TMEM)
   uint64_t* dq_empty = dq_full + 2;  // [2]
   uint64_t* dkv_full = dq_empty + 2;
-  uint64_t* kv_empty = dkv_full + 1;   // K/V smem free for the next unit
-  uint64_t* dkv_empty = kv_empty + 1;  // dV/dK TMEM drained
+  uint64_t* k_empty = dkv_full + 1;    // [2] K smem free for the unit after next
+  uint64_t* v_empty = k_empty + 2;     // V smem free (the unit's dP MMAs ran)
+  uint64_t* dkv_empty = v_empty + 1;   // dV/dK TMEM drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dkv_empty + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1332,8 +1339,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     prefetch_tmap(&tm_dq);
   }
   if (warp == 1 && lane == 0) {
-    mbar_init(kv_full, 1);
-    mbar_init(kv_empty, 1);
+    mbar_init(&k_full[0], 1);
+    mbar_init(&k_full[1], 1);
+    mbar_init(&k_empty[0], 1);
+    mbar_init(&k_empty[1], 1);
+    mbar_init(v_full, 1);
+    mbar_init(v_empty, 1);
     mbar_init(sp_loaded, 8);
     mbar_init(p_empty, 1);
     for (int s = 0; s < 2; ++s) {
@@ -1365,10 +1376,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int G = 0, uc = 0;
       for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
         const Unit w = decode(u);
-        mbar_wait(kv_empty, (uc & 1) ^ 1);
-        mbar_expect_tx(kv_full, 2 * kTileBytes);
-        tma_load_2d(sK, &tm_kv, kv_full, p.k_col + w.h * kD, w.krow0 + w.k0);
-        tma_load_2d(sV, &tm_kv, kv_full, p.v_col + w.h * kD, w.krow0 + w.k0);
+        const int kb = uc & 1;
+        mbar_wait(&k_empty[kb], ((uc >> 1) & 1) ^ 1);
+        mbar_expect_tx(&k_full[kb], kTileBytes);
+        tma_load_2d(sK + kb * kTileBytes, &tm_kv, &k_full[kb], p.k_col + w.h * kD, w.krow0 + w.k0);
+        mbar_wait(v_empty, (uc & 1) ^ 1);
+        mbar_expect_tx(v_full, kTileBytes);
+        tma_load_2d(sV, &tm_kv, v_full, p.v_col + w.h * kD, w.krow0 + w.k0);
         for (int it = 0; it < w.n_it; ++it, ++G) {
           const int st = G & 1, i = w.i0 + it;
           mbar_wait(&q_empty[st], ((G >> 1) & 1) ^ 1);
@@ -1381,13 +1395,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t id_s = idesc_bf16(128, 128, 0, 0);   // S, dP
       constexpr uint32_t id_kv = idesc_bf16(128, 64, 1, 1);   // dV, dK: A^T and B MN-major
       constexpr uint32_t id_q = idesc_bf16(128, 64, 0, 1);    // dQ: dS K-major, K_j MN-major
-      auto issue_sdp = [&](int G) {
+      // S / dP of query iteration G against K[kbuf]; `last`: the unit's last use of V
+      auto issue_sdp = [&](int G, int kbuf, bool last) {
         const int st = G & 1;
         mbar_wait(&q_full[st], (G >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
-          const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+          const uint32_t kb = smem_u32(sK + kbuf * kTileBytes), vb = smem_u32(sV);
 #pragma unroll
           for (int k = 0; k < kD / 16; ++k)
             umma_bf16(tmem, smem_desc_sw128(qa + k * 32, 16, 1024),
@@ -1397,25 +1412,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             umma_bf16(tmem + 128, smem_desc_sw128(doa + k * 32, 16, 1024),
                       smem_desc_sw128(vb + k * 32, 16, 1024), id_s, k > 0 ? 1u : 0u);
           umma_commit(sp_full);
+          if (last) umma_commit(v_empty);  // the next unit's V may load now
         }
         __syncwarp();
       };
       int G = 0, uc = 0;
       for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
         const Unit w = decode(u);
-        mbar_wait(kv_full, uc & 1);
-        issue_sdp(G);
+        const int kbuf = uc & 1;
+        mbar_wait(&k_full[kbuf], (uc >> 1) & 1);
+        mbar_wait(v_full, uc & 1);
+        issue_sdp(G, kbuf, w.n_it == 1);
         // the previous unit's dV / dK must have been drained before this unit's first
         mbar_wait(dkv_empty, (uc & 1) ^ 1);
         for (int it = 0; it < w.n_it; ++it, ++G) {
           const int st = G & 1, b = G & 1;
           mbar_wait(sp_loaded, G & 1);  // softmax holds S/dP(G) in registers
-          if (it + 1 < w.n_it) issue_sdp(G + 1);
+          if (it + 1 < w.n_it) issue_sdp(G + 1, kbuf, it + 2 == w.n_it);
           mbar_wait(&ds_full[b], (G >> 1) & 1);
           tc_fence_after();
           const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS + b * kPBytes);
           const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
-          const uint32_t kb = smem_u32(sK);
+          const uint32_t kb = smem_u32(sK + kbuf * kTileBytes);
           if (lane == 0) {
             // dV += P^T dO (K = queries: P read MN-major, two 64-key atoms 16 KB apart)
 #pragma unroll
@@ -1449,7 +1467,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         if (lane == 0) {
           umma_commit(dkv_full);
-          umma_commit(kv_empty);  // every MMA reading K / V of this unit has run
+          umma_commit(&k_empty[kbuf]);  // every MMA reading this unit's K has run
         }
         __syncwarp();
       }
@@ -1571,29 +1589,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&dq_empty[b]);
-        // the previous reduce must have finished reading the staging tile
-        if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        asm volatile("bar.sync 6, 128;" ::: "memory");
+        // one 32-column half at a time through the 16 KB staging box: the previous
+        // reduce must have finished reading it before it is rewritten
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
+        for (int hh = 0; hh < 2; ++hh) {
+          if (issuer) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          asm volatile("bar.sync 6, 128;" ::: "memory");
 #pragma unroll
           for (int c = 0; c < 8; ++c)
-            sts128(smem_u32(sdQ) + hh * (kPBytes / 2) + sw128(r, c),
+            sts128(smem_u32(sdQ) + sw128(r, c),
                    make_uint4(uq[hh * 32 + c * 4], uq[hh * 32 + c * 4 + 1], uq[hh * 32 + c * 4 + 2],
-                           uq[hh * 32 + c * 4 + 3]));
-        fence_async_smem();
-        asm volatile("bar.sync 6, 128;" ::: "memory");
-        if (issuer) {
-          // rows past seq carry zero (P = dS = 0 there), rows past the tensor are clipped
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh)
+                              uq[hh * 32 + c * 4 + 3]));
+          fence_async_smem();
+          asm volatile("bar.sync 6, 128;" ::: "memory");
+          if (issuer) {
+            // rows past seq carry zero (P = dS = 0 there), rows past the tensor are clipped
             asm volatile(
                 "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
                 " [%0, {%2, %3}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&tm_dq)),
-                "r"(smem_u32(sdQ + hh * (kPBytes / 2))), "r"(w.h * kD + hh * 32),
-                "r"(w.row0 + (w.i0 + it) * kTile)
+                "r"(smem_u32(sdQ)), "r"(w.h * kD + hh * 32), "r"(w.row0 + (w.i0 + it) * kTile)
                 : "memory");
-          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
         }
       }
       // dV, dK of this key tile (TMEM lane = key row), 32 columns at a time
@@ -1605,6 +1622,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         uint32_t uv[32];
         tmem_ld_32x32b_x32(tmem + 256 + part * 32 + lane_off, uv);
         tmem_ld_wait();
+        if (p.dbias_k) {
+          // column sums over this warp's 32 key rows: butterfly reduce-scatter,
+          // lane i ends with column i of the part (runs once per unit)
+          float cs[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) cs[c] = key < p.kv_seq ? __uint_as_float(uv[c]) : 0.f;
+#pragma unroll
+          for (int wdt = 16; wdt >= 1; wdt >>= 1) {
+            const bool upper = lane & wdt;
+#pragma unroll
+            for (int c = 0; c < wdt; ++c) {
+              const float send = upper ? cs[c] : cs[c + wdt];
+              const float keep = upper ? cs[c + wdt] : cs[c];
+              cs[c] = keep + __shfl_xor_sync(0xffffffffu, send, wdt);
+            }
+          }
+          float* db = ((part >> 1) ? p.dbias_k : p.dbias_v) + w.h * kD + (part & 1) * 32;
+          atomicAdd(db + lane, cs[0]);
+        }
         if (key < p.kv_seq) {
           const int which = part >> 1;  // 0: dV, 1: dK
           __nv_bfloat16* dst = (which ? p.dk : p.dv) + (long long)(w.krow0 + key) * p.dkv_ld +
@@ -1672,22 +1708,48 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const __nv_bfloat16*
 }
 
 // dst[:, 0:H] (row stride ld) = bf16(dq)
-__global__ void attn_dq_store_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv,
-                                     long long rows, int H, long long ld) {
+// dQ (f32 accumulator) -> bf16 into dqkv.  With dbias: += the column sums of
+// dQ (the Q part of the QKV bias gradient).  Thread (column group of 4, row
+// lane) walks a band of rows; the CTA's row lanes combine in shared memory and
+// add one partial per column.
+constexpr int kDqLanes = 4;
+__global__ void __launch_bounds__(256 * kDqLanes) attn_dq_store_kernel(
+    const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv, long long rows, int H,
+    long long ld, long long rows_per_cta, float* __restrict__ dbias) {
   pdl_wait();
-  const long long n4 = rows * H / 4;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    const float4 v = reinterpret_cast<const float4*>(dq)[i];
-    const long long e = i * 4, row = e / H, col = e % H;
-    uint2 w;
-    w.x = pack_bf16(v.x, v.y);
-    w.y = pack_bf16(v.z, v.w);
-    *reinterpret_cast<uint2*>(dqkv + row * ld + col) = w;
+  __shared__ float4 part[kDqLanes][256];
+  const int c4 = blockIdx.y * 256 + (threadIdx.x & 255), lane = threadIdx.x >> 8;
+  const bool col = c4 < (H >> 2);
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (col) {
+#pragma unroll 4
+    for (long long r = r0 + lane; r < r1; r += kDqLanes) {
+      const float4 v = reinterpret_cast<const float4*>(dq + r * H)[c4];
+      uint2 w;
+      w.x = pack_bf16(v.x, v.y);
+      w.y = pack_bf16(v.z, v.w);
+      *reinterpret_cast<uint2*>(dqkv + r * ld + c4 * 4) = w;
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  if (dbias == nullptr) return;
+  part[lane][threadIdx.x & 255] = acc;
+  __syncthreads();
+  if (lane == 0 && col) {
+#pragma unroll
+    for (int q = 1; q < kDqLanes; ++q) {
+      const float4 o = part[q][threadIdx.x];
+      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+    }
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dbias + c4 * 4), "f"(acc.x),
+                 "f"(acc.y), "f"(acc.z), "f"(acc.w)
+                 : "memory");
   }
 }
 
-constexpr int kBwdSmem = 1024 + kTileBytes * 6 + 4 * kPBytes + 256;  // K V Q[2] dO[2] | P dS[2] dQ-staging
+constexpr int kBwdSmem = 1024 + kTileBytes * 7 + 3 * kPBytes + kPBytes / 2 + 256;  // K[2] V Q[2] dO[2] | P dS[2] | dQ-staging
 
 }  // namespace
 }  // namespace dpn
@@ -1743,8 +1805,12 @@ int attn_bwd_launch(const void* q_src, long long q_ld, const void* kv_src, long 
                     int k_col, int v_col, const void* out, const void* dout, const float* lse,
                     __nv_bfloat16* dq_dst, long long dq_ld, __nv_bfloat16* dk, __nv_bfloat16* dv,
                     long long dkv_ld, float* workspace, int64_t workspace_floats, int64_t batch,
-                    int64_t seq, int64_t kv_seq, int64_t heads, float scale, int causal, void* stream) {
+                    int64_t seq, int64_t kv_seq, int64_t heads, float scale, int causal, void* stream,
+                    float* dbias_q = nullptr, float* dbias_k = nullptr, float* dbias_v = nullptr) {
   const long long H = heads * kD, rows = batch * seq;
+  DPN_REQUIRE((dbias_q == nullptr) == (dbias_k == nullptr) && (dbias_k == nullptr) == (dbias_v == nullptr) &&
+                  (reinterpret_cast<uintptr_t>(dbias_q) & 15) == 0,
+              "dbias must be a 16-byte aligned f32 [3H] (or null)");
   DPN_REQUIRE(workspace != nullptr && workspace_floats >= rows * H + batch * heads * seq,
               "workspace must hold batch*seq*(heads*64) + batch*heads*seq floats");
   cudaStream_t st = (cudaStream_t)stream;
@@ -1782,6 +1848,8 @@ int attn_bwd_launch(const void* q_src, long long q_ld, const void* kv_src, long 
   p.D = D;
   p.dq = dq;
   p.dqkv = dq_dst;
+  p.dbias_k = dbias_k;
+  p.dbias_v = dbias_v;
   static bool set = false;
   if (!set) {
     DPN_CHECK_CUDA(cudaFuncSetAttribute(attn_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1799,9 +1867,15 @@ int attn_bwd_launch(const void* q_src, long long q_ld, const void* kv_src, long 
   const unsigned grid = (unsigned)std::min<long long>(units, n_sm_b);  // persistent
   DPN_CHECK_CUDA(launch_pdl(attn_bwd_kernel, grid, kBwdThreads, kBwdSmem, st, tq, tkv, td, tdq, p));
   DPN_LAUNCH_CHECK();
-  DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel,
-                            (unsigned)std::min<long long>((rows * H / 4 + 255) / 256, 148 * 8), 256, 0,
-                            st, dq, dq_dst, rows, (int)H, dq_ld));
+  {
+    // one CTA per SM per column block of 1024 columns: ~rows/148 rows per CTA, so
+    // the bias partials are a small fraction of the bytes moved
+    const long long gy = (H / 4 + 255) / 256;
+    const long long bands = std::max<long long>(1, std::min<long long>(rows, 148 / std::min<long long>(gy, 148)));
+    const long long per = (rows + bands - 1) / bands;
+    DPN_CHECK_CUDA(launch_pdl(attn_dq_store_kernel, dim3((unsigned)((rows + per - 1) / per), (unsigned)gy),
+                              256 * kDqLanes, 0, st, dq, dq_dst, rows, (int)H, dq_ld, per, dbias_q));
+  }
   DPN_LAUNCH_CHECK();
   return 0;
 }
@@ -1811,14 +1885,15 @@ int attn_bwd_launch(const void* q_src, long long q_ld, const void* kv_src, long 
 extern "C" int dpn_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
                             void* dqkv, float* workspace, int64_t workspace_floats, int64_t batch,
                             int64_t seq, int64_t heads, int64_t head_dim, float scale, int causal,
-                            void* stream) {
+                            float* dbias, void* stream) {
   DPN_REQUIRE(head_dim == 64, "fused attention supports head_dim 64");
   DPN_REQUIRE(seq % 64 == 0 && seq > 0, "seq must be a positive multiple of 64");
   const long long H = heads * head_dim;
   __nv_bfloat16* d = static_cast<__nv_bfloat16*>(dqkv);
   return attn_bwd_launch(qkv, 3 * H, qkv, 3 * H, 0, (int)H, (int)(2 * H), out, dout, lse, d, 3 * H,
                          d + H, d + 2 * H, 3 * H, workspace, workspace_floats, batch, seq, seq, heads,
-                         scale, causal, stream);
+                         scale, causal, stream, dbias, dbias ? dbias + H : nullptr,
+                         dbias ? dbias + 2 * H : nullptr);
 }
 
 extern "C" int dpn_attn_fwd_cross(const void* q, const void* kv, void* out, float* lse, int64_t batch,

@@ -64,36 +64,19 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
   const int warps = blockDim.x >> 5;
   const int lane = threadIdx.x & 31;
   const int nvec = cols >> 3;
-  const long long stride = (long long)gridDim.x * warps;
-  // the next row's x is in flight while this one is normalised (one row of
-  // loads per warp did not cover HBM latency); gamma / beta come from L1
-  uint4 xr[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) xr[j] = make_uint4(0, 0, 0, 0);
-  long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5);
-  if (r < rows) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int c = lane + 32 * j;
-      if (c < nvec) xr[j] = *reinterpret_cast<const uint4*>(x + r * cols + c * 8);
-    }
-  }
-  for (; r < rows; r += stride) {
-    const long long rn = r + stride;
-    uint4 xn[NV];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int c = lane + 32 * j;
-      xn[j] = make_uint4(0, 0, 0, 0);
-      if (c < nvec && rn < rows) xn[j] = *reinterpret_cast<const uint4*>(x + rn * cols + c * 8);
-    }
+  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
+       r += (long long)gridDim.x * warps) {
+    const __nv_bfloat16* xr = x + r * cols;
     float v[NV][8];
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      load8(reinterpret_cast<const __nv_bfloat16*>(&xr[j]), v[j]);
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        load8(xr + c * 8, v[j]);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s += v[j][i];  // zero-filled past cols
+        for (int i = 0; i < 8; ++i) s += v[j][i];
+      }
     }
     const float mu = warp_sum(s) / cols;
     float q = 0.f;
@@ -125,8 +108,6 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const __nv_bfloat16* __rest
       mean_out[r] = mu;
       rstd_out[r] = rs;
     }
-#pragma unroll
-    for (int j = 0; j < NV; ++j) xr[j] = xn[j];
   }
 }
 

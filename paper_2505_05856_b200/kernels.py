@@ -174,15 +174,19 @@ def attn_fwd(qkv, out, lse, batch, seq, heads, causal, scale=None, stream=None):
           "dpn_attn_fwd")
 
 
-def attn_bwd(qkv, out, dout, lse, dqkv, batch, seq, heads, causal, scale=None, stream=None):
-    """Fused attention backward -> dqkv [b*s, 3H] (dQ | dK | dV)."""
+def attn_bwd(qkv, out, dout, lse, dqkv, batch, seq, heads, causal, scale=None, dbias=None,
+             stream=None):
+    """Fused attention backward -> dqkv [b*s, 3H] (dQ | dK | dV).
+    dbias: f32 [3H]: += column sums of dqkv (the QKV projection's bias gradient)."""
+    assert dbias is None or (dbias.dtype == torch.float32 and dbias.data_ptr() % 16 == 0)
     d = 64
     H = heads * d
     INSTR.launches += 3
     ws = _workspace(qkv.device, batch * seq * H + batch * heads * seq, stream)
     check(lib().dpn_attn_bwd(qkv.data_ptr(), out.data_ptr(), dout.data_ptr(), lse.data_ptr(),
                              dqkv.data_ptr(), ws.data_ptr(), ws.numel(), batch, seq, heads, d,
-                             scale if scale is not None else d ** -0.5, int(causal), _s(stream)),
+                             scale if scale is not None else d ** -0.5, int(causal),
+                             None if dbias is None else dbias.data_ptr(), _s(stream)),
           "dpn_attn_bwd")
 
 

@@ -324,6 +324,14 @@ class StageExecutor:
             if (src in in_stage and self.node_by_id[src].kind == "linear"
                     and [c.id for c in self.all_nodes if src in c.inputs] == [g_id]):
                 self.gelu_bias_of[fc2_id] = src
+        # QKV bias gradient accumulated by the fused attention backward
+        self.attn_bias_of: Dict[str, str] = {}  # attention id -> qkv linear id
+        for n in self.nodes:
+            if n.kind == "attn_fused" and n.inputs[0] in in_stage:
+                src = self.node_by_id[n.inputs[0]]
+                if (src.kind == "linear"
+                        and [c.id for c in self.all_nodes if src.id in c.inputs] == [n.id]):
+                    self.attn_bias_of[n.id] = src.id
         self._skip_bwd: Set[str] = set()
         # bias gradient of a linear node folded into the one-pass LayerNorm
         # backward of the LN reading that node's output (or, through the
@@ -1151,9 +1159,17 @@ class StageExecutor:
             qkv_t = out_tid(n.inputs[0])
             assert qkv_t not in self.grad_init
             dqkv = self.grad_buffer(qkv_t)
+            # the QKV projection's bias gradient (column sums of dqkv) is accumulated
+            # by the attention backward itself when the attention is its only reader
+            lin = self.attn_bias_of.get(n.id)
+            dbias = P.gradv(f"{lin}.bias") if lin is not None else None
+            if dbias is not None and dbias.data_ptr() % 16:
+                dbias = None
             K.attn_bwd(self.buf(qkv_t, slot, "bwd"), self.buf(tid, slot, "bwd"), dy,
                        self.buf(stats_tid(n.id), slot, "bwd"), dqkv, self.b, n.seq or cfg.seq,
-                       cfg.heads, n.causal, stream=st)
+                       cfg.heads, n.causal, dbias=dbias, stream=st)
+            if dbias is not None:
+                self._bias_done.add(lin)
             self.grad_init.add(qkv_t)
         elif k == "xattn":
             self._xattn_bwd(n, dy, slot, W, G)

@@ -472,13 +472,21 @@ def test_fused_attention_backward(b, s, A, causal):
     k.attn_fwd(qkv, out, lse, b, s, A, causal)
     dout = rnd(b * s, H)
     dqkv = torch.empty_like(qkv)
-    k.attn_bwd(qkv, out, dout, lse, dqkv, b, s, A, causal)
+    dbias = torch.randn(3 * H, device="cuda")
+    db0 = dbias.clone()
+    k.attn_bwd(qkv, out, dout, lse, dqkv, b, s, A, causal, dbias=dbias)
     torch.cuda.synchronize()
     x = qkv.float().requires_grad_()
     o_ref, _ = _attn_ref(x, b, s, A, causal)
     o_ref.backward(dout.float())
     for part in range(3):
         close(dqkv[:, part * H:(part + 1) * H], x.grad[:, part * H:(part + 1) * H])
+        # fused QKV bias gradient: column sums of dQ | dK | dV, against the fp32
+        # reference's; the dK sums are exactly zero (softmax rows of dS sum to 0),
+        # so the tolerance is relative to the sums of |d| rather than to the sums
+        g = x.grad[:, part * H:(part + 1) * H]
+        err = ((dbias - db0)[part * H:(part + 1) * H] - g.sum(0)).abs().max().item()
+        assert err <= 1e-2 * g.abs().sum(0).max().item(), f"part {part}: max err {err:.4g}"
 
 
 @pytest.mark.parametrize("b,t,s,A", [(2, 128, 512, 2), (3, 64, 192, 2), (16, 128, 512, 16)])
