@@ -41,6 +41,12 @@
 namespace dpn {
 namespace {
 
+#ifndef DPN_ATTN_POLY
+#define DPN_ATTN_POLY 0  // key pairs of every 4 exponentiated by exp2_fma2 in the forward (A/B: slower)
+#endif
+#ifndef DPN_ATTN_POLY_BWD
+#define DPN_ATTN_POLY_BWD 0  // the same for the backward's recomputed P
+#endif
 constexpr int kTile = 128;  // queries per CTA and keys per KV tile
 constexpr int kD = 64;
 constexpr int kKVStages = 3;
@@ -340,7 +346,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
             const float2 a = fma2(make_float2(s[c * 8 + e], s[c * 8 + e + 1]), make_float2(sl, sl),
                                   make_float2(-base, -base));
-            const float2 ev = make_float2(ex2(a.x), ex2(a.y));
+            // DPN_ATTN_POLY of every 4 key pairs exponentiate on the FMA pipe: the
+            // MUFU (XU) pipe is the forward's limiter (ncu: XU 99% busy)
+            const float2 ev = e >= 2 * (4 - DPN_ATTN_POLY) ? exp2_fma2(a) : make_float2(ex2(a.x), ex2(a.y));
             e8[e] = ev.x;
             e8[e + 1] = ev.y;
             sum2 = fma2(make_float2(1.f, 1.f), ev, sum2);
@@ -1529,7 +1537,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
               const float2 a = fma2(make_float2(__uint_as_float(us[c * 8 + e]), __uint_as_float(us[c * 8 + e + 1])),
                                     make_float2(sl, sl), make_float2(-lse2, -lse2));
-              float2 pr = make_float2(ex2(a.x), ex2(a.y));
+              // DPN_ATTN_POLY_BWD of every 4 key pairs on the FMA pipe (see exp2_fma2)
+              float2 pr = e >= 2 * (4 - DPN_ATTN_POLY_BWD) ? exp2_fma2(a) : make_float2(ex2(a.x), ex2(a.y));
               if constexpr (kMask) {
                 const int key = k0 + half * 64 + c * 8 + e;
                 pr.x = (qok && key < p.kv_seq && (!p.causal || key <= q)) ? pr.x : 0.f;

@@ -356,6 +356,31 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
   return f2_unpack(r);
 }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a)), "l"(f2_pack(b)));
+  return f2_unpack(r);
+}
+
+// 2^x for two values on the FMA pipe (no MUFU): round-to-nearest split
+// x = n + f (the 1.5*2^23 magic add), a degree-3 fit of 2^f on [-0.5, 0.5]
+// (max relative error 7.5e-5, far below bf16 resolution), and n added to the
+// exponent bits.  x is clamped at -125 (2^-125 stands in for 0 -- e.g. for
+// masked scores -- and contributes nothing at f32 / bf16 resolution).  Used for
+// part of the softmax exponentials when the MUFU (XU) pipe is the limiter.
+__device__ __forceinline__ float2 exp2_fma2(float2 x) {
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 j = add2(x, magic);
+  const float2 n = add2(j, make_float2(-12582912.f, -12582912.f));
+  const float2 f = fma2(n, make_float2(-1.f, -1.f), x);
+  float2 p = fma2(f, make_float2(0.05517108f, 0.05517108f), make_float2(0.24261111f, 0.24261111f));
+  p = fma2(p, f, make_float2(0.69326109f, 0.69326109f));
+  p = fma2(p, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
 
 // tanh-GELU / its derivative on two values with packed fp32 FMAs (the same
 // formulas as gelu_tanh / gelu_tanh_grad, two lanes per instruction)
