@@ -87,6 +87,9 @@ constexpr int kMaxSmem = 232448;  // 227 KB per CTA on sm_100
 #ifndef DPN_GEMM_GROUP
 #define DPN_GEMM_GROUP 8
 #endif
+#ifndef DPN_GEMM_HINT
+#define DPN_GEMM_HINT 0  // 1: A evict_first / B evict_last, 2: both evict_last (pair tiles)
+#endif
 #ifndef DPN_GEMM_L2_PROMO
 #define DPN_GEMM_L2_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
 #endif
@@ -563,8 +566,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint8_t* b_dst = sB + stage * C::kBBytes;
           const int k0 = kb * BK;
           auto load = [&](void* dst, const CUtensorMap* m, int c0, int c2) {
-            if constexpr (CG >= 2) tma_load_4d_pair(dst, m, &full[stage], c0, w.z1, c2, w.z2);
-            else tma_load_4d(dst, m, &full[stage], c0, w.z1, c2, w.z2);
+            if constexpr (CG >= 2 && DPN_GEMM_HINT != 0) {
+              const uint64_t pol = (m == &tmA && DPN_GEMM_HINT == 1) ? l2_policy_evict_first()
+                                                                    : l2_policy_evict_last();
+              tma_load_4d_pair_hint(dst, m, &full[stage], c0, w.z1, c2, w.z2, pol);
+            } else if constexpr (CG >= 2) {
+              tma_load_4d_pair(dst, m, &full[stage], c0, w.z1, c2, w.z2);
+            } else {
+              tma_load_4d(dst, m, &full[stage], c0, w.z1, c2, w.z2);
+            }
           };
           if constexpr (kMc) {
             // this CTA fetches 64 of its 128 A rows and multicasts them to the
