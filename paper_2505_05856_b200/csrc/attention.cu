@@ -82,10 +82,6 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
-// named barrier over the two warps (64 threads) that share a row quarter
-__device__ __forceinline__ void pair_sync(int quarter) {
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                             int c1) {
@@ -121,9 +117,18 @@ __device__ __forceinline__ void tmem_st_wait() {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kFwdThreads, 1)
+// KS = key splits per row: KS softmax warps share each TMEM lane quarter, each
+// owning 128 / KS keys of every tile with its own running max, sum and O
+// accumulator.  KS = 2: 8 softmax warps, O double-buffered by unit parity;
+// KS = 4: 16 softmax warps (latency hiding for the softmax chain), one O set.
+template <int KS>
+__global__ void __launch_bounds__(128 + 128 * KS, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
                     const AttnParams p) {
+  static_assert(KS == 2 || KS == 4, "key splits");
+  constexpr int kKeys = kTile / KS;         // keys per split
+  constexpr int kSoftWarps = 4 * KS;
+  constexpr int kOBufs = KS == 2 ? 2 : 1;   // O accumulator sets (by unit parity)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -184,10 +189,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);  // one arrival per softmax warp
-      mbar_init(&p_full[i], 8);
+      mbar_init(&s_empty[i], kSoftWarps);  // one arrival per softmax warp
+      mbar_init(&p_full[i], kSoftWarps);
       mbar_init(&p_empty[i], 1);
-      mbar_init(&o_empty[i], 8);
+      mbar_init(&o_empty[i], kSoftWarps);
     }
     mbar_init(pv_done, 1);
     fence_mbar_init();
@@ -198,11 +203,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   pdl_wait();
-  // TMEM columns: S[0] 0..127, S[1] 128..255; O[unit parity][key half] at
-  // 256 + 128 * parity + 64 * half (64 columns each).  Each key half keeps its
-  // own running max: O_half accumulates P_half V_half in TMEM (rescaled in
-  // place on the rare tiles where that half's max grows by more than 2^8), and
-  // the halves are combined once per unit.
+  // TMEM columns: S[0] 0..127, S[1] 128..255; O[unit parity][key split] at
+  // 256 + 128 * parity + 64 * split (KS = 2) or 256 + 64 * split (KS = 4), 64
+  // columns each.  Each key split keeps its own running max: O_split
+  // accumulates P_split V_split in TMEM (rescaled in place on the rare tiles
+  // where that split's max grows by more than 2^8), and the splits are
+  // combined once per unit.
 
   if (warp == 0) {
     if (lane == 0) {
@@ -234,7 +240,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     auto issue_pv = [&](int t, bool first, int ub, int ucount) {
       const int i = t & 1;
       mbar_wait(&p_full[i], (t >> 1) & 1);
-      if (first) mbar_wait(&o_empty[ub], ((ucount >> 1) & 1) ^ 1);
+      if (first) mbar_wait(&o_empty[ub], ((ucount / kOBufs) & 1) ^ 1);
       tc_fence_after();
       if (lane == 0) {
         const int st = t % kKVStages;
@@ -243,8 +249,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int k = 0; k < kTile / 16; ++k) {
           const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024);
           const uint64_t bd = smem_desc_sw128(vb + k * 2048, kD * 128, 1024);
-          umma_bf16(tmem + 256 + ub * 128 + (k >> 2) * 64, ad, bd, idesc_o,
-                    (first && (k & 3) == 0) ? 0u : 1u);
+          constexpr int kSteps = kKeys / 16;  // K=16 steps per key split
+          umma_bf16(tmem + 256 + ub * 128 + (k / kSteps) * 64, ad, bd, idesc_o,
+                    (first && (k % kSteps) == 0) ? 0u : 1u);
         }
         umma_commit(&p_empty[i]);
         umma_commit(&kv_empty[st]);
@@ -280,14 +287,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         __syncwarp();
         if (g >= 1) issue_pv(g - 1, prev_first, prev_ub, prev_uc);
         prev_first = j == 0;
-        prev_ub = uc & 1;
+        prev_ub = KS == 2 ? (uc & 1) : 0;
         prev_uc = uc;
       }
     }
     if (g >= 1) issue_pv(g - 1, prev_first, prev_ub, prev_uc);
   } else if (warp >= 4) {
     // ---------------- softmax ----------------
-    const int quarter = warp & 3, half = (warp - 4) >> 2;
+    const int quarter = warp & 3, half = (warp - 4) >> 2;  // half: key split
     const int r = quarter * 32 + lane;  // query row within the tile (== TMEM lane)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     float* xs = reinterpret_cast<float*>(tmem_slot + 4);  // [2 units][128 rows][half][m, l]
@@ -296,39 +303,40 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
       int qt, h, bb;
       decode(u, qt, h, bb);
-      const int n_kv = kv_tiles(qt), row0 = bb * p.seq, ub = uc & 1;
+      const int n_kv = kv_tiles(qt), row0 = bb * p.seq, ub = KS == 2 ? (uc & 1) : 0;
       const int q = qt * kTile + r;
       const uint32_t o_half = tmem + 256 + ub * 128 + half * 64 + lane_off;
       float ms = -INFINITY;  // this key half's running max, scaled log2 units
       float l = 0.f;         // this key half's running sum
       for (int j = 0; j < n_kv; ++j) {
         const int gj = g + j, i = gj & 1;
-        const int k0 = j * kTile + half * 64;
+        const int k0 = j * kTile + half * kKeys;
         const bool mask = (j + 1) * kTile > p.kv_seq || (p.causal && j == qt);
         mbar_wait(&s_full[i], (gj >> 1) & 1);
         tc_fence_after();
-        float s[64];
+        float s[kKeys];
         {
-          uint32_t uu[64];
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + lane_off, uu);
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, uu + 32);
+          uint32_t uu[kKeys];
+#pragma unroll
+          for (int c = 0; c < kKeys / 32; ++c)
+            tmem_ld_32x32b_x32(tmem + i * 128 + half * kKeys + c * 32 + lane_off, uu + c * 32);
           tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(uu[e]);
+          for (int e = 0; e < kKeys; ++e) s[e] = __uint_as_float(uu[e]);
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[i]);
         if (mask) {
 #pragma unroll
-          for (int c = 0; c < 64; ++c) {
+          for (int c = 0; c < kKeys; ++c) {
             const int key = k0 + c;
             if (!(key < p.kv_seq && (!p.causal || key <= q))) s[c] = -INFINITY;
           }
         }
         float mx = s[0];
 #pragma unroll
-        for (int c = 1; c < 64; ++c) mx = fmaxf(mx, s[c]);
+        for (int c = 1; c < kKeys; ++c) mx = fmaxf(mx, s[c]);
         mx *= sl;
         float alpha = 1.f;
         if (mx > ms + kRescaleLog2 || ms == -INFINITY) {
@@ -338,13 +346,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const float base = (ms == -INFINITY) ? 0.f : ms;
         float2 sum2 = make_float2(0.f, 0.f);
         mbar_wait(&p_empty[i], ((gj >> 1) & 1) ^ 1);
-        uint8_t* pt = sP + i * kPBytes + half * (kPBytes / 2);
+        // this split's keys: atom half * kKeys / 64, 16-byte chunks from (half * kKeys % 64) / 8
+        uint8_t* pt = sP + i * kPBytes + (half * kKeys / 64) * (kPBytes / 2);
+        constexpr int kChunk0Mul = kKeys / 8;  // chunks per split
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int cc = 0; cc < kKeys / 8; ++cc) {
+          const int c = cc + (half * kChunk0Mul) % 8;  // chunk within the 64-key atom
           float e8[8];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {  // two keys per packed f32x2 instruction
-            const float2 a = fma2(make_float2(s[c * 8 + e], s[c * 8 + e + 1]), make_float2(sl, sl),
+            const float2 a = fma2(make_float2(s[cc * 8 + e], s[cc * 8 + e + 1]), make_float2(sl, sl),
                                   make_float2(-base, -base));
             // DPN_ATTN_POLY of every 4 key pairs exponentiate on the FMA pipe: the
             // MUFU (XU) pipe is the forward's limiter (ncu: XU 99% busy)
@@ -385,37 +396,47 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       // ---- unit epilogue: combine the key halves ----
       mbar_wait(pv_done, (g + n_kv - 1) & 1);
       tc_fence_after();
-      float* xm = xs + ub * 512 + r * 4;
+      // per unit exchange of the splits' (m, l): [unit parity][row][split][2]
+      float* xm = xs + ub * (128 * KS * 2) + r * (KS * 2);
       xm[half * 2] = ms;
       xm[half * 2 + 1] = l;
-      pair_sync(quarter);
-      const float m0 = xm[0], l0 = xm[1], m1 = xm[2], l1 = xm[3];
-      const float m = fmaxf(m0, m1);
-      const float a0 = m0 == -INFINITY ? 0.f : ex2(m0 - m), a1 = m1 == -INFINITY ? 0.f : ex2(m1 - m);
-      const float lt = l0 * a0 + l1 * a1;
-      // this warp writes output columns half*32.. from both halves' accumulators
-      uint32_t o0[32], o1[32];
-      tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + half * 32 + lane_off, o0);
-      tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + 64 + half * 32 + lane_off, o1);
-      tmem_ld_wait();
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(32 * KS) : "memory");
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < KS; ++k) m = fmaxf(m, xm[2 * k]);
+      float a[KS], lt = 0.f;
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        a[k] = xm[2 * k] == -INFINITY ? 0.f : ex2(xm[2 * k] - m);
+        lt += xm[2 * k + 1] * a[k];
+      }
+      // this warp writes output columns half * 64/KS .. from every split's accumulator
+      constexpr int kCols = 64 / KS;
+      float v[kCols];
+#pragma unroll
+      for (int e = 0; e < kCols; ++e) v[e] = 0.f;
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + k * 64 + (half * kCols) / 32 * 32 + lane_off, o);
+        tmem_ld_wait();
+        const int off = (half * kCols) % 32;
+#pragma unroll
+        for (int e = 0; e < kCols; ++e) v[e] = fmaf(__uint_as_float(o[off + e]), a[k], v[e]);
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&o_empty[ub]);
       if (q < p.seq) {
         const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        const float s0 = a0 * inv, s1 = a1 * inv;
-        __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + half * 32;
+        __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + half * kCols;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          float v[8];
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            v[e] = fmaf(__uint_as_float(o0[c * 8 + e]), s0, __uint_as_float(o1[c * 8 + e]) * s1);
+        for (int c = 0; c < kCols / 8; ++c) {
           uint4 w;
-          w.x = pack_bf16(v[0], v[1]);
-          w.y = pack_bf16(v[2], v[3]);
-          w.z = pack_bf16(v[4], v[5]);
-          w.w = pack_bf16(v[6], v[7]);
+          w.x = pack_bf16(v[c * 8 + 0] * inv, v[c * 8 + 1] * inv);
+          w.y = pack_bf16(v[c * 8 + 2] * inv, v[c * 8 + 3] * inv);
+          w.z = pack_bf16(v[c * 8 + 4] * inv, v[c * 8 + 5] * inv);
+          w.w = pack_bf16(v[c * 8 + 6] * inv, v[c * 8 + 7] * inv);
           reinterpret_cast<uint4*>(op)[c] = w;
         }
         // natural-log LSE of scale * S:  (m + log2 l) / log2(e)
@@ -1214,9 +1235,14 @@ struct FwdKernel {
 FwdKernel fwd_kernel() {
   static FwdKernel k = [] {
     const char* e = getenv("DPN_ATTN_FWD");
-    FwdKernel r = (e && e[0] == '2')   ? FwdKernel{attn_fwd2_kernel, kFwd2Threads, kFwd2Smem}
-                  : (e && e[0] == '3') ? FwdKernel{attn_fwd3_kernel, kFwd3Threads, kFwd3Smem}
-                                       : FwdKernel{attn_fwd_kernel, kFwdThreads, kFwdSmem};
+#ifndef DPN_ATTN_FWD_DEFAULT
+#define DPN_ATTN_FWD_DEFAULT '1'
+#endif
+    const char v = e && e[0] ? e[0] : DPN_ATTN_FWD_DEFAULT;
+    FwdKernel r = v == '2'   ? FwdKernel{attn_fwd2_kernel, kFwd2Threads, kFwd2Smem}
+                  : v == '3' ? FwdKernel{attn_fwd3_kernel, kFwd3Threads, kFwd3Smem}
+                  : v == '4' ? FwdKernel{attn_fwd_kernel<4>, 128 + 128 * 4, kFwdSmem}
+                             : FwdKernel{attn_fwd_kernel<2>, kFwdThreads, kFwdSmem};
     cudaFuncSetAttribute(r.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, r.smem);
     return r;
   }();
