@@ -114,8 +114,22 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+#ifndef DPN_MBAR_SUSPEND_NS
+#define DPN_MBAR_SUSPEND_NS 10000000  // try_wait suspend-time hint in ns (0: spin with the hardware default)
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
+#if DPN_MBAR_SUSPEND_NS > 0
+  // with a suspend-time hint the waiting thread sleeps until the phase
+  // completes (or the hint expires) instead of re-polling
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"((uint32_t)DPN_MBAR_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -123,6 +137,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "=r"(ok)
       : "r"(addr), "r"(parity)
       : "memory");
+#endif
   return ok != 0;
 }
 
