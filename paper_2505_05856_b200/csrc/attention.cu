@@ -44,6 +44,9 @@ namespace {
 #ifndef DPN_ATTN_POLY
 #define DPN_ATTN_POLY 0  // key pairs of every 4 exponentiated by exp2_fma2 in the forward (A/B: slower)
 #endif
+#ifndef DPN_ATTN_PACK_ALU
+#define DPN_ATTN_PACK_ALU 0  // 1: the forward packs P to bf16 on the integer ALU instead of F2FP
+#endif
 #ifndef DPN_ATTN_POLY_BWD
 #define DPN_ATTN_POLY_BWD 0  // the same for the backward's recomputed P
 #endif
@@ -365,10 +368,17 @@ __global__ void __launch_bounds__(128 + 128 * KS, 1)
             sum2 = fma2(make_float2(1.f, 1.f), ev, sum2);
           }
           uint4 w;
+#if DPN_ATTN_PACK_ALU
+          w.x = pack_bf16_alu(e8[0], e8[1]);
+          w.y = pack_bf16_alu(e8[2], e8[3]);
+          w.z = pack_bf16_alu(e8[4], e8[5]);
+          w.w = pack_bf16_alu(e8[6], e8[7]);
+#else
           w.x = pack_bf16(e8[0], e8[1]);
           w.y = pack_bf16(e8[2], e8[3]);
           w.z = pack_bf16(e8[4], e8[5]);
           w.w = pack_bf16(e8[6], e8[7]);
+#endif
           sts128(smem_u32(pt) + sw128(r, c), w);
         }
         l = l * alpha + (sum2.x + sum2.y);
@@ -453,724 +463,10 @@ __global__ void __launch_bounds__(128 + 128 * KS, 1)
   }
 }
 
-// ---------------------------------------------------------------------------
-// Forward, two softmax sets (default): the same unit walk and TMA / MMA
-// protocol as attn_fwd_kernel, but the softmax runs on 16 warps in two sets
-// of 8.  Set k owns the KV tiles of global index t with t % 2 == k (S buffer k,
-// P buffer k) and keeps its own running max / sum and its own O accumulators
-// O[k][key half] in TMEM (4 x 64 columns + S[0..1] = all 512), so the S -> P
-// -> PV chains of consecutive tiles are independent: while one set
-// exponentiates tile t the tensor core runs tile t+1's S and tile t-1's PV
-// for the other, and the MMA warp issues S two tiles ahead of PV (4-deep KV
-// ring).  ncu of the single-set kernel at b32 h16 s512 (profiles/
-// r02_attn_fwd_stalls.md): the 8 softmax warps spent ~15% of their samples
-// waiting for the previous tile's PV and the MUFU pipe was never the limiter
-// (stall_math 1.3%) -- a latency chain, which two interleaved chains hide.
-// Per unit the four partials (set, half) combine once: every softmax warp
-// writes 16 output columns from all four accumulators.
-constexpr int kFwd2Threads = 576;  // warp 0 TMA + TMEM, warp 1 MMA, warps 2-17 softmax
-constexpr int kKV2Stages = 4;
-constexpr int kFwd2Bars = 2 + 2 * kKV2Stages + 6 * 2;
-constexpr int kFwd2Smem = 1024 + kTileBytes * (1 + 2 * kKV2Stages) + 2 * kPBytes + kFwd2Bars * 8 + 16 +
-                          2 * 128 * 8 * 4;
-
-__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-}
-
-__global__ void __maxnreg__(96)
-    attn_fwd2_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
-                     const AttnParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kTileBytes;                   // [stage] 16 KB
-  uint8_t* sV = sK + kKV2Stages * kTileBytes;      // [stage] 16 KB
-  uint8_t* sP = sV + kKV2Stages * kTileBytes;      // [set] 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;
-  uint64_t* kv_empty = kv_full + kKV2Stages;
-  uint64_t* s_full = kv_empty + kKV2Stages;  // [set]
-  uint64_t* s_empty = s_full + 2;            // [set]
-  uint64_t* p_full = s_empty + 2;            // [set]
-  uint64_t* p_empty = p_full + 2;            // [set]
-  uint64_t* pv_done = p_empty + 2;           // [set], one phase per tile of the set
-  uint64_t* o_empty = pv_done + 2;           // [set], one phase per unit the set takes part in
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kFwd2Bars);
-  float* xs = reinterpret_cast<float*>(tmem_slot + 4);  // [unit parity][128 rows][set][half][m, l]
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_kv_all = (p.kv_seq + kTile - 1) / kTile;
-  const int n_qt = (p.seq + kTile - 1) / kTile;
-  const long long bh = (long long)p.batch * p.heads;
-  const long long units = bh * n_qt;
-  auto decode = [&](long long u, int& qt, int& h, int& bb) {
-    int qi;
-    long long r;
-    if (p.causal) {
-      qi = (int)(u / bh);
-      r = u - (long long)qi * bh;
-    } else {
-      qi = (int)(u % n_qt);
-      r = u / n_qt;
-    }
-    qt = p.causal ? n_qt - 1 - qi : qi;
-    h = (int)(r % p.heads);
-    bb = (int)(r / p.heads);
-  };
-  auto kv_tiles = [&](int qt) { return p.causal ? min(n_kv_all, qt + 1) : n_kv_all; };
-  // tiles of set k in a unit whose first global tile index is g0
-  auto set_count = [&](long long g0, int n_kv, int k) {
-    const int first = ((g0 & 1) == k) ? 0 : 1;
-    return first < n_kv ? (n_kv - first + 1) / 2 : 0;
-  };
-
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tm_q);
-    prefetch_tmap(&tm_kv);
-  }
-  if (warp == 1 && lane == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int s = 0; s < kKV2Stages; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 8);  // the set's 8 softmax warps
-      mbar_init(&p_full[i], 8);
-      mbar_init(&p_empty[i], 1);
-      mbar_init(&pv_done[i], 1);
-      mbar_init(&o_empty[i], 16);  // every softmax warp reads a slice of both sets' O
-    }
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();
-  // TMEM columns: S[set] at 128 * set; O[set][key half] at 256 + 128 * set + 64 * half.
-
-  if (warp == 0) {
-    if (lane == 0) {
-      long long g = 0;
-      int uc = 0;
-      for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-        int qt, h, bb;
-        decode(u, qt, h, bb);
-        const int n_kv = kv_tiles(qt), row0 = bb * p.seq, krow0 = bb * p.kv_seq;
-        mbar_wait(q_empty, (uc & 1) ^ 1);
-        mbar_expect_tx(q_full, kTileBytes);
-        tma_load_2d(sQ, &tm_q, q_full, p.q_col + h * kD, row0 + qt * kTile);
-        for (int j = 0; j < n_kv; ++j, ++g) {
-          const int st = (int)(g % kKV2Stages);
-          mbar_wait(&kv_empty[st], (int)((g / kKV2Stages) & 1) ^ 1);
-          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-          tma_load_2d(sK + st * kTileBytes, &tm_kv, &kv_full[st], p.k_col + h * kD, krow0 + j * kTile);
-          tma_load_2d(sV + st * kTileBytes, &tm_kv, &kv_full[st], p.v_col + h * kD, krow0 + j * kTile);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
-    constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);
-    // PV of global tile t: `first` = the set's first tile in its unit; `ucnt` =
-    // units the set took part in before this one (o_empty phase)
-    struct Pending {
-      long long t;
-      int first, ucnt;
-    };
-    Pending pa{0, 0, 0}, pb{0, 0, 0};  // up to two PVs behind the S issue
-    int npend = 0;
-    auto issue_pv = [&](const Pending& d) {
-      const int i = (int)(d.t & 1);
-      mbar_wait(&p_full[i], (int)((d.t >> 1) & 1));
-      if (d.first) mbar_wait(&o_empty[i], (d.ucnt & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const int st = (int)(d.t % kKV2Stages);
-        const uint32_t pa = smem_u32(sP + i * kPBytes), vb = smem_u32(sV + st * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kTile / 16; ++k) {
-          const uint64_t ad = smem_desc_sw128(pa + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(vb + k * 2048, kD * 128, 1024);
-          umma_bf16(tmem + 256 + i * 128 + (k >> 2) * 64, ad, bd, idesc_o,
-                    (d.first && (k & 3) == 0) ? 0u : 1u);
-        }
-        umma_commit(&p_empty[i]);
-        umma_commit(&kv_empty[st]);
-        umma_commit(&pv_done[i]);
-      }
-      __syncwarp();
-    };
-    long long g = 0;
-    int uc = 0, ucnt0 = 0, ucnt1 = 0;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-      int qt, h, bb;
-      decode(u, qt, h, bb);
-      const int n_kv = kv_tiles(qt);
-      const int c0 = set_count(g, n_kv, 0), c1 = set_count(g, n_kv, 1);
-      mbar_wait(q_full, uc & 1);
-      for (int j = 0; j < n_kv; ++j) {
-        const long long t = g + j;
-        const int st = (int)(t % kKV2Stages), i = (int)(t & 1);
-        mbar_wait(&kv_full[st], (int)((t / kKV2Stages) & 1));
-        mbar_wait(&s_empty[i], (int)((t >> 1) & 1) ^ 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
-#pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
-            const uint64_t bd = smem_desc_sw128(kb + k * 32, 16, 1024);
-            umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[i]);
-          if (j == n_kv - 1) umma_commit(q_empty);
-        }
-        __syncwarp();
-        // S runs two tiles ahead of PV
-        const Pending d{t, j < 2 ? 1 : 0, i ? ucnt1 : ucnt0};
-        if (npend == 2) {
-          issue_pv(pa);
-          pa = pb;
-          pb = d;
-        } else if (npend == 1) {
-          pb = d;
-          npend = 2;
-        } else {
-          pa = d;
-          npend = 1;
-        }
-      }
-      ucnt0 += c0 > 0;
-      ucnt1 += c1 > 0;
-      g += n_kv;
-    }
-    if (npend >= 1) issue_pv(pa);
-    if (npend == 2) issue_pv(pb);
-  } else {
-    // ---------------- softmax: warps 2-17, four groups of four ----------------
-    // group (set, key half) = (warp - 2) / 4; a warp reads the TMEM lanes of
-    // its quarter warp % 4, so each group covers the four row quarters
-    const int grp = (warp - 2) >> 2;
-    const int set = grp >> 1, half = grp & 1;
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const float sl = p.scale_log2;
-    long long g = 0;
-    int uc = 0, tc_mine = 0, tc_other = 0;  // tiles this / the other set finished (pv_done phases)
-    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-      int qt, h, bb;
-      decode(u, qt, h, bb);
-      const int n_kv = kv_tiles(qt), row0 = bb * p.seq, ub = uc & 1;
-      const int q = qt * kTile + r;
-      const int cnt0 = set_count(g, n_kv, 0), cnt1 = set_count(g, n_kv, 1);
-      const int cnt_other = set ? cnt0 : cnt1;
-      const uint32_t o_half = tmem + 256 + set * 128 + half * 64 + lane_off;
-      float ms = -INFINITY, l = 0.f;
-      const int j0 = ((g & 1) == set) ? 0 : 1;
-      for (int j = j0; j < n_kv; j += 2) {
-        const long long t = g + j;
-        const int i = set;
-        const int k0 = j * kTile + half * 64;
-        const bool mask = (j + 1) * kTile > p.kv_seq || (p.causal && j == qt);
-        mbar_wait(&s_full[i], (int)((t >> 1) & 1));
-        tc_fence_after();
-        float s[64];
-        {
-          uint32_t uu[64];
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + lane_off, uu);
-          tmem_ld_32x32b_x32(tmem + i * 128 + half * 64 + 32 + lane_off, uu + 32);
-          tmem_ld_wait();
-#pragma unroll
-          for (int e = 0; e < 64; ++e) s[e] = __uint_as_float(uu[e]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[i]);
-        if (mask) {
-#pragma unroll
-          for (int c = 0; c < 64; ++c) {
-            const int key = k0 + c;
-            if (!(key < p.kv_seq && (!p.causal || key <= q))) s[c] = -INFINITY;
-          }
-        }
-        float mx = s[0];
-#pragma unroll
-        for (int c = 1; c < 64; ++c) mx = fmaxf(mx, s[c]);
-        mx *= sl;
-        float alpha = 1.f;
-        if (mx > ms + kRescaleLog2 || ms == -INFINITY) {
-          alpha = (ms == -INFINITY) ? 0.f : ex2(ms - mx);
-          ms = mx;
-        }
-        const float base = (ms == -INFINITY) ? 0.f : ms;
-        float2 sum2 = make_float2(0.f, 0.f);
-        mbar_wait(&p_empty[i], (int)((t >> 1) & 1) ^ 1);
-        uint8_t* pt = sP + i * kPBytes + half * (kPBytes / 2);
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          float e8[8];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float2 a = fma2(make_float2(s[c * 8 + e], s[c * 8 + e + 1]), make_float2(sl, sl),
-                                  make_float2(-base, -base));
-            const float2 ev = make_float2(ex2(a.x), ex2(a.y));
-            e8[e] = ev.x;
-            e8[e + 1] = ev.y;
-            sum2 = fma2(make_float2(1.f, 1.f), ev, sum2);
-          }
-          uint4 w;
-          w.x = pack_bf16(e8[0], e8[1]);
-          w.y = pack_bf16(e8[2], e8[3]);
-          w.z = pack_bf16(e8[4], e8[5]);
-          w.w = pack_bf16(e8[6], e8[7]);
-          sts128(smem_u32(pt) + sw128(r, c), w);
-        }
-        l = l * alpha + (sum2.x + sum2.y);
-        fence_async_smem();
-        if (j >= 2) {
-          // O[set][half] holds this set's earlier tiles once their PV is done
-          mbar_wait(&pv_done[i], (tc_mine - 1) & 1);
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
-            tc_fence_after();
-            uint32_t ou[64];
-            tmem_ld_32x32b_x32(o_half, ou);
-            tmem_ld_32x32b_x32(o_half + 32, ou + 32);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 64; ++e) ou[e] = __float_as_uint(__uint_as_float(ou[e]) * alpha);
-            tmem_st_32x32b_x32(o_half, ou);
-            tmem_st_32x32b_x32(o_half + 32, ou + 32);
-            tmem_st_wait();
-          }
-        }
-        tc_mine += 1;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[i]);
-      }
-      tc_other += cnt_other;  // the other set's tiles of this unit
-      // ---- unit epilogue: combine the four (set, key half) partials ----
-      if (cnt0 > 0) mbar_wait(&pv_done[0], ((set ? tc_other : tc_mine) - 1) & 1);
-      if (cnt1 > 0) mbar_wait(&pv_done[1], ((set ? tc_mine : tc_other) - 1) & 1);
-      tc_fence_after();
-      float* xm = xs + (ub * 128 + r) * 8;
-      xm[(set * 2 + half) * 2] = ms;
-      xm[(set * 2 + half) * 2 + 1] = l;
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(128) : "memory");
-      float m = -INFINITY;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) m = fmaxf(m, xm[k * 2]);
-      float a[4], lt = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        a[k] = xm[k * 2] == -INFINITY ? 0.f : ex2(xm[k * 2] - m);
-        lt += xm[k * 2 + 1] * a[k];
-      }
-      // this warp writes output columns 16 * (set * 2 + half) ..
-      const int c0 = 16 * (set * 2 + half);
-      float o[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) o[e] = 0.f;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if ((k >> 1 ? cnt1 : cnt0) == 0) continue;  // that set had no tile in this unit
-        uint32_t oo[16];
-        tmem_ld_32x32b_x16(tmem + 256 + (k >> 1) * 128 + (k & 1) * 64 + c0 + lane_off, oo);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = fmaf(__uint_as_float(oo[e]), a[k], o[e]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (cnt0 > 0) mbar_arrive(&o_empty[0]);
-        if (cnt1 > 0) mbar_arrive(&o_empty[1]);
-      }
-      if (q < p.seq) {
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + c0;
-#pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          uint4 w;
-          w.x = pack_bf16(o[cc * 8 + 0] * inv, o[cc * 8 + 1] * inv);
-          w.y = pack_bf16(o[cc * 8 + 2] * inv, o[cc * 8 + 3] * inv);
-          w.z = pack_bf16(o[cc * 8 + 4] * inv, o[cc * 8 + 5] * inv);
-          w.w = pack_bf16(o[cc * 8 + 6] * inv, o[cc * 8 + 7] * inv);
-          reinterpret_cast<uint4*>(op)[cc] = w;
-        }
-        if (set == 0 && half == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (m + log2f(lt)) / kLog2e;
-      }
-      g += n_kv;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_free<512>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------------------
-// Forward, two softmax sets of whole rows (DPN_ATTN_FWD=3, experimental): set k
-// (4 warps, one per TMEM lane quarter, a thread owns a query row and all 128
-// keys of a tile) takes the KV tiles t with t % 2 == k, with its own S buffer,
-// P buffer, running max / sum and O accumulator; the tensor core runs one
-// set's S / PV while the other exponentiates.  Three warpgroups: WG0 (warp 0
-// TMA + TMEM, warp 1 MMA) gives its registers to the two softmax warpgroups
-// (setmaxnreg 56 / 224), which hold the 128 scores of a row without spills.
-// TMEM: S[set] 128 columns each, O[unit parity][set] 64 columns each.
-constexpr int kFwd3Threads = 384;  // WG0: warp 0 TMA + TMEM, warp 1 MMA; WG1 / WG2: softmax sets
-constexpr int kFwd3Bars = 2 + 2 * kKV2Stages + 4 * 2 + 2;
-constexpr int kFwd3Smem = 1024 + kTileBytes * (1 + 2 * kKV2Stages) + 2 * kPBytes + kFwd3Bars * 8 + 16 +
-                          2 * 128 * 2 * 2 * 4;
-
-__global__ void __launch_bounds__(kFwd3Threads, 1)
-    attn_fwd3_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_kv,
-                     const AttnParams p) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kTileBytes;
-  uint8_t* sV = sK + kKV2Stages * kTileBytes;
-  uint8_t* sP = sV + kKV2Stages * kTileBytes;  // [set] 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 2 * kPBytes);
-  uint64_t* q_full = bars;
-  uint64_t* q_empty = bars + 1;
-  uint64_t* kv_full = bars + 2;
-  uint64_t* kv_empty = kv_full + kKV2Stages;
-  uint64_t* s_full = kv_empty + kKV2Stages;  // [set]
-  uint64_t* s_empty = s_full + 2;            // [set]
-  uint64_t* p_full = s_empty + 2;            // [set]
-  uint64_t* p_empty = p_full + 2;            // [set]
-  uint64_t* pv_done = p_empty + 2;           // [set]
-  uint64_t* o_empty = pv_done + 2;           // [unit parity]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kFwd3Bars);
-  float* xs = reinterpret_cast<float*>(tmem_slot + 4);  // [unit parity][128 rows][set][m, l]
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_kv_all = (p.kv_seq + kTile - 1) / kTile;
-  const int n_qt = (p.seq + kTile - 1) / kTile;
-  const long long bh = (long long)p.batch * p.heads;
-  const long long units = bh * n_qt;
-  auto decode = [&](long long u, int& qt, int& h, int& bb) {
-    int qi;
-    long long r;
-    if (p.causal) {
-      qi = (int)(u / bh);
-      r = u - (long long)qi * bh;
-    } else {
-      qi = (int)(u % n_qt);
-      r = u / n_qt;
-    }
-    qt = p.causal ? n_qt - 1 - qi : qi;
-    h = (int)(r % p.heads);
-    bb = (int)(r / p.heads);
-  };
-  auto kv_tiles = [&](int qt) { return p.causal ? min(n_kv_all, qt + 1) : n_kv_all; };
-  auto set_count = [&](long long g0, int n_kv, int k) {
-    const int first = ((g0 & 1) == k) ? 0 : 1;
-    return first < n_kv ? (n_kv - first + 1) / 2 : 0;
-  };
-
-  if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tm_q);
-    prefetch_tmap(&tm_kv);
-  }
-  if (warp == 1 && lane == 0) {
-    mbar_init(q_full, 1);
-    mbar_init(q_empty, 1);
-    for (int s = 0; s < kKV2Stages; ++s) {
-      mbar_init(&kv_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 4);  // the set's 4 softmax warps
-      mbar_init(&p_full[i], 4);
-      mbar_init(&p_empty[i], 1);
-      mbar_init(&pv_done[i], 1);
-      mbar_init(&o_empty[i], 8);  // every softmax warp reads both sets' O of the unit
-    }
-    fence_mbar_init();
-  }
-  if (warp == 0) tmem_alloc<512>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  pdl_wait();
-
-  if (warp == 0) {
-    regs_dec<56>();
-    if (lane == 0) {
-      long long g = 0;
-      int uc = 0;
-      for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-        int qt, h, bb;
-        decode(u, qt, h, bb);
-        const int n_kv = kv_tiles(qt), row0 = bb * p.seq, krow0 = bb * p.kv_seq;
-        mbar_wait(q_empty, (uc & 1) ^ 1);
-        mbar_expect_tx(q_full, kTileBytes);
-        tma_load_2d(sQ, &tm_q, q_full, p.q_col + h * kD, row0 + qt * kTile);
-        for (int j = 0; j < n_kv; ++j, ++g) {
-          const int st = (int)(g % kKV2Stages);
-          mbar_wait(&kv_empty[st], (int)((g / kKV2Stages) & 1) ^ 1);
-          mbar_expect_tx(&kv_full[st], 2 * kTileBytes);
-          tma_load_2d(sK + st * kTileBytes, &tm_kv, &kv_full[st], p.k_col + h * kD, krow0 + j * kTile);
-          tma_load_2d(sV + st * kTileBytes, &tm_kv, &kv_full[st], p.v_col + h * kD, krow0 + j * kTile);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    regs_dec<56>();
-    constexpr uint32_t idesc_s = idesc_bf16(128, 128, 0, 0);
-    constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);
-    struct Pending {
-      long long t;
-      int first, uc;
-    };
-    Pending pa{0, 0, 0}, pb{0, 0, 0};
-    int npend = 0;
-    auto issue_pv = [&](const Pending& d) {
-      const int i = (int)(d.t & 1), ub = d.uc & 1;
-      mbar_wait(&p_full[i], (int)((d.t >> 1) & 1));
-      if (d.first) mbar_wait(&o_empty[ub], ((d.uc >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (lane == 0) {
-        const int st = (int)(d.t % kKV2Stages);
-        const uint32_t pa_ = smem_u32(sP + i * kPBytes), vb = smem_u32(sV + st * kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kTile / 16; ++k) {
-          const uint64_t ad = smem_desc_sw128(pa_ + (k >> 2) * (kPBytes / 2) + (k & 3) * 32, 16, 1024);
-          const uint64_t bd = smem_desc_sw128(vb + k * 2048, kD * 128, 1024);
-          umma_bf16(tmem + 256 + ub * 128 + i * 64, ad, bd, idesc_o, (d.first && k == 0) ? 0u : 1u);
-        }
-        umma_commit(&p_empty[i]);
-        umma_commit(&kv_empty[st]);
-        umma_commit(&pv_done[i]);
-      }
-      __syncwarp();
-    };
-    long long g = 0;
-    int uc = 0;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-      int qt, h, bb;
-      decode(u, qt, h, bb);
-      const int n_kv = kv_tiles(qt);
-      mbar_wait(q_full, uc & 1);
-      for (int j = 0; j < n_kv; ++j) {
-        const long long t = g + j;
-        const int st = (int)(t % kKV2Stages), i = (int)(t & 1);
-        mbar_wait(&kv_full[st], (int)((t / kKV2Stages) & 1));
-        mbar_wait(&s_empty[i], (int)((t >> 1) & 1) ^ 1);
-        tc_fence_after();
-        if (lane == 0) {
-          const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + st * kTileBytes);
-#pragma unroll
-          for (int k = 0; k < kD / 16; ++k) {
-            const uint64_t ad = smem_desc_sw128(qa + k * 32, 16, 1024);
-            const uint64_t bd = smem_desc_sw128(kb + k * 32, 16, 1024);
-            umma_bf16(tmem + i * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
-          }
-          umma_commit(&s_full[i]);
-          if (j == n_kv - 1) umma_commit(q_empty);
-        }
-        __syncwarp();
-        const Pending d{t, j < 2 ? 1 : 0, uc};
-        if (npend == 2) {
-          issue_pv(pa);
-          pa = pb;
-          pb = d;
-        } else if (npend == 1) {
-          pb = d;
-          npend = 2;
-        } else {
-          pa = d;
-          npend = 1;
-        }
-      }
-      g += n_kv;
-    }
-    if (npend >= 1) issue_pv(pa);
-    if (npend == 2) issue_pv(pb);
-  } else if (warp >= 4) {
-    // ---------------- softmax: warps 4-11, set = (warp - 4) / 4 ----------------
-    regs_inc<224>();
-    const int set = (warp - 4) >> 2;
-    const int quarter = warp & 3;
-    const int r = quarter * 32 + lane;
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const float sl = p.scale_log2;
-    long long g = 0;
-    int uc = 0, tc_mine = 0, tc_other = 0;
-    for (long long u = blockIdx.x; u < units; u += gridDim.x, ++uc) {
-      int qt, h, bb;
-      decode(u, qt, h, bb);
-      const int n_kv = kv_tiles(qt), row0 = bb * p.seq, ub = uc & 1;
-      const int q = qt * kTile + r;
-      const int cnt0 = set_count(g, n_kv, 0), cnt1 = set_count(g, n_kv, 1);
-      const int cnt_other = set ? cnt0 : cnt1;
-      const uint32_t o_mine = tmem + 256 + ub * 128 + set * 64 + lane_off;
-      float ms = -INFINITY, l = 0.f;
-      const int j0 = ((g & 1) == set) ? 0 : 1;
-      for (int j = j0; j < n_kv; j += 2) {
-        const long long t = g + j;
-        const int i = set;
-        const int k0 = j * kTile;
-        const bool mask = (j + 1) * kTile > p.kv_seq || (p.causal && j == qt);
-        mbar_wait(&s_full[i], (int)((t >> 1) & 1));
-        tc_fence_after();
-        uint32_t sv[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tmem + i * 128 + c * 32 + lane_off, sv + c * 32);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&s_empty[i]);
-        if (mask) {
-#pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            const int key = k0 + c;
-            if (!(key < p.kv_seq && (!p.causal || key <= q))) sv[c] = __float_as_uint(-INFINITY);
-          }
-        }
-        float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-        for (int c = 0; c < 128; c += 4) {
-          m4[0] = fmaxf(m4[0], __uint_as_float(sv[c]));
-          m4[1] = fmaxf(m4[1], __uint_as_float(sv[c + 1]));
-          m4[2] = fmaxf(m4[2], __uint_as_float(sv[c + 2]));
-          m4[3] = fmaxf(m4[3], __uint_as_float(sv[c + 3]));
-        }
-        const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * sl;
-        float alpha = 1.f;
-        if (mx > ms + kRescaleLog2 || ms == -INFINITY) {
-          alpha = (ms == -INFINITY) ? 0.f : ex2(ms - mx);
-          ms = mx;
-        }
-        const float base = (ms == -INFINITY) ? 0.f : ms;
-        float2 sum2 = make_float2(0.f, 0.f);
-        mbar_wait(&p_empty[i], (int)((t >> 1) & 1) ^ 1);
-        uint8_t* pt = sP + i * kPBytes;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          float e8[8];
-#pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float2 a = fma2(make_float2(__uint_as_float(sv[c * 8 + e]), __uint_as_float(sv[c * 8 + e + 1])),
-                                  make_float2(sl, sl), make_float2(-base, -base));
-            const float2 ev = make_float2(ex2(a.x), ex2(a.y));
-            e8[e] = ev.x;
-            e8[e + 1] = ev.y;
-            sum2 = fma2(make_float2(1.f, 1.f), ev, sum2);
-          }
-          uint4 w;
-          w.x = pack_bf16(e8[0], e8[1]);
-          w.y = pack_bf16(e8[2], e8[3]);
-          w.z = pack_bf16(e8[4], e8[5]);
-          w.w = pack_bf16(e8[6], e8[7]);
-          sts128(smem_u32(pt) + (c >> 3) * (kPBytes / 2) + sw128(r, c & 7), w);
-        }
-        l = l * alpha + (sum2.x + sum2.y);
-        fence_async_smem();
-        if (j >= 2) {
-          mbar_wait(&pv_done[i], (tc_mine - 1) & 1);
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
-            tc_fence_after();
-            uint32_t ou[64];
-            tmem_ld_32x32b_x32(o_mine, ou);
-            tmem_ld_32x32b_x32(o_mine + 32, ou + 32);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < 64; ++e) ou[e] = __float_as_uint(__uint_as_float(ou[e]) * alpha);
-            tmem_st_32x32b_x32(o_mine, ou);
-            tmem_st_32x32b_x32(o_mine + 32, ou + 32);
-            tmem_st_wait();
-          }
-        }
-        tc_mine += 1;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[i]);
-      }
-      tc_other += cnt_other;
-      // ---- unit epilogue: combine the two sets ----
-      if (cnt0 > 0) mbar_wait(&pv_done[0], ((set ? tc_other : tc_mine) - 1) & 1);
-      if (cnt1 > 0) mbar_wait(&pv_done[1], ((set ? tc_mine : tc_other) - 1) & 1);
-      tc_fence_after();
-      float* xm = xs + (ub * 128 + r) * 4;
-      xm[set * 2] = ms;
-      xm[set * 2 + 1] = l;
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + quarter), "r"(64) : "memory");
-      const float m = fmaxf(xm[0], xm[2]);
-      const float a0 = xm[0] == -INFINITY ? 0.f : ex2(xm[0] - m);
-      const float a1 = xm[2] == -INFINITY ? 0.f : ex2(xm[2] - m);
-      const float lt = xm[1] * a0 + xm[3] * a1;
-      // this warp writes output columns 32 * set .. from both sets' accumulators
-      float o[32];
-#pragma unroll
-      for (int e = 0; e < 32; ++e) o[e] = 0.f;
-      if (cnt0 > 0) {
-        uint32_t oo[32];
-        tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + 0 * 64 + set * 32 + lane_off, oo);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] = __uint_as_float(oo[e]) * a0;
-      }
-      if (cnt1 > 0) {
-        uint32_t oo[32];
-        tmem_ld_32x32b_x32(tmem + 256 + ub * 128 + 1 * 64 + set * 32 + lane_off, oo);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) o[e] = fmaf(__uint_as_float(oo[e]), a1, o[e]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[ub]);
-      if (q < p.seq) {
-        const float inv = lt > 0.f ? 1.f / lt : 0.f;
-        __nv_bfloat16* op = p.out + (long long)(row0 + q) * p.H + h * kD + set * 32;
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          uint4 w;
-          w.x = pack_bf16(o[cc * 8 + 0] * inv, o[cc * 8 + 1] * inv);
-          w.y = pack_bf16(o[cc * 8 + 2] * inv, o[cc * 8 + 3] * inv);
-          w.z = pack_bf16(o[cc * 8 + 4] * inv, o[cc * 8 + 5] * inv);
-          w.w = pack_bf16(o[cc * 8 + 6] * inv, o[cc * 8 + 7] * inv);
-          reinterpret_cast<uint4*>(op)[cc] = w;
-        }
-        if (set == 0) p.lse[((long long)bb * p.heads + h) * p.seq + q] = (m + log2f(lt)) / kLog2e;
-      }
-      g += n_kv;
-    }
-  } else {
-    regs_dec<56>();
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_free<512>(tmem);
-  }
-}
+// Experimental forward kernels measured and removed (git history, commit
+// c58a59f and earlier): two softmax sets of 8 warps each owning alternate KV
+// tiles (106.9 vs 87.5 us at b32: 18 warps spill at 96 registers) and two sets
+// of whole-row warps with setmaxnreg (112.7 vs 85 us); DESIGN.md section 6.
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -1226,8 +522,7 @@ int map_2d_f32(CUtensorMap* map, const void* ptr, long long rows, long long cols
 // + 256 B of barriers / TMEM slot, then the per-unit (m, l) exchange [2][128][2][2] f32
 constexpr int kFwdSmem = 1024 + kTileBytes * (2 + 2 * kKVStages) + 2 * kPBytes + 256 + 1024 * 4;
 
-// Forward kernel choice: the single-set kernel unless DPN_ATTN_FWD=2 (the
-// two-set kernel, under validation; tools/attn_micro.py A/B).
+// Forward kernel choice (tools/attn_micro.py A/B).
 struct FwdKernel {
   void (*fn)(CUtensorMap, CUtensorMap, AttnParams);
   int threads, smem;
@@ -1235,14 +530,10 @@ struct FwdKernel {
 FwdKernel fwd_kernel() {
   static FwdKernel k = [] {
     const char* e = getenv("DPN_ATTN_FWD");
-#ifndef DPN_ATTN_FWD_DEFAULT
-#define DPN_ATTN_FWD_DEFAULT '1'
-#endif
-    const char v = e && e[0] ? e[0] : DPN_ATTN_FWD_DEFAULT;
-    FwdKernel r = v == '2'   ? FwdKernel{attn_fwd2_kernel, kFwd2Threads, kFwd2Smem}
-                  : v == '3' ? FwdKernel{attn_fwd3_kernel, kFwd3Threads, kFwd3Smem}
-                  : v == '4' ? FwdKernel{attn_fwd_kernel<4>, 128 + 128 * 4, kFwdSmem}
-                             : FwdKernel{attn_fwd_kernel<2>, kFwdThreads, kFwdSmem};
+    // DPN_ATTN_FWD=4: four key splits per row (16 softmax warps; measured 2x
+    // slower, kept for A/B), else two
+    FwdKernel r = (e && e[0] == '4') ? FwdKernel{attn_fwd_kernel<4>, 128 + 128 * 4, kFwdSmem}
+                                     : FwdKernel{attn_fwd_kernel<2>, kFwdThreads, kFwdSmem};
     cudaFuncSetAttribute(r.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, r.smem);
     return r;
   }();

@@ -460,4 +460,13 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// the same rounding (to nearest even) on the integer ALU for finite inputs:
+// an alternative to F2FP where the conversion pipe is the contended one
+__device__ __forceinline__ uint32_t pack_bf16_alu(float a, float b) {
+  uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+  ua += 0x7FFFu + ((ua >> 16) & 1u);
+  ub += 0x7FFFu + ((ub >> 16) & 1u);
+  return __byte_perm(ua, ub, 0x7632);
+}
+
 }  // namespace dpn
