@@ -39,7 +39,11 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // one 128-byte swizzle row of bf16
-constexpr int kEpiWarps = 8;  // two per SM sub-partition: each pair splits the columns
+#ifndef DPN_GEMM_EPI_WARPS
+#define DPN_GEMM_EPI_WARPS 8
+#endif
+constexpr int kEpiWarps = DPN_GEMM_EPI_WARPS;  // 8: two per SM sub-partition, each pair splits the columns
+constexpr int kEpiGroups = kEpiWarps / 4;      // warps sharing a TMEM lane quarter
 constexpr int kEpiWarp0 = 4;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);
 
@@ -327,7 +331,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
   if (p.c_f32) {
     constexpr int kChunks = BN / 32;
 #pragma unroll 1
-    for (int c = half; c < kChunks; c += 2) {
+    for (int c = half; c < kChunks; c += kEpiGroups) {
       const int col0 = n0 + c * 32;
       if (col0 >= p.N) break;
       uint32_t r[32];
@@ -356,7 +360,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
   const bool res = p.res != nullptr;
   const bool aux = p.gelu && p.aux != nullptr;
 #pragma unroll 1
-  for (int c = half; c < kChunks; c += 2) {
+  for (int c = half; c < kChunks; c += kEpiGroups) {
     const int col0 = n0 + c * 64;
     if (col0 >= p.N) break;
     float v[64];
@@ -411,7 +415,7 @@ __device__ __forceinline__ void epilogue_tile_tma(const GemmParams& p, const CUt
         }
       }
       __syncwarp();  // every lane has read the residual tile: prefetch the next chunk's
-      const int cn = c + 2;
+      const int cn = c + kEpiGroups;
       if (lane == 0 && cn < kChunks && n0 + cn * 64 < p.N) {
         mbar_expect_tx(rbar, kEpiStage);
         tma_load_2d_cta(s_side, tmR, rbar, n0 + cn * 64, row_base);
@@ -701,7 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const long long r_base = (long long)w.z1 * p.r_s1 + (long long)w.z2 * p.r_s2;
       const uint32_t taddr = tmem_base + acc * BN + ((uint32_t)lanes << 16);
 #pragma unroll 1
-      for (int c = half; c < BN / 32; c += 2) {
+      for (int c = half; c < BN / 32; c += kEpiGroups) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
