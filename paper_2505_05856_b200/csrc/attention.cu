@@ -560,17 +560,24 @@ FwdKernel fwd_kernel() {
 // D_i = rowsum(dO_i * O_i) comes from attn_bwd_prep.
 //
 // 512 threads, four warpgroups with re-balanced registers (setmaxnreg):
-//   WG0  warp 0 TMA (K/V once, Q/dO double-buffered), warp 1 MMA issuer,
+//   WG0  warp 0 TMA (K/V once, Q/dO in a 3-deep ring), warp 1 MMA issuer,
 //        warp 2 TMEM allocator                                    (56 regs)
 //   WG1-2 softmax: warp w owns rows 32*(w%4).. and key half (w-4)/4   (184 regs)
 //   WG3  dQ drain: TMEM dQ -> smem staging -> cp.reduce.async.bulk.tensor
 //        (.add), off the softmax critical path                    (88 regs)
 // MMA issue order per query tile: S/dP(i+1) as soon as the softmax holds
-// S/dP(i) in registers, then dV(i), dQ(i), dK(i).  dS is double-buffered in
-// smem, P single-buffered (stored last, after dV(i-1) released it).
+// S/dP(i) in registers, then dV(i), dQ(i), dK(i).  dS and P are single-buffered
+// in smem (P stored last, after dV(i-1) released it).
 namespace {
 
 constexpr int kBwdThreads = 512;
+// Q / dO ring depth: the load of query tile G+1's operands may start once
+// tile G+2-kQStages's MMAs ran (with 2 stages the TMA round trip was exposed
+// every iteration: the softmax warps waited ~half their time for S / dP);
+// the smem comes from single-buffering dS (its next write is ~a softmax pass
+// after the dQ / dK MMAs that read it were issued)
+constexpr int kQStages = 3;
+constexpr int kDSBufs = 1;
 
 struct AttnBwdParams {
   int batch, seq, heads, H;  // seq = query rows per sequence
@@ -601,22 +608,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   uint8_t* sK = smem;                     // [2] by unit parity: the next unit's K loads
                                           // during this one
   uint8_t* sV = sK + 2 * kTileBytes;      // released after the unit's last dP MMA
-  uint8_t* sQ = sV + kTileBytes;          // [2]
-  uint8_t* sdO = sQ + 2 * kTileBytes;     // [2]
-  uint8_t* sP = sdO + 2 * kTileBytes;     // 32 KB
-  uint8_t* sdS = sP + kPBytes;            // [2] 32 KB
-  uint8_t* sdQ = sdS + 2 * kPBytes;       // 16 KB f32 staging: one [128][32] SW128 box
+  uint8_t* sQ = sV + kTileBytes;          // [kQStages]
+  uint8_t* sdO = sQ + kQStages * kTileBytes;  // [kQStages]
+  uint8_t* sP = sdO + kQStages * kTileBytes;  // 32 KB
+  uint8_t* sdS = sP + kPBytes;            // [kDSBufs] 32 KB
+  uint8_t* sdQ = sdS + kDSBufs * kPBytes; // 16 KB f32 staging: one [128][32] SW128 box
   uint64_t* bars = reinterpret_cast<uint64_t*>(sdQ + kPBytes / 2);
   uint64_t* k_full = bars;        // [2]
   uint64_t* v_full = bars + 2;
-  uint64_t* q_full = bars + 3;    // [2]
-  uint64_t* q_empty = q_full + 2; // [2]
-  uint64_t* sp_full = q_empty + 2;
+  uint64_t* q_full = bars + 3;    // [kQStages]
+  uint64_t* q_empty = q_full + kQStages; // [kQStages]
+  uint64_t* sp_full = q_empty + kQStages;
   uint64_t* sp_loaded = sp_full + 1;
   uint64_t* p_empty = sp_loaded + 1;
-  uint64_t* ds_full = p_empty + 1;  // [2]
-  uint64_t* ds_empty = ds_full + 2; // [2]
-  uint64_t* dq_full = ds_empty + 2;  // [2] (dQ is double-buffered in TMEM)
+  uint64_t* ds_full = p_empty + 1;  // [kDSBufs]
+  uint64_t* ds_empty = ds_full + kDSBufs; // [kDSBufs]
+  uint64_t* dq_full = ds_empty + kDSBufs;  // [2] (dQ is double-buffered in TMEM)
   uint64_t* dq_empty = dq_full + 2;  // [2]
   uint64_t* dkv_full = dq_empty + 2;
   uint64_t* k_empty = dkv_full + 1;    // [2] K smem free for the unit after next
@@ -672,9 +679,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_init(v_empty, 1);
     mbar_init(sp_loaded, 8);
     mbar_init(p_empty, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kQStages; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&q_empty[s], 1);
+    }
+    for (int s = 0; s < kDSBufs; ++s) {
       mbar_init(&ds_full[s], 8);
       mbar_init(&ds_empty[s], 1);
     }
@@ -709,8 +718,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_expect_tx(v_full, kTileBytes);
         tma_load_2d(sV, &tm_kv, v_full, p.v_col + w.h * kD, w.krow0 + w.k0);
         for (int it = 0; it < w.n_it; ++it, ++G) {
-          const int st = G & 1, i = w.i0 + it;
-          mbar_wait(&q_empty[st], ((G >> 1) & 1) ^ 1);
+          const int st = G % kQStages, i = w.i0 + it;
+          mbar_wait(&q_empty[st], ((G / kQStages) & 1) ^ 1);
           mbar_expect_tx(&q_full[st], 2 * kTileBytes);
           tma_load_2d(sQ + st * kTileBytes, &tm_qkv, &q_full[st], p.q_col + w.h * kD, w.row0 + i * kTile);
           tma_load_2d(sdO + st * kTileBytes, &tm_do, &q_full[st], w.h * kD, w.row0 + i * kTile);
@@ -722,8 +731,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       constexpr uint32_t id_q = idesc_bf16(128, 64, 0, 1);    // dQ: dS K-major, K_j MN-major
       // S / dP of query iteration G against K[kbuf]; `last`: the unit's last use of V
       auto issue_sdp = [&](int G, int kbuf, bool last) {
-        const int st = G & 1;
-        mbar_wait(&q_full[st], (G >> 1) & 1);
+        const int st = G % kQStages;
+        mbar_wait(&q_full[st], (G / kQStages) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
@@ -751,12 +760,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // the previous unit's dV / dK must have been drained before this unit's first
         mbar_wait(dkv_empty, (uc & 1) ^ 1);
         for (int it = 0; it < w.n_it; ++it, ++G) {
-          const int st = G & 1, b = G & 1;
+          const int st = G % kQStages, b = G & 1, db = G % kDSBufs;
           mbar_wait(sp_loaded, G & 1);  // softmax holds S/dP(G) in registers
           if (it + 1 < w.n_it) issue_sdp(G + 1, kbuf, it + 2 == w.n_it);
-          mbar_wait(&ds_full[b], (G >> 1) & 1);
+          mbar_wait(&ds_full[db], (G / kDSBufs) & 1);
           tc_fence_after();
-          const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS + b * kPBytes);
+          const uint32_t pa = smem_u32(sP), dsa = smem_u32(sdS + db * kPBytes);
           const uint32_t qa = smem_u32(sQ + st * kTileBytes), doa = smem_u32(sdO + st * kTileBytes);
           const uint32_t kb = smem_u32(sK + kbuf * kTileBytes);
           if (lane == 0) {
@@ -785,7 +794,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               umma_bf16(tmem + 320, smem_desc_sw128(dsa + k * 2048, kPBytes / 2, 1024),
                         smem_desc_sw128(qa + k * 2048, kD * 128, 1024), id_kv,
                         (it > 0 || k > 0) ? 1u : 0u);
-            umma_commit(&ds_empty[b]);
+            umma_commit(&ds_empty[db]);
             umma_commit(&q_empty[st]);
           }
           __syncwarp();
@@ -829,7 +838,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const float Dq = d_next * sc;
         row_stats(it + 1, lse_next, d_next);
         const bool mask = !qok || k0 + kTile > p.kv_seq || (p.causal && i == kt);
-        const int pb = G & 1;
+        const int pb = G % kDSBufs;
         uint8_t* tdS = sdS + pb * kPBytes;
         mbar_wait(sp_full, G & 1);
         tc_fence_after();
@@ -842,7 +851,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(sp_loaded);  // the MMA may overwrite S/dP now
-        mbar_wait(&ds_empty[pb], ((G >> 1) & 1) ^ 1);
+        mbar_wait(&ds_empty[pb], ((G / kDSBufs) & 1) ^ 1);
         uint4 pk[8];  // P row chunk, packed bf16 (stored once dV(G-1) released sP)
         // the key mask only exists on boundary tiles: two straight-line copies
         auto tile = [&](auto masked) {
@@ -1075,7 +1084,7 @@ __global__ void __launch_bounds__(256 * kDqLanes) attn_dq_store_kernel(
   }
 }
 
-constexpr int kBwdSmem = 1024 + kTileBytes * 7 + 3 * kPBytes + kPBytes / 2 + 256;  // K[2] V Q[2] dO[2] | P dS[2] | dQ-staging
+constexpr int kBwdSmem = 1024 + kTileBytes * (3 + 2 * kQStages) + (1 + kDSBufs) * kPBytes + kPBytes / 2 + 256;  // K[2] V Q[] dO[] | P dS[] | dQ-staging
 
 }  // namespace
 }  // namespace dpn

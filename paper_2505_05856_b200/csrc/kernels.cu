@@ -738,23 +738,51 @@ __global__ void embed_fwd_kernel(const int* __restrict__ ids, const __nv_bfloat1
   }
 }
 
-__global__ void embed_bwd_kernel(const int* __restrict__ ids, const __nv_bfloat16* __restrict__ dout,
-                                 float* __restrict__ dtok, float* __restrict__ dpos,
-                                 long long rows, int seq, int hidden) {
+// Embedding backward: a warp owns one (position, batch slice): it walks the
+// slice's rows at that position, adds each row into its token's gradient row
+// with 16-byte vector reds, and sums the rows in registers so the position
+// gradient gets one vector red per slice (rows at one position no longer all
+// hit the same dpos row with scalar atomics).
+constexpr int kEmbSlices = 4;
+__global__ void __launch_bounds__(256) embed_bwd_kernel(const int* __restrict__ ids,
+                                                        const __nv_bfloat16* __restrict__ dout,
+                                                        float* __restrict__ dtok, float* __restrict__ dpos,
+                                                        long long rows, int seq, int hidden) {
   pdl_wait();
-  const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int nvec = hidden >> 3;
-  for (long long r = (long long)blockIdx.x * warps + (threadIdx.x >> 5); r < rows;
-       r += (long long)gridDim.x * warps) {
-    const long long id = ids[r];
-    const int sp = (int)(r % seq);
-    for (int c = lane; c < nvec; c += 32) {
-      float g[8];
-      load8(dout + r * hidden + c * 8, g);
+  const long long batches = rows / seq;
+  const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+  for (long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       w < (long long)seq * kEmbSlices; w += warps) {
+    const int sp = (int)(w % seq), sl = (int)(w / seq);
+    float acc[kMaxVec][8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        atomicAdd(&dtok[id * hidden + c * 8 + k], g[k]);
-        atomicAdd(&dpos[(long long)sp * hidden + c * 8 + k], g[k]);
+    for (int j = 0; j < kMaxVec; ++j)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc[j][k] = 0.f;
+    for (long long b = sl; b < batches; b += kEmbSlices) {
+      const long long r = b * seq + sp;
+      const long long id = ids[r];
+#pragma unroll
+      for (int j = 0; j < kMaxVec; ++j) {
+        const int c = lane + 32 * j;
+        if (c < nvec) {
+          float g[8];
+          load8(dout + r * hidden + c * 8, g);
+          red_add_v4(dtok + id * hidden + c * 8, g);
+          red_add_v4(dtok + id * hidden + c * 8 + 4, g + 4);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[j][k] += g[k];
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxVec; ++j) {
+      const int c = lane + 32 * j;
+      if (c < nvec) {
+        red_add_v4(dpos + (long long)sp * hidden + c * 8, acc[j]);
+        red_add_v4(dpos + (long long)sp * hidden + c * 8 + 4, acc[j] + 4);
       }
     }
   }
@@ -1012,9 +1040,11 @@ extern "C" int dpn_embed_fwd(const int32_t* ids, const void* tok, const void* po
 
 extern "C" int dpn_embed_bwd(const int32_t* ids, const void* dout, float* dtok, float* dpos,
                              int64_t rows, int64_t seq, int64_t hidden, void* stream) {
-  DPN_REQUIRE(hidden % 8 == 0, "hidden must be a multiple of 8");
+  DPN_REQUIRE(hidden % 8 == 0 && hidden <= 8 * 32 * kMaxVec, "hidden must be a multiple of 8, <= 2048");
+  DPN_REQUIRE(seq > 0 && rows % seq == 0, "rows must be a whole number of sequences");
+  DPN_REQUIRE(((uintptr_t)dtok & 15) == 0 && ((uintptr_t)dpos & 15) == 0, "dtok / dpos 16-byte alignment");
   if (rows == 0) return 0;
-  DPN_CHECK_CUDA(launch_pdl(embed_bwd_kernel, grid_for(rows, 8), 256, 0, (cudaStream_t)stream, 
+  DPN_CHECK_CUDA(launch_pdl(embed_bwd_kernel, grid_for(seq * kEmbSlices, 8), 256, 0, (cudaStream_t)stream, 
       ids, (const __nv_bfloat16*)dout, dtok, dpos, rows, (int)seq, (int)hidden));
   DPN_LAUNCH_CHECK();
   return 0;
