@@ -560,24 +560,23 @@ FwdKernel fwd_kernel() {
 // D_i = rowsum(dO_i * O_i) comes from attn_bwd_prep.
 //
 // 512 threads, four warpgroups with re-balanced registers (setmaxnreg):
-//   WG0  warp 0 TMA (K/V once, Q/dO in a 3-deep ring), warp 1 MMA issuer,
+//   WG0  warp 0 TMA (K/V once, Q/dO double-buffered), warp 1 MMA issuer,
 //        warp 2 TMEM allocator                                    (56 regs)
 //   WG1-2 softmax: warp w owns rows 32*(w%4).. and key half (w-4)/4   (184 regs)
 //   WG3  dQ drain: TMEM dQ -> smem staging -> cp.reduce.async.bulk.tensor
 //        (.add), off the softmax critical path                    (88 regs)
 // MMA issue order per query tile: S/dP(i+1) as soon as the softmax holds
-// S/dP(i) in registers, then dV(i), dQ(i), dK(i).  dS and P are single-buffered
-// in smem (P stored last, after dV(i-1) released it).
+// S/dP(i) in registers, then dV(i), dQ(i), dK(i).  dS is double-buffered in
+// smem, P single-buffered (stored last, after dV(i-1) released it).
 namespace {
 
 constexpr int kBwdThreads = 512;
-// Q / dO ring depth: the load of query tile G+1's operands may start once
-// tile G+2-kQStages's MMAs ran (with 2 stages the TMA round trip was exposed
-// every iteration: the softmax warps waited ~half their time for S / dP);
-// the smem comes from single-buffering dS (its next write is ~a softmax pass
-// after the dQ / dK MMAs that read it were issued)
-constexpr int kQStages = 3;
-constexpr int kDSBufs = 1;
+// Q / dO ring depth and dS buffers (smem allows 2 + 2 or 3 + 1).  The softmax
+// warps spend about half their time waiting for S / dP (ncu, profiles/
+// r02s3_final_ncu.md); a 3-deep Q / dO ring with a single dS buffer measured
+// slower (218.9 vs 215 us at b32), so the wait is not the Q / dO load.
+constexpr int kQStages = 2;
+constexpr int kDSBufs = 2;
 
 struct AttnBwdParams {
   int batch, seq, heads, H;  // seq = query rows per sequence
