@@ -201,7 +201,8 @@ def gemm_traffic():
     of the bench step (profiles/, cold-cache replay), else None."""
     import gzip
     import csv as _csv
-    for name in ("r02s3_launches_step_b64.csv.gz", "r02_launches_step.csv.gz", "r01_launches_step_b32.csv.gz"):
+    for name in ("r02s3final_launches_step_b64.csv.gz", "r02s3_launches_step_b64.csv.gz",
+                 "r02_launches_step.csv.gz", "r01_launches_step_b32.csv.gz"):
         p = ROOT / "profiles" / name
         if p.exists():
             break
