@@ -91,6 +91,9 @@ constexpr int kMaxSmem = 232448;  // 227 KB per CTA on sm_100
 #ifndef DPN_GEMM_GROUP
 #define DPN_GEMM_GROUP 8
 #endif
+#ifndef DPN_GEMM_COMMIT_PAIRS
+#define DPN_GEMM_COMMIT_PAIRS 0
+#endif
 #ifndef DPN_GEMM_HINT
 #define DPN_GEMM_HINT 0  // 1: A evict_first / B evict_last, 2: both evict_last (pair tiles)
 #endif
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // 1024 B apart (SBO); +16 rows * 128 B = 2048 B per K=16 step.
       constexpr uint32_t a_lbo = A_MN ? BK * 128 : 16, b_lbo = B_MN ? BK * 128 : 16;
       constexpr uint32_t a_kstep = A_MN ? 2048 : 32, b_kstep = B_MN ? 2048 : 32;
-      int stage = 0;
+      int stage = 0, prev_stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
@@ -639,16 +642,25 @@ __global__ void __launch_bounds__(kThreads, 1)
               if constexpr (CG >= 2) umma_bf16_pair(tmem_d, ad, bd, idesc, accum);
               else umma_bf16(tmem_d, ad, bd, idesc, accum);
             }
-            if constexpr (CG >= 2) {
-              // multicast: the stage is free only once both pairs consumed it
-              umma_commit_pair(&empty[stage], kMc ? 0xF : pair_mask);
-              if (kb == w.kb1 - 1) umma_commit_pair(&tfull[acc], pair_mask);
-            } else {
-              umma_commit(&empty[stage]);
-              if (kb == w.kb1 - 1) umma_commit(&tfull[acc]);
+            // DPN_GEMM_COMMIT_PAIRS: release smem stages two k-blocks at a time
+            // (one commit point per 8 MMAs instead of per 4)
+            const bool flush = !DPN_GEMM_COMMIT_PAIRS || ((kb - w.kb0) & 1) || kb == w.kb1 - 1;
+            const bool with_prev = DPN_GEMM_COMMIT_PAIRS && ((kb - w.kb0) & 1);
+            if (flush) {
+              if constexpr (CG >= 2) {
+                // multicast: the stage is free only once both pairs consumed it
+                if (with_prev) umma_commit_pair(&empty[prev_stage], kMc ? 0xF : pair_mask);
+                umma_commit_pair(&empty[stage], kMc ? 0xF : pair_mask);
+                if (kb == w.kb1 - 1) umma_commit_pair(&tfull[acc], pair_mask);
+              } else {
+                if (with_prev) umma_commit(&empty[prev_stage]);
+                umma_commit(&empty[stage]);
+                if (kb == w.kb1 - 1) umma_commit(&tfull[acc]);
+              }
             }
           }
           __syncwarp();
+          prev_stage = stage;
           if (++stage == C::kStages) {
             stage = 0;
             phase ^= 1;

@@ -6,7 +6,8 @@
 #   gpurun -- 'bash tools/ab_variants.sh base sus0'
 # Each variant runs twice, interleaved, through the GEMM, attention and
 # LayerNorm micro-benchmarks; JSON lines land in gpurun_out/ab/.
-# Knobs: DPN_GEMM_MAX_STAGES / DPN_GEMM_GROUP / DPN_GEMM_L2_PROMO / DPN_GEMM_HINT / DPN_GEMM_EPI_WARPS
+# Knobs: DPN_GEMM_MAX_STAGES / DPN_GEMM_GROUP / DPN_GEMM_L2_PROMO / DPN_GEMM_HINT / DPN_GEMM_EPI_WARPS /
+# DPN_GEMM_COMMIT_PAIRS
 # (gemm.cu), DPN_MBAR_SUSPEND_NS (common.cuh), DPN_ATTN_POLY / DPN_ATTN_POLY_BWD /
 # DPN_ATTN_PACK_ALU (attention.cu), DPN_LN_ROWS / DPN_LN_CTAS (kernels.cu).
 mkdir -p gpurun_out/ab
